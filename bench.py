@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark of the task-stream hot path (BASELINE.json metric on config C5).
+
+A step = one pass of the whole path over one batch of synthetic input:
+submit the C5 task stream (64 chained vector_scal sweeps over 16,384 tiles of
+a 4 GiB float32 vector; this rank's owner-computes share) through
+bt_insert_task_batch -> dependency inference + chain fusion -> pack + upload
+-> persistent scheduler kernel -> bt_task_wait_for_all.  Inputs are resident
+in HBM before the timed region (registered once, device-homed).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+Prints ONE JSON line on rank 0.  See DESIGN.md section "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "vector_scal effective HBM GB/s (frac of 8 TB/s) and tasks/s at 1/2/4/8 B200"
+NOMINAL_HBM_GBPS = 8000.0
+SM_COUNT = 148
+FP32_LANES_PER_SM = 128
+
+C5 = dict(nx=1 << 30, ntiles=16384, sweeps=64)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def workload_name(cfg):
+    return (f"C5: {cfg['nx']} float32 ({cfg['nx'] * 4 / 2**30:.0f} GiB), {cfg['ntiles']} tiles x "
+            f"{cfg['nx'] // cfg['ntiles']}, {cfg['sweeps']} chained vector_scal sweeps (sweep-major), "
+            f"owner-computes tiles")
+
+
+class ClockSampler:
+    """NVML clocks + throttle reasons sampled in a thread during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+
+
+def synth_tile_values(torch, n, seed, device):
+    """x in [1,2): 23 random mantissa bits (same recipe as workloads.unit_interval_floats)."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    bits = torch.randint(0, 1 << 23, (n,), dtype=torch.int32, device=device, generator=g) | 0x3F800000
+    return bits.view(torch.float32)
+
+
+def rank_tasks(np, handles, factors):
+    """This rank's task stream, sweep-major: for s: for t in my tiles: SCAL(f_s; t)."""
+    nt, ns = len(handles), len(factors)
+    codelets = np.full(nt * ns, 1, np.int32)
+    scalars = np.repeat(factors.astype(np.float32), nt)
+    h0 = np.tile(np.asarray(handles, np.uint64), ns)
+    return codelets, scalars, h0
+
+
+def run_reference(args):
+    """--impl reference: the sequential C oracle, timed on this host's cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+    import oracle
+    import workloads as W
+    cfg = dict(C5)
+    tile = cfg["nx"] // cfg["ntiles"]
+    sample_tiles = args.ref_tiles
+    rng = np.random.default_rng(W.SEED_BASE + 4)
+    f = W.sweep_factors(rng, cfg["sweeps"])
+    x = W.unit_interval_floats(np.random.default_rng(1), sample_tiles * tile)
+    p = W.sweep_program(x.shape[0], sample_tiles, f, x)
+    off0, len0, off1, len1 = oracle.model.resolve(p)
+    t = p.tasks
+    bufs = [x]
+
+    def step():
+        oracle.run_tasks(bufs, t["codelet"], t["scalar"], t["b0"], off0, len0, t["b1"], off1, len1)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    elems = sample_tiles * tile
+    value = 8.0 * elems / dt / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "tasks_per_s": sample_tiles * cfg["sweeps"] / dt,
+            "config": {"workload": workload_name(cfg), "sample": f"{sample_tiles} of {cfg['ntiles']} tiles, "
+                       f"all {cfg['sweeps']} sweeps, task-major"},
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{sample_tiles} tiles x {tile} floats x {cfg['sweeps']} sweeps "
+                                       f"({sample_tiles * cfg['sweeps']} tasks) per step"},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(np, seconds_target=12.0):
+    """The oracle as it stands, single thread, on a bounded sample of C5."""
+    import oracle
+    import workloads as W
+    tile = C5["nx"] // C5["ntiles"]
+    rng = np.random.default_rng(W.SEED_BASE + 4)
+    f = W.sweep_factors(rng, C5["sweeps"])
+    ntile = 64
+    x = W.unit_interval_floats(np.random.default_rng(2), ntile * tile)
+    p = W.sweep_program(x.shape[0], ntile, f, x)
+    off0, len0, off1, len1 = oracle.model.resolve(p)
+    t = p.tasks
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        oracle.run_tasks([x], t["codelet"], t["scalar"], t["b0"], off0, len0, t["b1"], off1, len1)
+        reps += 1
+        if time.perf_counter() - t0 > seconds_target:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": 8.0 * ntile * tile * reps / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"{reps} x ({ntile} tiles x {tile} floats x {C5['sweeps']} sweeps, task-major), "
+                      f"{dt:.1f} s single-threaded",
+            "tasks_per_s": reps * ntile * C5["sweeps"] / dt}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-fusion", action="store_true", help="unfused (scheduler-bound) variant")
+    ap.add_argument("--sweeps", type=int, default=C5["sweeps"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--ref-tiles", type=int, default=64)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_1304_0878_b200 import btask as B
+    import workloads as W
+
+    cfg = dict(C5, sweeps=args.sweeps)
+    T, S = cfg["ntiles"], cfg["sweeps"]
+    tile = cfg["nx"] // T
+    t_lo, t_hi = rank * T // world, (rank + 1) * T // world
+    my_tiles = t_hi - t_lo
+    elems = my_tiles * tile
+    factors = W.sweep_factors(np.random.default_rng(W.SEED_BASE + 4), S)
+
+    stream = torch.cuda.current_stream(dev)
+    flags = B.BT_FLAG_NO_FUSION if args.no_fusion else 0
+    rt = B.Runtime(device=local, stream=stream.cuda_stream, rank=0, nranks=1, flags=flags)
+
+    # ---- device-resident inputs (registered once, outside the timed region)
+    x = synth_tile_values(torch, elems, 1000 + rank, dev)
+    h = rt.register_tensor(x)
+    subs = rt.partition(h, my_tiles)
+    codelets, scalars, h0 = rank_tasks(np, subs, factors)
+    ntasks = codelets.shape[0]
+
+    def step():
+        rt.insert_batch(codelets, scalars, h0)
+        rt.wait()
+
+    for _ in range(args.warmup):
+        step()
+    rt.stats_reset()
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    st = rt.stats()
+    kern_ms = st["device_ms"] / max(1, st["epochs"])
+    host_ms = st["host_build_ms"] / args.steps
+    t = torch.tensor([ms, kern_ms, host_ms], device=dev, dtype=torch.float64)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, kern_ms_max, host_ms_max = t.tolist()
+
+    rt.unpartition(h)
+    rt.unregister(h)
+    del x
+    torch.cuda.empty_cache()
+
+    # ---- e2e: host (pinned) buffers through the public API, copies inside the region
+    e2e_ms = None
+    h2d = d2h = 0
+    if args.e2e_steps > 0:
+        addr, host = B.pinned_empty(elems * 4)
+        host[:] = synth_tile_values(torch, elems, 2000 + rank, dev).cpu().numpy()
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        rt.stats_reset()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            he = rt.register(addr, elems, 0)
+            se = rt.partition(he, my_tiles)
+            c2, s2, g2 = rank_tasks(np, se, factors)
+            rt.insert_batch(c2, s2, g2)
+            rt.wait()
+            rt.unpartition(he)
+            rt.unregister(he)                 # device -> host copy of the result
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
+        st2 = rt.stats()
+        h2d = elems * 4 + st2["upload_bytes"] // args.e2e_steps
+        d2h = elems * 4 + 64
+        te = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        if dist:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_ms = te.item()
+        B.bt_free(addr)
+    rt.close()
+
+    if rank == 0:
+        peaks, peak_src = load_peaks()
+        total_elems = cfg["nx"] * 1.0
+        compulsory = 8.0 * total_elems                     # read + write each element once per step
+        value = compulsory / (ms * 1e-3) / 1e9
+        clocks = clk.summary()
+        # roofline of the dominant kernel (the persistent scheduler kernel, one launch per step):
+        # fused chain of S multiplies per element -> FP32-multiply bound when S exceeds the ridge
+        per_launch_elems = elems                          # rank 0's launch
+        fmul = per_launch_elems * S
+        alu_peak = SM_COUNT * FP32_LANES_PER_SM * (peaks.get("sm_max_mhz") or 1965.0) * 1e6 / 1e12
+        hbm_bytes = 8.0 * per_launch_elems
+        t_alu = fmul / (alu_peak * 1e12)
+        t_hbm = hbm_bytes / (peaks["hbm_gbs"] * 1e9)
+        fused = not args.no_fusion
+        if fused and t_alu > t_hbm:
+            roof = {"bound": "alu", "achieved": fmul / (kern_ms * 1e-3) / 1e12, "peak": alu_peak,
+                    "unit": "TFMUL/s", "peak_source": f"{SM_COUNT} SMs x {FP32_LANES_PER_SM} FP32 lanes x "
+                                                     f"{peaks.get('sm_max_mhz')} MHz (DESIGN.md)"}
+        else:
+            b = hbm_bytes if fused else 8.0 * per_launch_elems * S
+            roof = {"bound": "hbm", "achieved": b / (kern_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                    "unit": "GB/s", "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["kernel"] = "bt::scheduler_kernel"
+        roof["kernel_ms"] = kern_ms
+        roof["hbm_GBps_physical_min"] = hbm_bytes / (kern_ms * 1e-3) / 1e9
+        roof["traffic"] = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+                tr = json.load(fh).get("c5_fused" if fused else "c5_unfused")
+                if tr and tr.get("elems_per_launch") == per_launch_elems:
+                    roof["traffic"] = tr["dram_bytes_per_launch"]
+        except OSError:
+            pass
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "frac_of_8TBps": value / NOMINAL_HBM_GBPS, "frac_of_measured_hbm": value / peaks["hbm_gbs"],
+            "tasks_per_s": ntasks * world / (ms * 1e-3),
+            "effective_unfused_GBps": 8.0 * total_elems * S / (ms * 1e-3) / 1e9,
+            "host_build_ms_per_step": host_ms_max, "kernel_ms_per_step": kern_ms_max,
+            "config": {"workload": workload_name(cfg), "tasks_per_step": ntasks * world,
+                       "fusion": fused, "parallelism": f"owner-computes tiles over {world} rank(s)",
+                       "l2": "4 GiB working set > 126 MB L2 (no flush needed)"},
+            "gpu_launches": int(st["epochs"]),
+            "clocks": clocks,
+            "roofline": roof,
+        }
+        if e2e_ms is not None:
+            line["e2e"] = {"value": compulsory / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
+                           "h2d_bytes_per_step": int(h2d * world), "d2h_bytes_per_step": int(d2h * world),
+                           "ms_per_step": e2e_ms, "path": "bt_malloc pinned host buffer -> register (H2D) -> "
+                           "partition -> insert_task_batch -> wait -> unregister (D2H)"}
+        if world == 1 and not args.skip_cpu:
+            line["cpu_baseline"] = cpu_baseline(np)
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

