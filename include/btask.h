@@ -94,6 +94,8 @@ typedef struct bt_config {
   uint32_t max_fused;     /* max SCAL tasks fused into one work item; 0 = default (256) */
   int ctas_per_sm;        /* persistent CTAs per SM; 0 = maximum occupancy */
   uint64_t epoch_tasks;   /* auto-flush an epoch after this many pending tasks; 0 = never */
+  int host_threads;       /* dependency-builder threads (parallel SCAL runs); 0 = min(16, cores) */
+  uint32_t parallel_min;  /* shortest SCAL run of a batch built in parallel; 0 = default (16384) */
 } bt_config;
 
 /* Fill *cfg with defaults.  Returns 0. */

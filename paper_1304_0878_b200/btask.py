@@ -30,7 +30,7 @@ class bt_config(ctypes.Structure):
     _fields_ = [("abi_version", ctypes.c_uint32), ("device", ctypes.c_int), ("stream", ctypes.c_void_p),
                 ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("flags", ctypes.c_uint32),
                 ("chunk_bytes", ctypes.c_uint32), ("max_fused", ctypes.c_uint32), ("ctas_per_sm", ctypes.c_int),
-                ("epoch_tasks", ctypes.c_uint64)]
+                ("epoch_tasks", ctypes.c_uint64), ("host_threads", ctypes.c_int), ("parallel_min", ctypes.c_uint32)]
 
 
 class bt_stats(ctypes.Structure):
@@ -111,13 +111,15 @@ class Runtime:
     """Pythonic wrapper over one bt_runtime (one GPU)."""
 
     def __init__(self, device: int = -1, stream=None, rank: int = 0, nranks: int = 1, flags: int = 0,
-                 chunk_bytes: int = 0, max_fused: int = 0, ctas_per_sm: int = 0, epoch_tasks: int = 0):
+                 chunk_bytes: int = 0, max_fused: int = 0, ctas_per_sm: int = 0, epoch_tasks: int = 0,
+                 host_threads: int = 0, parallel_min: int = 0):
         cfg = bt_config()
         bt_config_init(ctypes.byref(cfg))
         cfg.device, cfg.rank, cfg.nranks, cfg.flags = device, rank, nranks, flags
         cfg.stream = stream
         cfg.chunk_bytes, cfg.max_fused, cfg.ctas_per_sm, cfg.epoch_tasks = chunk_bytes, max_fused, ctas_per_sm, \
             epoch_tasks
+        cfg.host_threads, cfg.parallel_min = host_threads, parallel_min
         h = ctypes.c_void_p()
         rc = bt_init(ctypes.byref(cfg), ctypes.byref(h))
         if rc:

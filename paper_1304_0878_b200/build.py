@@ -14,14 +14,14 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libbtask.so")
 SOURCES = ["scheduler.cu", "runtime.cpp", "builder.cpp"]
-HEADERS = ["device_abi.h", "builder.hpp"]
+HEADERS = ["device_abi.h", "builder.hpp", "pool.hpp"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-fmad=false",                 # no FFMA contraction: bit-exact AXPY (R14)
     "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
-    "-Xcompiler", "-fPIC,-O2,-fno-fast-math,-Wall",
+    "-Xcompiler", "-fPIC,-O2,-fno-fast-math,-Wall,-pthread",
     "-Xptxas", "-warn-spills",
     "--cudart", "static",
     "-shared",

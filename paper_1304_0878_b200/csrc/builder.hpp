@@ -10,67 +10,94 @@
 //                   then writers = {T}, readers = {}
 //   access R only : readers += {T}
 // Partition copies the parent's state into every part; unpartition sets the
-// parent's state to the union of its parts' states (reading R9) -- so no
-// barrier task is needed and tiles stay independent.
+// parent's state to the union of its parts' states (reading R9) -- no barrier
+// task is needed and tiles stay independent.
 //
 // Vertical fusion (BASELINE north_star: "a fused pass over consecutive inout
-// scalings of the same tile"): a SCAL(RW) whose only predecessor is the
+// scalings of the same tile"): a SCAL(RW) whose only predecessor would be the
 // current single writer W of its handle, where W is a SCAL item of this epoch
 // on the same handle with no successor yet, is appended to W's factor list
-// instead of becoming a new item.  Factor lists are stored as a trie of
-// (parent, factor) nodes so that the tiles of a sweep-major stream share one
-// list (C5: 16,384 items, one 64-factor list).
+// instead of becoming a new item.  The factors stay in submission order; the
+// device applies them one rounding at a time.
+//
+// Two insertion paths produce identical DAGs up to item numbering:
+//  * sequential (any codelet): add_scal / add_task;
+//  * parallel lanes for long runs of SCAL tasks: a SCAL touches one handle,
+//    so the stream decomposes by handle.  Lane p owns the handles with
+//    slot % P == p, processes their tasks in submission order into
+//    lane-local items ("tagged" ids, bit 31), then merge() renumbers them
+//    into the global item array.
 #pragma once
 #include <stdint.h>
+#include <string.h>
 
+#include <atomic>
 #include <vector>
 
 namespace bt {
 
 constexpr uint32_t NONE = 0xFFFFFFFFu;
+constexpr uint32_t TAG = 0x80000000u;     // lane-local item id / lane-local factor offset
 
+// Per leaf (sub)handle.  12 bytes; multi-writer / reader sets live in exts.
 struct DepState {
-  uint32_t epoch = NONE;           // states of older epochs are empty
-  uint32_t writer = NONE;          // single latest writer (common case)
-  std::vector<uint32_t> writers;   // >1 latest writers (after unpartition)
+  uint32_t epoch = NONE;   // states of older epochs are empty
+  uint32_t writer = NONE;  // single latest writer (common case)
+  uint32_t ext = NONE;     // index into Builder::exts, or NONE
+};
+
+struct DepExt {
+  std::vector<uint32_t> writers;  // >1 latest writers (after unpartition)
   std::vector<uint32_t> readers;
-  void reset(uint32_t e) {
-    epoch = e;
-    writer = NONE;
-    writers.clear();
-    readers.clear();
-  }
 };
 
 struct HItem {
-  uint32_t kind;
+  uint32_t kind;       // 1 SCAL, 2 AXPY, 3 COPY
   uint32_t k;          // tasks in this item
   uint32_t slot0, slot1;
   uint64_t x, y, n;    // device addresses / elements
-  uint32_t arg;        // AXPY scalar bits; SCAL: trie node of the factor list
+  uint32_t arg;        // AXPY: scalar bits
+  uint32_t fofs;       // SCAL: factor offset in the factor pool (TAG: lane pool)
+  uint32_t fcap;       // SCAL: reserved factors at fofs
   uint32_t npred;
-  uint32_t nsucc;
-  uint32_t stamp;      // dedupe marker (id of the item being built)
+  uint32_t nsucc;      // updated atomically by lanes for shared predecessors
+  uint32_t stamp;      // dedupe marker (sequential path)
 };
 
-struct TrieNode {
-  uint32_t parent;
-  uint32_t fbits;
-  uint32_t child;      // first child created (memo), NONE if none
-  uint32_t child_fbits;
-};
-
-struct Access {
+struct LaneEntry {
   uint32_t slot;
-  uint32_t mode;       // BT_R | BT_W bits
+  uint32_t fbits;
+  uint32_t task;       // epoch task index
+  uint32_t pad;
+};
+
+struct alignas(64) Lane {
+  std::vector<HItem> items;
+  std::vector<uint64_t> edges;        // (pred << 32) | succ, ids possibly TAGged
+  std::vector<float> fpool;
+  std::vector<uint32_t> touched;      // slots whose state now holds a tagged id
+  std::vector<uint32_t> relocated;    // global items whose factors moved to fpool
+  std::vector<uint64_t> recorded;     // (task << 32) | tagged item (record_tasks)
+  uint64_t fused = 0;
+  char pad_[64];                      // keep neighbouring lanes off this cache line
+  void clear() {
+    items.clear();
+    edges.clear();
+    fpool.clear();
+    touched.clear();
+    relocated.clear();
+    recorded.clear();
+    fused = 0;
+  }
 };
 
 class Builder {
  public:
   // Epoch-scoped outputs
   std::vector<HItem> items;
-  std::vector<uint64_t> edges;      // (pred << 32) | succ, in creation order
-  std::vector<TrieNode> nodes;      // factor trie; node 0 is the root
+  std::vector<uint64_t> edges;      // (pred << 32) | succ
+  std::vector<float> fpool;         // factor lists of SCAL items
+  std::vector<DepExt> exts;
   std::vector<uint32_t> task_item;  // per epoch task (only if record_tasks)
   std::vector<uint32_t> task_pos;
   uint64_t ntasks = 0;              // tasks of this epoch (local or not)
@@ -80,130 +107,128 @@ class Builder {
   uint32_t max_fused = 256;
   uint32_t epoch = 0;
 
-  Builder() { clear(); }
-
   void clear() {
     items.clear();
     edges.clear();
-    nodes.clear();
-    nodes.push_back(TrieNode{NONE, 0, NONE, 0});
+    fpool.clear();
+    exts.clear();
     task_item.clear();
     task_pos.clear();
     ntasks = 0;
     fused = 0;
   }
-
   void next_epoch() {
     clear();
     ++epoch;
   }
 
-  // Record a task executed on another rank (kept for the task->item map).
-  void add_remote() {
+  void record(uint32_t item, uint32_t pos) {
     if (record_tasks) {
-      task_item.push_back(NONE);
-      task_pos.push_back(0);
+      task_item.push_back(item);
+      task_pos.push_back(pos);
     }
+  }
+
+  // A task executed on another rank (kept for the task -> item map).
+  void add_remote() {
+    record(NONE, 0);
     ++ntasks;
   }
 
+  // ---- sequential path ------------------------------------------------
   // SCAL(f; x:RW) on leaf slot s (x = device address of element 0, n elems).
   void add_scal(DepState &st, uint32_t s, uint64_t x, uint64_t n, uint32_t fbits) {
     fresh(st);
-    if (fusion && st.readers.empty() && st.writers.empty() && st.writer != NONE) {
+    ++ntasks;
+    if (fusion && st.ext == NONE && st.writer != NONE) {
       HItem &w = items[st.writer];
       if (w.kind == 1 && w.slot0 == s && w.nsucc == 0 && w.k < max_fused) {
-        w.arg = child(w.arg, fbits);
-        if (record_tasks) {
-          task_item.push_back(st.writer);
-          task_pos.push_back(w.k);
-        }
-        ++w.k;
+        append_factor(w, fbits);
+        record(st.writer, w.k - 1);
         ++fused;
-        ++ntasks;
         return;
       }
     }
-    const uint32_t t = new_item(1, s, NONE, x, 0, n, child(0, fbits));
-    depend_write(st, t);
+    const uint32_t t = new_item(1, s, NONE, x, 0, n, 0);
+    HItem &it = items[t];
+    it.fofs = (uint32_t)fpool.size();
+    it.fcap = 4;
+    fpool.resize(fpool.size() + 4);
+    memcpy(&fpool[it.fofs], &fbits, 4);
+    collect(st, t, 3u);
     st.writer = t;
+    st.ext = NONE;
   }
 
-  // Generic task with up to two accesses (AXPY: x R, y RW; COPY: x R, y W).
-  void add_task(uint32_t kind, DepState *st0, const Access &a0, DepState *st1, const Access &a1, uint64_t x,
-                uint64_t y, uint64_t n, uint32_t arg) {
+  // Generic task with two accesses (AXPY: x R, y RW; COPY: x R, y W).
+  void add_task(uint32_t kind, DepState *st0, uint32_t s0, uint32_t m0, DepState *st1, uint32_t s1, uint32_t m1,
+                uint64_t x, uint64_t y, uint64_t n, uint32_t arg) {
     fresh(*st0);
     if (st1 != st0) fresh(*st1);
-    const uint32_t t = new_item(kind, a0.slot, a1.slot, x, y, n, arg);
+    ++ntasks;
+    const uint32_t t = new_item(kind, s0, s1, x, y, n, arg);
     if (st1 == st0) {  // same handle twice: modes OR-ed (reading R6)
-      const uint32_t m = a0.mode | a1.mode;
-      apply(*st0, t, m);
+      const uint32_t m = m0 | m1;
+      collect(*st0, t, m);
+      update(*st0, t, m);
     } else {
-      // collect all predecessors first, then update the states
-      collect(*st0, t, a0.mode);
-      collect(*st1, t, a1.mode);
-      update(*st0, t, a0.mode);
-      update(*st1, t, a1.mode);
+      collect(*st0, t, m0);
+      collect(*st1, t, m1);
+      update(*st0, t, m0);
+      update(*st1, t, m1);
     }
   }
 
   // Partition: every part inherits the parent's state (reading R9).
-  void partition_state(DepState &parent, DepState *parts, uint32_t nparts) {
-    fresh(parent);
-    for (uint32_t i = 0; i < nparts; ++i) {
-      DepState &c = parts[i];
-      c.reset(epoch);
-      c.writer = parent.writer;
-      c.writers = parent.writers;
-      c.readers = parent.readers;
-    }
-  }
-
+  void partition_state(DepState &parent, DepState *parts, uint32_t nparts);
   // Unpartition: the parent's writers/readers are the union over the parts.
-  void unpartition_state(DepState &parent, DepState *parts, uint32_t nparts) {
-    parent.reset(epoch);
-    std::vector<uint32_t> w, r;
-    for (uint32_t i = 0; i < nparts; ++i) {
-      DepState &c = parts[i];
-      if (c.epoch != epoch) continue;
-      if (c.writer != NONE) w.push_back(c.writer);
-      w.insert(w.end(), c.writers.begin(), c.writers.end());
-      r.insert(r.end(), c.readers.begin(), c.readers.end());
-    }
-    dedupe(w);
-    dedupe(r);
-    if (w.size() == 1) parent.writer = w[0];
-    else parent.writers = std::move(w);
-    parent.readers = std::move(r);
-  }
+  void unpartition_state(DepState &parent, DepState *parts, uint32_t nparts);
+
+  // ---- parallel lanes (SCAL runs) -------------------------------------
+  // Process one SCAL on slot e.slot owned by this lane (no other thread
+  // touches deps[e.slot] or the SCAL items whose slot0 is e.slot).
+  void lane_scal(Lane &L, DepState &st, const LaneEntry &e, uint64_t x, uint64_t n);
+  // Renumber lane items into the global arrays; deps[] of touched slots fixed.
+  // Runs lane p's share on worker p via `par` (a fork/join runner).
+  template <class Par>
+  void merge(std::vector<Lane> &lanes, DepState *deps, Par &&par);
+
+  const float *factors(const HItem &it) const { return &fpool[it.fofs]; }
 
  private:
   void fresh(DepState &st) {
-    if (st.epoch != epoch) st.reset(epoch);
+    if (st.epoch != epoch) {
+      st.epoch = epoch;
+      st.writer = NONE;
+      st.ext = NONE;
+    }
   }
 
-  static void dedupe(std::vector<uint32_t> &v);
-
-  uint32_t child(uint32_t parent, uint32_t fbits) {
-    TrieNode &p = nodes[parent];
-    if (p.child != NONE && p.child_fbits == fbits) return p.child;
-    const uint32_t id = (uint32_t)nodes.size();
-    if (p.child == NONE) {
-      p.child = id;
-      p.child_fbits = fbits;
+  DepExt &ext_of(DepState &st) {
+    if (st.ext == NONE) {
+      st.ext = (uint32_t)exts.size();
+      exts.emplace_back();
     }
-    nodes.push_back(TrieNode{parent, fbits, NONE, 0});
-    return id;
+    return exts[st.ext];
+  }
+
+  void append_factor(HItem &w, uint32_t fbits) {
+    if (w.k == w.fcap) {
+      const uint32_t cap = w.fcap * 2;
+      const uint32_t ofs = (uint32_t)fpool.size();
+      fpool.resize(fpool.size() + cap);
+      memmove(&fpool[ofs], &fpool[w.fofs], 4ull * w.k);
+      w.fofs = ofs;
+      w.fcap = cap;
+    }
+    memcpy(&fpool[w.fofs + w.k], &fbits, 4);
+    ++w.k;
   }
 
   uint32_t new_item(uint32_t kind, uint32_t s0, uint32_t s1, uint64_t x, uint64_t y, uint64_t n, uint32_t arg) {
     const uint32_t t = (uint32_t)items.size();
-    items.push_back(HItem{kind, 1, s0, s1, x, y, n, arg, 0, 0, NONE});
-    if (record_tasks) {
-      task_item.push_back(t);
-      task_pos.push_back(0);
-    }
-    ++ntasks;
+    items.push_back(HItem{kind, 1, s0, s1, x, y, n, arg, 0, 0, 0, 0, NONE});
+    record(t, 0);
     return t;
   }
 
@@ -218,31 +243,63 @@ class Builder {
 
   void collect(DepState &st, uint32_t t, uint32_t mode) {
     if (st.writer != NONE) edge(st.writer, t);
-    for (uint32_t w : st.writers) edge(w, t);
-    if (mode & 2u)
-      for (uint32_t r : st.readers) edge(r, t);
+    if (st.ext != NONE) {
+      const DepExt &e = exts[st.ext];
+      for (uint32_t w : e.writers) edge(w, t);
+      if (mode & 2u)
+        for (uint32_t r : e.readers) edge(r, t);
+    }
   }
 
   void update(DepState &st, uint32_t t, uint32_t mode) {
     if (mode & 2u) {
       st.writer = t;
-      st.writers.clear();
-      st.readers.clear();
+      st.ext = NONE;           // the DepExt entry is simply dropped
     } else {
-      st.readers.push_back(t);
+      ext_of(st).readers.push_back(t);
     }
   }
-
-  void apply(DepState &st, uint32_t t, uint32_t mode) {
-    collect(st, t, mode);
-    update(st, t, mode);
-  }
-
-  void depend_write(DepState &st, uint32_t t) {
-    collect(st, t, 3u);
-    st.writers.clear();
-    st.readers.clear();
-  }
 };
+
+// ---------------------------------------------------------------- merge --
+template <class Par>
+void Builder::merge(std::vector<Lane> &lanes, DepState *deps, Par &&par) {
+  const size_t P = lanes.size();
+  std::vector<uint32_t> ibase(P), fbase(P);
+  std::vector<size_t> ebase(P);
+  size_t ni = items.size(), nf = fpool.size(), ne = edges.size();
+  for (size_t p = 0; p < P; ++p) {
+    ibase[p] = (uint32_t)ni;
+    fbase[p] = (uint32_t)nf;
+    ebase[p] = ne;
+    ni += lanes[p].items.size();
+    nf += lanes[p].fpool.size();
+    ne += lanes[p].edges.size();
+    fused += lanes[p].fused;
+  }
+  items.resize(ni);
+  fpool.resize(nf);
+  edges.resize(ne);
+  par([&](int p) {
+    Lane &L = lanes[p];
+    const uint32_t ib = ibase[p], fb = fbase[p];
+    auto fix = [ib](uint32_t id) { return (id & TAG) && id != NONE ? ib + (id & ~TAG) : id; };
+    if (!L.fpool.empty()) memcpy(&fpool[fb], L.fpool.data(), 4 * L.fpool.size());
+    for (size_t j = 0; j < L.items.size(); ++j) {
+      HItem it = L.items[j];
+      if (it.fofs & TAG) it.fofs = fb + (it.fofs & ~TAG);
+      items[ib + j] = it;
+    }
+    for (uint32_t w : L.relocated) items[w].fofs = fb + (items[w].fofs & ~TAG);
+    uint64_t *E = edges.data() + ebase[p];
+    for (size_t j = 0; j < L.edges.size(); ++j) {
+      const uint64_t e = L.edges[j];
+      E[j] = ((uint64_t)fix((uint32_t)(e >> 32)) << 32) | fix((uint32_t)e);
+    }
+    for (uint32_t s : L.touched) deps[s].writer = fix(deps[s].writer);
+    if (record_tasks)
+      for (uint64_t r : L.recorded) task_item[r >> 32] = fix((uint32_t)r);
+  });
+}
 
 }  // namespace bt

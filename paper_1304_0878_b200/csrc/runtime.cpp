@@ -10,18 +10,22 @@
 #include <errno.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
 #include <chrono>
 #include <map>
+#include <memory>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
 #include "../../include/btask.h"
 #include "builder.hpp"
 #include "device_abi.h"
+#include "pool.hpp"
 
 namespace bt {
 cudaError_t launch_epoch(const EpochArgs &args, int grid, cudaStream_t stream);
@@ -33,9 +37,13 @@ using namespace bt;
 
 namespace {
 
-constexpr uint32_t kDefaultChunkBytes = 256u << 10;
+constexpr uint32_t kMaxChunkBytes = 256u << 10;     // adaptive chunking: upper bound
+constexpr uint64_t kMinChunkElems = 2048;           // adaptive chunking: lower bound (8 KiB)
+constexpr uint32_t kUnitsPerCta = 64;               // adaptive chunking: target work units per CTA
 constexpr uint32_t kDefaultMaxFused = 256;
+constexpr uint32_t kDefaultParallelMin = 16384;
 constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;   // 20 s
+constexpr size_t kParallelPack = 1u << 15;          // items above which the pack runs on the pool
 
 const char *codelet_name(int c) {
   switch (c) {
@@ -51,21 +59,28 @@ double now_ms() {
   return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
 }
 
-struct Slot {
+enum : uint32_t { F_LIVE = 1, F_PARTITIONED = 2, F_BLOCKED = 4 };
+
+// Hot per-(sub)handle fields read on every insert (32 bytes).
+struct SlotHot {
   uint32_t gen = 1;
-  bool live = false;
+  uint32_t flags = 0;
+  int32_t rank = 0;
+  uint32_t pad = 0;
+  float *dptr = nullptr;      // device address of element 0 (null: no local storage)
+  uint64_t nx = 0;
+};
+
+struct Slot {
   uint32_t parent = NONE;
   uint32_t child_index = 0;
   uint32_t nparts = 0;        // partitioned into nparts children if > 0
   uint32_t first_child = NONE;
   uint32_t root = NONE;       // top-level ancestor (itself for a top-level handle)
-  float *dptr = nullptr;      // device address of element 0 (null: no local storage)
-  uint64_t nx = 0;
   uint64_t offset = 0;        // element offset inside the root
   void *hptr = nullptr;       // root only: registered pointer
   int home_node = 0;
-  int rank = 0;
-  int acquired = 0;           // 0, BT_R or BT_RW
+  int acquired = 0;           // 0, BT_R or BT_RW (on the acquired handle itself)
   bool owns_dev = false;      // root only: runtime-allocated replica
 };
 
@@ -93,18 +108,21 @@ struct bt_runtime {
   int sms = 0;
   int grid_max = 0;
   int block = 0;
-  uint64_t chunk_elems = 0;
   int poisoned = 0;
   std::string last_error;
 
+  std::vector<SlotHot> hot;
   std::vector<Slot> slots;
   std::vector<DepState> deps;
-  std::map<uint32_t, std::vector<uint32_t>> free_ranges;   // count -> starts
-  std::map<uintptr_t, std::pair<uintptr_t, uint32_t>> ranges;  // start -> (end, root slot)
-  std::unordered_map<uintptr_t, uint32_t> by_ptr;          // exact base -> root slot
+  std::map<uint32_t, std::vector<uint32_t>> free_ranges;        // count -> starts
+  std::map<uintptr_t, std::pair<uintptr_t, uint32_t>> ranges;   // start -> (end, root slot)
+  std::unordered_map<uintptr_t, uint32_t> by_ptr;               // exact base -> root slot
   uint32_t live_roots = 0;
 
   Builder builder;
+  std::unique_ptr<Pool> pool;
+  std::vector<Lane> lanes;
+  std::vector<std::vector<LaneEntry>> buckets;                  // [chunk * P + lane]
   EpochBuf ep[2];
   int ep_cur = 0;
   bt_stats stats{};
@@ -119,8 +137,13 @@ struct bt_runtime {
   std::vector<uint32_t> trace_item;
 
   // pack scratch
-  std::vector<uint32_t> cursor, node_off, csr_off;
-  std::vector<uint8_t> node_written;
+  std::vector<uint32_t> succ_off, cursor;
+
+  template <class F>
+  void par(F &&f) {
+    std::function<void(int)> fn = f;
+    pool->run(fn);
+  }
 };
 
 namespace {
@@ -146,23 +169,23 @@ int cuda_fail(bt_runtime *rt, cudaError_t e, const char *what) {
   return fail(rt, -EIO, "%s: %s", what, cudaGetErrorString(e));
 }
 
-#define CUDA_TRY(rt, call)                                   \
-  do {                                                       \
-    cudaError_t e_ = (call);                                 \
+#define CUDA_TRY(rt, call)                                    \
+  do {                                                        \
+    cudaError_t e_ = (call);                                  \
     if (e_ != cudaSuccess) return cuda_fail((rt), e_, #call); \
   } while (0)
 
 inline bt_handle make_handle(const bt_runtime *rt, uint32_t s) {
-  return ((uint64_t)rt->slots[s].gen << 32) | (uint64_t)(s + 1);
+  return ((uint64_t)rt->hot[s].gen << 32) | (uint64_t)(s + 1);
 }
 
 // Resolve a handle to a live slot, or NONE.
 inline uint32_t resolve(const bt_runtime *rt, bt_handle h) {
   const uint64_t idx = (h & 0xFFFFFFFFull);
-  if (idx == 0 || idx > rt->slots.size()) return NONE;
+  if (idx == 0 || idx > rt->hot.size()) return NONE;
   const uint32_t s = (uint32_t)(idx - 1);
-  const Slot &sl = rt->slots[s];
-  if (!sl.live || sl.gen != (uint32_t)(h >> 32)) return NONE;
+  const SlotHot &sh = rt->hot[s];
+  if (!(sh.flags & F_LIVE) || sh.gen != (uint32_t)(h >> 32)) return NONE;
   return s;
 }
 
@@ -173,35 +196,56 @@ uint32_t alloc_slots(bt_runtime *rt, uint32_t count) {
     s = it->second.back();
     it->second.pop_back();
   } else {
-    s = (uint32_t)rt->slots.size();
+    s = (uint32_t)rt->hot.size();
+    rt->hot.resize(s + count);
     rt->slots.resize(s + count);
     rt->deps.resize(s + count);
   }
   for (uint32_t i = 0; i < count; ++i) {
-    Slot &sl = rt->slots[s + i];
-    const uint32_t gen = sl.gen;
-    sl = Slot();
-    sl.gen = gen;
-    sl.live = true;
-    rt->deps[s + i].epoch = NONE;
+    SlotHot &h = rt->hot[s + i];
+    const uint32_t gen = h.gen;
+    h = SlotHot();
+    h.gen = gen;
+    h.flags = F_LIVE;
+    rt->slots[s + i] = Slot();
+    rt->deps[s + i] = DepState();
   }
   return s;
 }
 
 void free_slots(bt_runtime *rt, uint32_t s, uint32_t count) {
   for (uint32_t i = 0; i < count; ++i) {
-    Slot &sl = rt->slots[s + i];
-    sl.live = false;
-    ++sl.gen;
-    if (sl.gen == 0) sl.gen = 1;
+    SlotHot &h = rt->hot[s + i];
+    h.flags = 0;
+    if (++h.gen == 0) h.gen = 1;
     rt->deps[s + i] = DepState();
   }
   rt->free_ranges[count].push_back(s);
 }
 
+void set_blocked(bt_runtime *rt, uint32_t s, bool on) {
+  std::vector<uint32_t> stack{s};
+  while (!stack.empty()) {
+    const uint32_t x = stack.back();
+    stack.pop_back();
+    if (on) rt->hot[x].flags |= F_BLOCKED;
+    else rt->hot[x].flags &= ~F_BLOCKED;
+    const Slot &sl = rt->slots[x];
+    for (uint32_t t = 0; t < sl.nparts; ++t) stack.push_back(sl.first_child + t);
+  }
+}
+
 bool acquired_chain(const bt_runtime *rt, uint32_t s) {
-  for (uint32_t p = s; p != NONE; p = rt->slots[p].parent)
-    if (rt->slots[p].acquired) return true;
+  if (rt->hot[s].flags & F_BLOCKED) return true;
+  // a descendant acquired also blocks partition/acquire of s
+  std::vector<uint32_t> stack{s};
+  while (!stack.empty()) {
+    const uint32_t x = stack.back();
+    stack.pop_back();
+    if (rt->slots[x].acquired) return true;
+    const Slot &sl = rt->slots[x];
+    for (uint32_t t = 0; t < sl.nparts; ++t) stack.push_back(sl.first_child + t);
+  }
   return false;
 }
 
@@ -260,27 +304,30 @@ int retire(bt_runtime *rt, EpochBuf &e) {
                 (unsigned long long)e.units);
   }
   if (e.traced) {
-    rt->trace_t.assign(reinterpret_cast<const uint64_t *>(e.hblob + e.trace_off_h),
-                       reinterpret_cast<const uint64_t *>(e.hblob + e.trace_off_h) + 4 * e.units);
+    const uint64_t *t = reinterpret_cast<const uint64_t *>(e.hblob + e.trace_off_h);
+    rt->trace_t.assign(t, t + 4 * e.units);
     const uint32_t *ti = reinterpret_cast<const uint32_t *>(e.hblob + e.trace_off_h + 32 * e.units);
     rt->trace_item.assign(ti, ti + e.units);
   }
   return 0;
 }
 
-// CSR of successors + offsets, from the builder's edge list (creation order).
-void build_csr(bt_runtime *rt, std::vector<uint32_t> &off, uint32_t *succ) {
-  const auto &items = rt->builder.items;
-  const size_t n = items.size();
-  off.resize(n + 1);
-  uint32_t acc = 0;
-  for (size_t i = 0; i < n; ++i) {
-    off[i] = acc;
-    acc += items[i].nsucc;
-  }
-  off[n] = acc;
-  rt->cursor.assign(off.begin(), off.end() - 1);
-  for (uint64_t e : rt->builder.edges) succ[rt->cursor[e >> 32]++] = (uint32_t)e;
+// Elements per work unit for this epoch: fixed (bt_config.chunk_bytes), or
+// adaptive: about kUnitsPerCta units per persistent CTA, a power of two in
+// [8 KiB, 256 KiB] -- small enough to balance the tail, large enough to
+// amortise one pop + release per unit.
+uint64_t chunk_elems_for(const bt_runtime *rt, uint64_t total_elems) {
+  if (rt->cfg.chunk_bytes) return std::max<uint64_t>(8, (rt->cfg.chunk_bytes / 4) / 8 * 8);
+  const uint64_t target = total_elems / ((uint64_t)std::max(1, rt->grid_max) * kUnitsPerCta);
+  uint64_t c = kMinChunkElems;
+  while (c * 2 <= target && c * 2 <= kMaxChunkBytes / 4) c *= 2;
+  return c;
+}
+
+// Split [0, n) into the pool's ranges.
+inline void range_of(size_t n, int P, int p, size_t &lo, size_t &hi) {
+  lo = n * (size_t)p / (size_t)P;
+  hi = n * (size_t)(p + 1) / (size_t)P;
 }
 
 int flush_epoch(bt_runtime *rt) {
@@ -296,21 +343,57 @@ int flush_epoch(bt_runtime *rt) {
 
   const size_t N = B.items.size();
   const size_t E = B.edges.size();
-  const uint64_t CE = rt->chunk_elems;
-  // factor lists: one materialised copy per distinct trie node used by an item
-  rt->node_off.assign(B.nodes.size(), NONE);
-  size_t F = 0;
-  for (const HItem &it : B.items)
-    if (it.kind == K_SCAL && rt->node_off[it.arg] == NONE) {
-      rt->node_off[it.arg] = (uint32_t)F;
-      F += it.k;
+  const bool big = N >= kParallelPack && rt->pool->size() > 1;
+  const int P = big ? rt->pool->size() : 1;
+
+  // work-unit size from the epoch's total elements (sampled for huge epochs)
+  const size_t stride = std::max<size_t>(1, N / 4096);
+  uint64_t sampled = 0, cnt = 0;
+  for (size_t i = 0; i < N; i += stride, ++cnt) sampled += B.items[i].n;
+  const uint64_t CE = chunk_elems_for(rt, sampled / cnt * N);
+
+  // Pass A (per range): units, initially ready units, successors, factors
+  // (a SCAL item whose factor list equals the previous item's reuses it).
+  struct RangeAcc {
+    uint64_t units = 0, ready = 0, succ = 0, fac = 0;
+  };
+  std::vector<RangeAcc> acc(P);
+  rt->cursor.resize(N);   // per item: 1 = reuses the previous item's factor list
+  auto passA = [&](int p) {
+    size_t lo, hi;
+    range_of(N, P, p, lo, hi);
+    RangeAcc a;
+    const HItem *prev = nullptr;
+    for (size_t i = lo; i < hi; ++i) {
+      const HItem &it = B.items[i];
+      const uint64_t nc = (it.n + CE - 1) / CE;
+      a.units += nc;
+      if (it.npred == 0) a.ready += nc;
+      a.succ += it.nsucc;
+      uint32_t reuse = 0;
+      if (it.kind == K_SCAL) {
+        if (prev && prev->k == it.k && memcmp(B.factors(*prev), B.factors(it), 4ull * it.k) == 0) reuse = 1;
+        else a.fac += it.k;
+        prev = &it;
+      }
+      rt->cursor[i] = reuse;
     }
-  uint64_t U = 0, U0 = 0;
-  for (const HItem &it : B.items) {
-    const uint64_t nc = (it.n + CE - 1) / CE;
-    U += nc;
-    if (it.npred == 0) U0 += nc;
+    acc[p] = a;
+  };
+  if (big) rt->par(passA);
+  else passA(0);
+  std::vector<RangeAcc> base(P);
+  RangeAcc tot;
+  for (int p = 0; p < P; ++p) {
+    base[p] = tot;
+    tot.units += acc[p].units;
+    tot.ready += acc[p].ready;
+    tot.succ += acc[p].succ;
+    tot.fac += acc[p].fac;
   }
+  const uint64_t U = tot.units, U0 = tot.ready, F = tot.fac;
+  if (tot.succ != E) return fail(rt, -EIO, "internal: successor count mismatch");
+
   // device layout: ctr | items | pending | succ | factors | queue[U] | chunk_done[N] | trace
   const size_t o_ctr = 0;
   const size_t o_items = 64;
@@ -339,39 +422,60 @@ int flush_epoch(bt_runtime *rt) {
   uint32_t *succ = reinterpret_cast<uint32_t *>(h + o_succ);
   float *fac = reinterpret_cast<float *>(h + o_fac);
   unsigned long long *q = reinterpret_cast<unsigned long long *>(h + o_queue);
+  rt->succ_off.resize(N);
 
-  std::vector<uint32_t> &offs = rt->csr_off;
-  build_csr(rt, offs, succ);
-  // factor lists: each used trie node is written once, walking to the root
-  rt->node_written.assign(B.nodes.size(), 0);
-  for (const HItem &it : B.items) {
-    if (it.kind != K_SCAL || rt->node_written[it.arg]) continue;
-    rt->node_written[it.arg] = 1;
-    float *dst = fac + rt->node_off[it.arg];
-    uint32_t node = it.arg;
-    for (int64_t j = (int64_t)it.k - 1; j >= 0; --j) {
-      const TrieNode &nd = B.nodes[node];
-      memcpy(dst + j, &nd.fbits, 4);
-      node = nd.parent;
+  // Pass B (per range): fill items, counters, factors, initial ready queue.
+  auto passB = [&](int p) {
+    size_t lo, hi;
+    range_of(N, P, p, lo, hi);
+    uint64_t qi = base[p].ready, so = base[p].succ, fo = base[p].fac;
+    uint32_t prev_fo = 0;
+    for (size_t i = lo; i < hi; ++i) {
+      const HItem &it = B.items[i];
+      DItem &d = di[i];
+      d.x = it.x;
+      d.y = it.y;
+      d.n = it.n;
+      d.kind = it.kind;
+      d.k = it.k;
+      if (it.kind == K_SCAL) {
+        if (!rt->cursor[i]) {
+          memcpy(fac + fo, B.factors(it), 4ull * it.k);
+          prev_fo = (uint32_t)fo;
+          fo += it.k;
+        }
+        d.arg = prev_fo;
+      } else {
+        d.arg = it.arg;
+      }
+      const uint64_t nc = (it.n + CE - 1) / CE;
+      d.nchunks = (uint32_t)nc;
+      d.succ_off = (uint32_t)so;
+      d.nsucc = it.nsucc;
+      rt->succ_off[i] = (uint32_t)so;
+      so += it.nsucc;
+      pend[i] = (int32_t)it.npred;
+      if (it.npred == 0)
+        for (uint64_t c = 0; c < nc; ++c) q[qi++] = ((unsigned long long)i << 32) | c;
     }
-  }
-  uint64_t qi = 0;
-  for (size_t i = 0; i < N; ++i) {
-    const HItem &it = B.items[i];
-    DItem &d = di[i];
-    d.x = it.x;
-    d.y = it.y;
-    d.n = it.n;
-    d.kind = it.kind;
-    d.k = it.k;
-    d.arg = it.kind == K_SCAL ? rt->node_off[it.arg] : it.arg;
-    const uint64_t nc = (it.n + CE - 1) / CE;
-    d.nchunks = (uint32_t)nc;
-    d.succ_off = offs[i];
-    d.nsucc = it.nsucc;
-    pend[i] = (int32_t)it.npred;
-    if (it.npred == 0)
-      for (uint64_t c = 0; c < nc; ++c) q[qi++] = ((unsigned long long)i << 32) | c;
+  };
+  if (big) rt->par(passB);
+  else passB(0);
+  // CSR scatter (successor order within a list: edge creation order when
+  // sequential; any order is valid)
+  if (big) {
+    uint32_t *cur = rt->succ_off.data();
+    rt->par([&](int p) {
+      size_t lo, hi;
+      range_of(E, P, p, lo, hi);
+      for (size_t j = lo; j < hi; ++j) {
+        const uint64_t ed = B.edges[j];
+        const uint32_t pos = __atomic_fetch_add(&cur[ed >> 32], 1u, __ATOMIC_RELAXED);
+        succ[pos] = (uint32_t)ed;
+      }
+    });
+  } else {
+    for (uint64_t ed : B.edges) succ[rt->succ_off[ed >> 32]++] = (uint32_t)ed;
   }
 
   char *d = e.dblob;
@@ -457,8 +561,9 @@ int bt_init(const bt_config *cfg_in, bt_runtime **out) {
   if (cfg.nranks < 1 || cfg.rank < 0 || cfg.rank >= cfg.nranks) return -EINVAL;
   if (cfg.max_fused == 0) cfg.max_fused = kDefaultMaxFused;
   if (cfg.max_fused > (uint32_t)max_factors()) return -EINVAL;
-  if (cfg.chunk_bytes == 0) cfg.chunk_bytes = kDefaultChunkBytes;
-  if (cfg.chunk_bytes < 32) return -EINVAL;
+  if (cfg.chunk_bytes != 0 && cfg.chunk_bytes < 32) return -EINVAL;
+  if (cfg.host_threads < 0) return -EINVAL;
+  if (cfg.parallel_min == 0) cfg.parallel_min = kDefaultParallelMin;
 
   bt_runtime *rt = new (std::nothrow) bt_runtime();
   if (!rt) return -ENOMEM;
@@ -467,7 +572,11 @@ int bt_init(const bt_config *cfg_in, bt_runtime **out) {
   rt->builder.fusion = (cfg.flags & BT_FLAG_NO_FUSION) == 0;
   rt->builder.max_fused = cfg.max_fused;
   rt->builder.record_tasks = rt->host_only;
-  rt->chunk_elems = std::max<uint64_t>(8, (cfg.chunk_bytes / 4) / 8 * 8);
+  int threads = cfg.host_threads;
+  if (threads == 0) threads = (int)std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency()));
+  rt->pool.reset(new Pool(threads));
+  rt->lanes.resize(threads);
+  rt->buckets.resize((size_t)threads * threads);
 
   if (!rt->host_only) {
     int ndev = 0;
@@ -518,11 +627,13 @@ int bt_init(const bt_config *cfg_in, bt_runtime **out) {
       }
     }
     // keep freed replicas in the pool (register/unregister loops reuse them)
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    cudaMemPool_t mp;
+    if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
       uint64_t thr = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
     }
+  } else {
+    rt->grid_max = 148 * 4;   // only used by the chunk policy
   }
   *out = rt;
   return 0;
@@ -596,13 +707,14 @@ int bt_vector_data_register(bt_runtime *rt, bt_handle *out, int home_node, void 
     }
   }
   const uint32_t s = alloc_slots(rt, 1);
+  SlotHot &sh = rt->hot[s];
   Slot &sl = rt->slots[s];
   sl.root = s;
-  sl.dptr = dptr;
-  sl.nx = nx;
+  sh.dptr = dptr;
+  sh.nx = nx;
   sl.hptr = ptr;
   sl.home_node = home_node;
-  sl.rank = ptr ? rt->cfg.rank : -1;
+  sh.rank = ptr ? rt->cfg.rank : -1;
   sl.owns_dev = owns;
   if (ptr) {
     rt->ranges[lo] = {hi, s};
@@ -628,23 +740,26 @@ int bt_data_partition(bt_runtime *rt, bt_handle h, uint32_t nparts) {
   if (s == NONE) return fail(rt, -ENOENT, "attempt to use unregistered pointer");
   if (rt->slots[s].nparts) return fail(rt, -EBUSY, "handle already partitioned");
   if (acquired_chain(rt, s)) return fail(rt, -EBUSY, "handle is acquired");
-  if (nparts == 0 || nparts > rt->slots[s].nx) return fail(rt, -EINVAL, "bad number of parts");
-  const uint32_t c0 = alloc_slots(rt, nparts);   // may reallocate slots/deps
+  if (nparts == 0 || nparts > rt->hot[s].nx) return fail(rt, -EINVAL, "bad number of parts");
+  const uint32_t c0 = alloc_slots(rt, nparts);   // may reallocate the slot arrays
+  SlotHot &ph = rt->hot[s];
   Slot &p = rt->slots[s];
-  const uint64_t base = p.nx / nparts, extra = p.nx % nparts;
+  const uint64_t base = ph.nx / nparts, extra = ph.nx % nparts;
   for (uint32_t t = 0; t < nparts; ++t) {
+    SlotHot &ch = rt->hot[c0 + t];
     Slot &c = rt->slots[c0 + t];
     const uint64_t off = t * base + std::min<uint64_t>(t, extra);
     c.parent = s;
     c.child_index = t;
     c.root = p.root;
     c.offset = p.offset + off;
-    c.nx = base + (t < extra ? 1 : 0);
-    c.dptr = p.dptr ? p.dptr + off : nullptr;
-    c.rank = p.rank;
+    ch.nx = base + (t < extra ? 1 : 0);
+    ch.dptr = ph.dptr ? ph.dptr + off : nullptr;
+    ch.rank = ph.rank;
   }
   p.nparts = nparts;
   p.first_child = c0;
+  ph.flags |= F_PARTITIONED;
   rt->builder.partition_state(rt->deps[s], &rt->deps[c0], nparts);
   return 0;
 }
@@ -675,6 +790,7 @@ int bt_data_unpartition(bt_runtime *rt, bt_handle h) {
   free_slots(rt, p.first_child, p.nparts);
   p.nparts = 0;
   p.first_child = NONE;
+  rt->hot[s].flags &= ~F_PARTITIONED;
   return 0;
 }
 
@@ -683,12 +799,11 @@ int bt_data_set_rank(bt_runtime *rt, bt_handle h, int rank) {
   uint32_t s = resolve(rt, h);
   if (s == NONE) return fail(rt, -ENOENT, "attempt to use unregistered pointer");
   if (rank < 0 || rank >= rt->cfg.nranks) return fail(rt, -EINVAL, "rank %d out of range", rank);
-  // the handle and all its parts (recursively)
-  std::vector<uint32_t> stack{s};
+  std::vector<uint32_t> stack{s};   // the handle and all its parts (recursively)
   while (!stack.empty()) {
     uint32_t x = stack.back();
     stack.pop_back();
-    rt->slots[x].rank = rank;
+    rt->hot[x].rank = rank;
     const Slot &sl = rt->slots[x];
     for (uint32_t t = 0; t < sl.nparts; ++t) stack.push_back(sl.first_child + t);
   }
@@ -719,9 +834,9 @@ inline int64_t operand(bt_runtime *rt, int codelet, bt_handle h) {
     fail(rt, -ENOENT, "attempt to use unregistered pointer (task `%s')", codelet_name(codelet));
     return -ENOENT;
   }
-  const Slot &sl = rt->slots[s];
-  if (sl.nparts) return insert_fail(rt, codelet, -EBUSY, "handle is partitioned");
-  if (acquired_chain(rt, s)) return insert_fail(rt, codelet, -EBUSY, "handle is acquired");
+  const uint32_t f = rt->hot[s].flags;
+  if (f & F_PARTITIONED) return insert_fail(rt, codelet, -EBUSY, "handle is partitioned");
+  if (f & F_BLOCKED) return insert_fail(rt, codelet, -EBUSY, "handle is acquired");
   return s;
 }
 
@@ -729,7 +844,7 @@ int submit(bt_runtime *rt, int codelet, float scalar, bt_handle h0, bt_handle h1
   int64_t s0 = operand(rt, codelet, h0);
   if (s0 < 0) return (int)s0;
   if (codelet == BT_CL_SCAL) {
-    const Slot &x = rt->slots[s0];
+    const SlotHot &x = rt->hot[s0];
     if (x.rank != rt->cfg.rank) {
       if (x.rank < 0) return insert_fail(rt, codelet, -EINVAL, "data has no home rank");
       rt->builder.add_remote();
@@ -743,8 +858,8 @@ int submit(bt_runtime *rt, int codelet, float scalar, bt_handle h0, bt_handle h1
   } else {
     int64_t s1 = operand(rt, codelet, h1);
     if (s1 < 0) return (int)s1;
-    const Slot &x = rt->slots[s0];
-    const Slot &y = rt->slots[s1];
+    const SlotHot &x = rt->hot[s0];
+    const SlotHot &y = rt->hot[s1];
     if (x.nx != y.nx) return insert_fail(rt, codelet, -EINVAL, "operand lengths differ");
     if (x.rank != y.rank) {
       if (x.rank < 0 || y.rank < 0) return insert_fail(rt, codelet, -EINVAL, "data has no home rank");
@@ -759,16 +874,120 @@ int submit(bt_runtime *rt, int codelet, float scalar, bt_handle h0, bt_handle h1
     if ((!x.dptr || !y.dptr) && !rt->host_only) return insert_fail(rt, codelet, -EINVAL, "no local storage");
     uint32_t ab = 0;
     if (codelet == BT_CL_AXPY) memcpy(&ab, &scalar, 4);
-    Access a0{(uint32_t)s0, (uint32_t)BT_R};
-    Access a1{(uint32_t)s1, (uint32_t)(codelet == BT_CL_AXPY ? BT_RW : BT_W)};
-    DepState *d0 = &rt->deps[s0];
-    DepState *d1 = &rt->deps[s1];
-    rt->builder.add_task((uint32_t)codelet, d0, a0, d1, a1, reinterpret_cast<uint64_t>(x.dptr),
-                         reinterpret_cast<uint64_t>(y.dptr), x.nx, ab);
+    rt->builder.add_task((uint32_t)codelet, &rt->deps[s0], (uint32_t)s0, (uint32_t)BT_R, &rt->deps[s1],
+                         (uint32_t)s1, (uint32_t)(codelet == BT_CL_AXPY ? BT_RW : BT_W),
+                         reinterpret_cast<uint64_t>(x.dptr), reinterpret_cast<uint64_t>(y.dptr), x.nx, ab);
   }
   ++rt->stats.tasks_submitted;
   ++rt->stats.tasks_local;
   if (rt->cfg.epoch_tasks && rt->builder.ntasks >= rt->cfg.epoch_tasks && !rt->host_only) return flush_epoch(rt);
+  return 0;
+}
+
+// Lane owning slot s: blocks of 64 consecutive slots (768 bytes of DepState)
+// per lane, so that lanes never write the same cache line.
+inline uint32_t lane_of(uint32_t s, int P) { return (s >> 6) % (uint32_t)P; }
+
+// A run of SCAL tasks [i0, i1) built on the pool: phase 1 validates and
+// buckets tasks by owning lane (slot % P); phase 2 runs each lane's tasks in
+// submission order; merge renumbers.  Returns 1 (nothing changed) if any task
+// of the run would fail, so that the caller replays it sequentially and stops
+// at the first error exactly like bt_insert_task.
+int scal_run_parallel(bt_runtime *rt, const float *scalars, const bt_handle *h0, size_t i0, size_t i1) {
+  const int P = rt->pool->size();
+  const size_t n = i1 - i0;
+  Builder &B = rt->builder;
+  const uint64_t tbase = B.ntasks;
+  const int myrank = rt->cfg.rank;
+  const bool host_only = rt->host_only;
+  std::vector<int> bad(P, 0);
+  std::vector<uint64_t> remote(P, 0);
+  const size_t nslots = rt->hot.size();
+  const SlotHot *hot = rt->hot.data();
+  static const bool dbg = getenv("BT_DEBUG_TIMING") != nullptr;
+  double tp0 = now_ms();
+  rt->par([&](int c) {
+    size_t lo, hi;
+    range_of(n, P, c, lo, hi);
+    // this chunk's buckets, moved to the stack while filling (no false sharing
+    // of vector headers between threads)
+    std::vector<std::vector<LaneEntry>> mine(P);
+    for (int l = 0; l < P; ++l) {
+      mine[l].swap(rt->buckets[(size_t)c * P + l]);
+      mine[l].clear();
+    }
+    struct Restore {
+      std::vector<std::vector<LaneEntry>> &m;
+      bt_runtime *rt;
+      int c, P;
+      ~Restore() {
+        for (int l = 0; l < P; ++l) m[l].swap(rt->buckets[(size_t)c * P + l]);
+      }
+    } restore{mine, rt, c, P};
+    uint64_t rem = 0;
+    for (size_t j = lo; j < hi; ++j) {
+      const bt_handle h = h0[i0 + j];
+      const uint64_t idx = h & 0xFFFFFFFFull;
+      if (idx == 0 || idx > nslots) {
+        bad[c] = 1;
+        return;
+      }
+      const uint32_t s = (uint32_t)(idx - 1);
+      const SlotHot &sh = hot[s];
+      if (sh.gen != (uint32_t)(h >> 32) || (sh.flags & (F_LIVE | F_PARTITIONED | F_BLOCKED)) != F_LIVE) {
+        bad[c] = 1;
+        return;
+      }
+      if (sh.rank != myrank) {
+        if (sh.rank < 0) {
+          bad[c] = 1;
+          return;
+        }
+        ++rem;
+        continue;
+      }
+      if (!sh.dptr && !host_only) {
+        bad[c] = 1;
+        return;
+      }
+      LaneEntry e;
+      e.slot = s;
+      memcpy(&e.fbits, &scalars[i0 + j], 4);
+      e.task = (uint32_t)(tbase + j);
+      e.pad = 0;
+      mine[lane_of(s, P)].push_back(e);
+    }
+    remote[c] = rem;
+  });
+  for (int c = 0; c < P; ++c)
+    if (bad[c]) {
+      if (dbg) fprintf(stderr, "scal_run_parallel: chunk %d rejected, sequential replay\n", c);
+      return 1;
+    }
+  if (B.record_tasks) {
+    B.task_item.resize(tbase + n, NONE);
+    B.task_pos.resize(tbase + n, 0);
+  }
+  DepState *deps = rt->deps.data();
+  double tp1 = now_ms();
+  rt->par([&](int l) {
+    Lane &L = rt->lanes[l];
+    L.clear();
+    for (int c = 0; c < P; ++c)
+      for (const LaneEntry &e : rt->buckets[(size_t)c * P + l]) {
+        const SlotHot &sh = hot[e.slot];
+        B.lane_scal(L, deps[e.slot], e, reinterpret_cast<uint64_t>(sh.dptr), sh.nx);
+      }
+  });
+  double tp2 = now_ms();
+  B.merge(rt->lanes, deps, [&](const std::function<void(int)> &f) { rt->pool->run(f); });
+  if (dbg) fprintf(stderr, "scal_run_parallel n=%zu P=%d phase1 %.3f ms phase2 %.3f ms merge %.3f ms\n", n, P,
+                   tp1 - tp0, tp2 - tp1, now_ms() - tp2);
+  uint64_t rem = 0;
+  for (int c = 0; c < P; ++c) rem += remote[c];
+  B.ntasks += n;
+  rt->stats.tasks_submitted += n;
+  rt->stats.tasks_local += n - rem;
   return 0;
 }
 
@@ -811,16 +1030,31 @@ int bt_insert_task_batch(bt_runtime *rt, size_t ntasks, const int32_t *codelets,
   const double t0 = now_ms();
   size_t i = 0;
   int rc = 0;
-  for (; i < ntasks; ++i) {
-    const int c = codelets[i];
-    if (c != BT_CL_SCAL) {
-      if ((c != BT_CL_AXPY && c != BT_CL_COPY) || !h1) {
-        rc = fail(rt, -EINVAL, "failed to insert task: bad codelet %d or missing operand array", c);
-        break;
+  const size_t pmin = rt->cfg.parallel_min;
+  while (i < ntasks && rc == 0) {
+    if (codelets[i] == BT_CL_SCAL && rt->pool->size() > 1) {
+      size_t j = i;
+      while (j < ntasks && codelets[j] == BT_CL_SCAL) ++j;
+      if (j - i >= pmin && scal_run_parallel(rt, scalars, h0, i, j) == 0) {
+        i = j;
+        if (rt->cfg.epoch_tasks && rt->builder.ntasks >= rt->cfg.epoch_tasks && !rt->host_only)
+          rc = flush_epoch(rt);
+        continue;
       }
+      for (; i < j; ++i) {      // short run, or a task of the run fails: sequential
+        rc = submit(rt, BT_CL_SCAL, scalars[i], h0[i], 0);
+        if (rc) break;
+      }
+      continue;
+    }
+    const int c = codelets[i];
+    if (c != BT_CL_SCAL && ((c != BT_CL_AXPY && c != BT_CL_COPY) || !h1)) {
+      rc = fail(rt, -EINVAL, "failed to insert task: bad codelet %d or missing operand array", c);
+      break;
     }
     rc = submit(rt, c, scalars[i], h0[i], c == BT_CL_SCAL ? 0 : h1[i]);
     if (rc) break;
+    ++i;
   }
   rt->stats.host_build_ms += now_ms() - t0;
   if (nsubmitted) *nsubmitted = i;
@@ -847,17 +1081,19 @@ int bt_data_acquire(bt_runtime *rt, bt_handle h, int mode) {
   if (s == NONE) return fail(rt, -ENOENT, "attempt to use unregistered pointer");
   if (mode != BT_R && mode != BT_RW) return fail(rt, -EINVAL, "acquire mode must be R or RW");
   if (acquired_chain(rt, s)) return fail(rt, -EBUSY, "already acquired");
-  Slot &sl = rt->slots[s];
+  const Slot &sl = rt->slots[s];
+  const SlotHot &sh = rt->hot[s];
   const Slot &root = rt->slots[sl.root];
   if (root.home_node != 0 || !root.hptr) return fail(rt, -EINVAL, "no host copy to acquire into");
   if (rt->host_only) return fail(rt, -ENODEV, "host-only runtime");
-  if (sl.rank != rt->cfg.rank || !sl.dptr) return fail(rt, -EINVAL, "data not stored on this rank");
+  if (sh.rank != rt->cfg.rank || !sh.dptr) return fail(rt, -EINVAL, "data not stored on this rank");
   cudaSetDevice(rt->device);
   if (int r = wait_all(rt)) return r;
-  CUDA_TRY(rt, cudaMemcpyAsync(static_cast<float *>(root.hptr) + sl.offset, sl.dptr, sl.nx * 4,
+  CUDA_TRY(rt, cudaMemcpyAsync(static_cast<float *>(root.hptr) + sl.offset, sh.dptr, sh.nx * 4,
                                cudaMemcpyDeviceToHost, rt->stream));
   CUDA_TRY(rt, cudaStreamSynchronize(rt->stream));
   rt->slots[s].acquired = mode;
+  set_blocked(rt, s, true);
   return 0;
 }
 
@@ -869,13 +1105,15 @@ int bt_data_release(bt_runtime *rt, bt_handle h) {
   if (!sl.acquired) return fail(rt, -EINVAL, "handle is not acquired");
   if (sl.acquired == BT_RW) {
     const Slot &root = rt->slots[sl.root];
+    const SlotHot &sh = rt->hot[s];
     cudaSetDevice(rt->device);
-    CUDA_TRY(rt, cudaMemcpyAsync(sl.dptr, static_cast<float *>(root.hptr) + sl.offset, sl.nx * 4,
+    CUDA_TRY(rt, cudaMemcpyAsync(sh.dptr, static_cast<float *>(root.hptr) + sl.offset, sh.nx * 4,
                                  cudaMemcpyHostToDevice, rt->stream));
-    // host writes under RW acquire: later tasks must see them (stream order)
+    // host writes under RW acquire: later tasks see them (stream order)
     CUDA_TRY(rt, cudaStreamSynchronize(rt->stream));
   }
   sl.acquired = 0;
+  set_blocked(rt, s, false);
   return 0;
 }
 
@@ -884,16 +1122,18 @@ int bt_data_unregister(bt_runtime *rt, bt_handle h) {
   uint32_t s = resolve(rt, h);
   if (s == NONE) return fail(rt, -ENOENT, "attempt to use unregistered pointer");
   Slot &sl = rt->slots[s];
+  SlotHot &sh = rt->hot[s];
   if (sl.parent != NONE) return fail(rt, -EBUSY, "cannot unregister a sub-handle");
   if (sl.nparts) return fail(rt, -EBUSY, "unpartition before unregistering");
+  if (sl.acquired) return fail(rt, -EBUSY, "release before unregistering");
   if (!rt->host_only) {
     cudaSetDevice(rt->device);
     if (int r = wait_all(rt)) return r;
-    if (sl.home_node == 0 && sl.hptr && sl.dptr) {
-      CUDA_TRY(rt, cudaMemcpyAsync(sl.hptr, sl.dptr, sl.nx * 4, cudaMemcpyDeviceToHost, rt->stream));
+    if (sl.home_node == 0 && sl.hptr && sh.dptr) {
+      CUDA_TRY(rt, cudaMemcpyAsync(sl.hptr, sh.dptr, sh.nx * 4, cudaMemcpyDeviceToHost, rt->stream));
       CUDA_TRY(rt, cudaStreamSynchronize(rt->stream));
     }
-    if (sl.owns_dev) CUDA_TRY(rt, cudaFreeAsync(sl.dptr, rt->stream));
+    if (sl.owns_dev) CUDA_TRY(rt, cudaFreeAsync(sh.dptr, rt->stream));
   }
   if (sl.hptr) {
     rt->ranges.erase(reinterpret_cast<uintptr_t>(sl.hptr));
@@ -947,13 +1187,19 @@ int bt_dag_snapshot(bt_runtime *rt, bt_dag_view *out) {
   rt->snap_kind.resize(N);
   rt->snap_k.resize(N);
   rt->snap_npred.resize(N);
+  rt->snap_off.resize(N + 1);
   rt->snap_succ.resize(B.edges.size());
-  build_csr(rt, rt->snap_off, rt->snap_succ.data());
+  uint32_t acc = 0;
   for (size_t i = 0; i < N; ++i) {
+    rt->snap_off[i] = acc;
+    acc += B.items[i].nsucc;
     rt->snap_kind[i] = (uint8_t)B.items[i].kind;
     rt->snap_k[i] = B.items[i].k;
     rt->snap_npred[i] = B.items[i].npred;
   }
+  rt->snap_off[N] = acc;
+  rt->cursor.assign(rt->snap_off.begin(), rt->snap_off.end() - 1);
+  for (uint64_t ed : B.edges) rt->snap_succ[rt->cursor[ed >> 32]++] = (uint32_t)ed;
   rt->snap_task_item = B.task_item;
   rt->snap_task_pos = B.task_pos;
   out->ntasks = B.ntasks;

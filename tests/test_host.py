@@ -118,11 +118,40 @@ def check_dag(program, snap):
 
 
 @pytest.mark.parametrize("fusion", [True, False])
-def test_builder_matches_conflict_relation_random(B, fusion):
+@pytest.mark.parametrize("threads,pmin", [(1, 0), (4, 1), (3, 2)])
+def test_builder_matches_conflict_relation_random(B, fusion, threads, pmin):
+    """Sequential builder (1 thread) and the parallel SCAL-run lanes (forced on
+    every run of >= pmin SCALs) both enforce exactly the conflict relation."""
     for seed in range(150):
         p = W.random_small_program(seed, max_tasks=10)
-        snap = snapshot_program(B, p, flags=0 if fusion else B.BT_FLAG_NO_FUSION)
+        snap = snapshot_program(B, p, flags=0 if fusion else B.BT_FLAG_NO_FUSION, host_threads=threads,
+                                parallel_min=pmin)
         assert snap["ntasks"] == p.ntasks
+        check_dag(p, snap)
+
+
+@pytest.mark.parametrize("fusion", [True, False])
+def test_parallel_lanes_long_scal_runs(B, fusion):
+    """Long SCAL runs over partitioned buffers, split by AXPY/COPY tasks that
+    tie tiles together, built by 5 lanes; max_fused forces chain splits."""
+    rng = np.random.default_rng(77)
+    for rep in range(6):
+        nbuf, nparts, n = 3, 7, 70
+        bufs = [W.unit_interval_floats(rng, n) for _ in range(nbuf)]
+        rows = []
+        for blk in range(4):
+            for _ in range(int(rng.integers(20, 60))):
+                b = int(rng.integers(0, nbuf))
+                rows.append((W.SCAL, np.float32(rng.uniform(0.5, 2)), b, int(rng.integers(0, nparts)), -1, -1))
+            b0, b1 = rng.choice(nbuf, 2, replace=False)
+            t = int(rng.integers(0, nparts))
+            rows.append((W.AXPY if blk % 2 else W.COPY, np.float32(0.25), int(b0), t, int(b1), t))
+        tasks = W._tasks(len(rows))
+        for i, r in enumerate(rows):
+            tasks[i] = r
+        p = W.Program(bufs, [nparts] * nbuf, tasks)
+        snap = snapshot_program(B, p, flags=0 if fusion else B.BT_FLAG_NO_FUSION, host_threads=5,
+                                parallel_min=8, max_fused=4)
         check_dag(p, snap)
 
 
