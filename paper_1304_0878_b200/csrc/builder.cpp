@@ -56,7 +56,7 @@ void Builder::unpartition_state(DepState &parent, DepState *parts, uint32_t npar
 }
 
 namespace {
-inline void lane_append(std::vector<float> &gpool, Lane &L, HItem &it, uint32_t fbits, uint32_t w, bool global) {
+inline void lane_append(vec<float> &gpool, Lane &L, HItem &it, uint32_t fbits, uint32_t w, bool global) {
   if (it.fofs & TAG) {
     uint32_t ofs = it.fofs & ~TAG;
     if (it.k == it.fcap) {

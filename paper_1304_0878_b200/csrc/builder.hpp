@@ -32,9 +32,34 @@
 #include <string.h>
 
 #include <atomic>
+#include <memory>
+#include <utility>
 #include <vector>
 
 namespace bt {
+
+// std::allocator that default-initialises (no zero fill on resize): the
+// builder resizes multi-megabyte arrays whose every element it overwrites.
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = NoInitAlloc<U>;
+  };
+  NoInitAlloc() = default;
+  template <class U>
+  NoInitAlloc(const NoInitAlloc<U> &) {}
+  template <class U>
+  void construct(U *p) noexcept {
+    ::new (static_cast<void *>(p)) U;
+  }
+  template <class U, class... A>
+  void construct(U *p, A &&...a) {
+    ::new (static_cast<void *>(p)) U(std::forward<A>(a)...);
+  }
+};
+template <class T>
+using vec = std::vector<T, NoInitAlloc<T>>;
 
 constexpr uint32_t NONE = 0xFFFFFFFFu;
 constexpr uint32_t TAG = 0x80000000u;     // lane-local item id / lane-local factor offset
@@ -72,9 +97,9 @@ struct LaneEntry {
 };
 
 struct alignas(64) Lane {
-  std::vector<HItem> items;
-  std::vector<uint64_t> edges;        // (pred << 32) | succ, ids possibly TAGged
-  std::vector<float> fpool;
+  vec<HItem> items;
+  vec<uint64_t> edges;                // (pred << 32) | succ, ids possibly TAGged
+  vec<float> fpool;
   std::vector<uint32_t> touched;      // slots whose state now holds a tagged id
   std::vector<uint32_t> relocated;    // global items whose factors moved to fpool
   std::vector<uint64_t> recorded;     // (task << 32) | tagged item (record_tasks)
@@ -94,9 +119,9 @@ struct alignas(64) Lane {
 class Builder {
  public:
   // Epoch-scoped outputs
-  std::vector<HItem> items;
-  std::vector<uint64_t> edges;      // (pred << 32) | succ
-  std::vector<float> fpool;         // factor lists of SCAL items
+  vec<HItem> items;
+  vec<uint64_t> edges;              // (pred << 32) | succ
+  vec<float> fpool;                 // factor lists of SCAL items
   std::vector<DepExt> exts;
   std::vector<uint32_t> task_item;  // per epoch task (only if record_tasks)
   std::vector<uint32_t> task_pos;

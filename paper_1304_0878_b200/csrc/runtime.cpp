@@ -39,7 +39,7 @@ namespace {
 
 constexpr uint32_t kMaxChunkBytes = 256u << 10;     // adaptive chunking: upper bound
 constexpr uint64_t kMinChunkElems = 2048;           // adaptive chunking: lower bound (8 KiB)
-constexpr uint32_t kUnitsPerCta = 64;               // adaptive chunking: target work units per CTA
+constexpr uint32_t kUnitsPerCta = 16;               // adaptive chunking: target work units per CTA
 constexpr uint32_t kDefaultMaxFused = 256;
 constexpr uint32_t kDefaultParallelMin = 16384;
 constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;   // 20 s
@@ -122,7 +122,7 @@ struct bt_runtime {
   Builder builder;
   std::unique_ptr<Pool> pool;
   std::vector<Lane> lanes;
-  std::vector<std::vector<LaneEntry>> buckets;                  // [chunk * P + lane]
+  std::vector<vec<LaneEntry>> buckets;                  // [chunk * P + lane]
   EpochBuf ep[2];
   int ep_cur = 0;
   bt_stats stats{};
@@ -893,7 +893,8 @@ inline uint32_t lane_of(uint32_t s, int P) { return (s >> 6) % (uint32_t)P; }
 // submission order; merge renumbers.  Returns 1 (nothing changed) if any task
 // of the run would fail, so that the caller replays it sequentially and stops
 // at the first error exactly like bt_insert_task.
-int scal_run_parallel(bt_runtime *rt, const float *scalars, const bt_handle *h0, size_t i0, size_t i1) {
+int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scalars, const bt_handle *h0, size_t i0,
+                      size_t i1) {
   const int P = rt->pool->size();
   const size_t n = i1 - i0;
   Builder &B = rt->builder;
@@ -911,13 +912,13 @@ int scal_run_parallel(bt_runtime *rt, const float *scalars, const bt_handle *h0,
     range_of(n, P, c, lo, hi);
     // this chunk's buckets, moved to the stack while filling (no false sharing
     // of vector headers between threads)
-    std::vector<std::vector<LaneEntry>> mine(P);
+    std::vector<vec<LaneEntry>> mine(P);
     for (int l = 0; l < P; ++l) {
       mine[l].swap(rt->buckets[(size_t)c * P + l]);
       mine[l].clear();
     }
     struct Restore {
-      std::vector<std::vector<LaneEntry>> &m;
+      std::vector<vec<LaneEntry>> &m;
       bt_runtime *rt;
       int c, P;
       ~Restore() {
@@ -926,6 +927,10 @@ int scal_run_parallel(bt_runtime *rt, const float *scalars, const bt_handle *h0,
     } restore{mine, rt, c, P};
     uint64_t rem = 0;
     for (size_t j = lo; j < hi; ++j) {
+      if (codelets[i0 + j] != BT_CL_SCAL) {
+        bad[c] = 1;
+        return;
+      }
       const bt_handle h = h0[i0 + j];
       const uint64_t idx = h & 0xFFFFFFFFull;
       if (idx == 0 || idx > nslots) {
@@ -1031,11 +1036,16 @@ int bt_insert_task_batch(bt_runtime *rt, size_t ntasks, const int32_t *codelets,
   size_t i = 0;
   int rc = 0;
   const size_t pmin = rt->cfg.parallel_min;
+  // common case first: the whole batch is one long valid SCAL run
+  if (ntasks >= pmin && rt->pool->size() > 1 && scal_run_parallel(rt, codelets, scalars, h0, 0, ntasks) == 0) {
+    i = ntasks;
+    if (rt->cfg.epoch_tasks && rt->builder.ntasks >= rt->cfg.epoch_tasks && !rt->host_only) rc = flush_epoch(rt);
+  }
   while (i < ntasks && rc == 0) {
     if (codelets[i] == BT_CL_SCAL && rt->pool->size() > 1) {
       size_t j = i;
       while (j < ntasks && codelets[j] == BT_CL_SCAL) ++j;
-      if (j - i >= pmin && scal_run_parallel(rt, scalars, h0, i, j) == 0) {
+      if (j - i >= pmin && j - i < ntasks && scal_run_parallel(rt, codelets, scalars, h0, i, j) == 0) {
         i = j;
         if (rt->cfg.epoch_tasks && rt->builder.ntasks >= rt->cfg.epoch_tasks && !rt->host_only)
           rc = flush_epoch(rt);

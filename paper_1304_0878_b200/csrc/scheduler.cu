@@ -1,20 +1,30 @@
 // scheduler.cu -- the persistent sm_100a scheduler kernel and its task bodies.
 //
 // One launch executes one epoch: a DAG of work items built on the host from
-// the submission order (runtime.cpp).  Every resident CTA loops:
+// the submission order (runtime.cpp).  Each resident CTA is warp-specialised:
 //
-//   pop    t = atomicAdd(head, 1); spin on ld.acquire(queue[t]) until the unit
-//          (item, chunk) is published; t >= total_units ends the CTA.
-//   body   run the item's task body on its chunk of elements:
-//            SCAL   x[i] = x[i]*f_1*...*f_k   (k sequential RN multiplies,
+//   warp 0 (scheduler)   pop     t = atomicAdd(head, 1); spin on ld.acquire
+//                                (queue[t]) until the unit (item, chunk) is
+//                                published; t >= total_units ends the CTA.
+//                        stage   copy the item's factor list to shared memory
+//                        release when an item's last chunk is done, decrement
+//                                each successor's pending counter; a successor
+//                                reaching 0 is ready: its chunks are appended
+//                                to the queue (atomicAdd(tail) + stores after a
+//                                gpu-scope fence).
+//   warps 1..8 (compute) run the task body on the unit's elements:
+//            SCAL   x[i] = x[i]*f_1*...*f_k   (k sequential RN multiplies in
 //                   submission order: PAPER.md:157-158; a fused chain of k
 //                   vector_scal tasks is exactly k roundings per element)
 //            AXPY   y[i] = fl(fl(a*x[i]) + y[i])
 //            COPY   y[i] = x[i]
-//   release when the item's last chunk is done, decrement each successor's
-//          pending counter; a successor reaching 0 is ready: its chunks are
-//          appended to the queue (atomicAdd(tail, nchunks) + stores after a
-//          gpu-scope fence).
+//
+// The two roles exchange units through two shared-memory slots: FULL[b] is a
+// named barrier (scheduler -> compute), EMPTY[b] an mbarrier the scheduler
+// polls without blocking (compute -> scheduler).  Popping unit u+1 and
+// releasing unit u-1 overlap the body of unit u, so the scheduling cost
+// leaves the critical path of a busy CTA; while spinning for a not yet
+// published unit the scheduler keeps releasing the units its CTA finishes.
 //
 // This is StarPU's "scheduler's queue" moved on-device:
 // dependencies inferred at submission become per-item
@@ -33,9 +43,12 @@
 
 namespace bt {
 
-constexpr int kBlock = 256;
-constexpr int kMaxFactors = 1024;      // upper bound of bt_config.max_fused
+constexpr int kCompute = 256;                  // compute threads (8 warps)
+constexpr int kBlock = 32 + kCompute;          // + 1 scheduler warp
+constexpr int kMaxFactors = 1024;              // upper bound of bt_config.max_fused
 constexpr unsigned long long kStop = ~0ull - 1;
+// named barrier ids (0 is __syncthreads): FULL[slot] = 1 + slot
+constexpr int kBarFull = 1;
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
   unsigned long long v;
@@ -45,7 +58,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned ld_volatile_u32(const unsigned *p) {
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned *p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
@@ -54,6 +67,32 @@ __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+// Named barriers with immediate ids (a register id makes ptxas reserve all 16
+// hardware barriers and caps the CTAs per SM).
+template <int ID>
+__device__ __forceinline__ void bar_sync_n(int n) {
+  asm volatile("bar.sync %0, %1;" ::"n"(ID), "r"(n) : "memory");
+}
+template <int ID>
+__device__ __forceinline__ void bar_arrive_n(int n) {
+  asm volatile("bar.arrive %0, %1;" ::"n"(ID), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_sync(int id, int n) {
+  switch (id) {
+    case 1: bar_sync_n<1>(n); break;
+    case 2: bar_sync_n<2>(n); break;
+    case 3: bar_sync_n<3>(n); break;
+    default: bar_sync_n<4>(n); break;
+  }
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  switch (id) {
+    case 1: bar_arrive_n<1>(n); break;
+    case 2: bar_arrive_n<2>(n); break;
+    case 3: bar_arrive_n<3>(n); break;
+    default: bar_arrive_n<4>(n); break;
+  }
 }
 
 // ---- 256-bit global accesses, cached in L2 only --------------------------
@@ -116,46 +155,44 @@ __device__ __forceinline__ uint64_t head_elems(const float *p, uint64_t n) {
   return h < n ? h : n;
 }
 
-__device__ void scal_range(float *x, uint64_t n, const float *sf, uint32_t k) {
-  const int tid = threadIdx.x;
+template <int U>
+__device__ void scal_range(float *x, uint64_t n, const float *sf, uint32_t k, int tid) {
   const uint64_t head = head_elems(x, n);
-  for (uint64_t i = tid; i < head; i += kBlock) __stcg(x + i, chain_scalar(__ldcg(x + i), sf, k));
+  for (uint64_t i = tid; i < head; i += kCompute) __stcg(x + i, chain_scalar(__ldcg(x + i), sf, k));
   float *xv = x + head;
   const uint64_t nv = (n - head) >> 3;
-  constexpr int U = 2;
   uint64_t i = tid;
-  for (; i + (U - 1) * kBlock < nv; i += U * kBlock) {
+  for (; i + (U - 1) * kCompute < nv; i += U * kCompute) {
     float v[U][8];
 #pragma unroll
-    for (int a = 0; a < U; ++a) ld8(xv + 8 * (i + a * kBlock), v[a]);
+    for (int a = 0; a < U; ++a) ld8(xv + 8 * (i + a * kCompute), v[a]);
     chain_apply<U>(v, sf, k);
 #pragma unroll
-    for (int a = 0; a < U; ++a) st8(xv + 8 * (i + a * kBlock), v[a]);
+    for (int a = 0; a < U; ++a) st8(xv + 8 * (i + a * kCompute), v[a]);
   }
-  for (; i < nv; i += kBlock) {
+  for (; i < nv; i += kCompute) {
     float v[1][8];
     ld8(xv + 8 * i, v[0]);
     chain_apply<1>(v, sf, k);
     st8(xv + 8 * i, v[0]);
   }
-  for (uint64_t t = head + 8 * nv + tid; t < n; t += kBlock) __stcg(x + t, chain_scalar(__ldcg(x + t), sf, k));
+  for (uint64_t t = head + 8 * nv + tid; t < n; t += kCompute) __stcg(x + t, chain_scalar(__ldcg(x + t), sf, k));
 }
 
 // AXPY: y[i] = fl(fl(a*x[i]) + y[i]) (two roundings, no FFMA).
 __device__ __forceinline__ float axpy1(float a, float x, float y) { return __fadd_rn(__fmul_rn(a, x), y); }
 
-__device__ void axpy_range(const float *x, float *y, uint64_t n, float a) {
-  const int tid = threadIdx.x;
+__device__ void axpy_range(const float *x, float *y, uint64_t n, float a, int tid) {
   if (((reinterpret_cast<uintptr_t>(x) ^ reinterpret_cast<uintptr_t>(y)) & 31u) != 0) {
-    for (uint64_t i = tid; i < n; i += kBlock) __stcg(y + i, axpy1(a, __ldcg(x + i), __ldcg(y + i)));
+    for (uint64_t i = tid; i < n; i += kCompute) __stcg(y + i, axpy1(a, __ldcg(x + i), __ldcg(y + i)));
     return;
   }
   const uint64_t head = head_elems(y, n);
-  for (uint64_t i = tid; i < head; i += kBlock) __stcg(y + i, axpy1(a, __ldcg(x + i), __ldcg(y + i)));
+  for (uint64_t i = tid; i < head; i += kCompute) __stcg(y + i, axpy1(a, __ldcg(x + i), __ldcg(y + i)));
   const float *xv = x + head;
   float *yv = y + head;
   const uint64_t nv = (n - head) >> 3;
-  for (uint64_t i = tid; i < nv; i += kBlock) {
+  for (uint64_t i = tid; i < nv; i += kCompute) {
     float xr[8], yr[8];
     ld8(xv + 8 * i, xr);
     ld8(yv + 8 * i, yr);
@@ -163,139 +200,273 @@ __device__ void axpy_range(const float *x, float *y, uint64_t n, float a) {
     for (int q = 0; q < 8; ++q) yr[q] = axpy1(a, xr[q], yr[q]);
     st8(yv + 8 * i, yr);
   }
-  for (uint64_t t = head + 8 * nv + tid; t < n; t += kBlock) __stcg(y + t, axpy1(a, __ldcg(x + t), __ldcg(y + t)));
+  for (uint64_t t = head + 8 * nv + tid; t < n; t += kCompute) __stcg(y + t, axpy1(a, __ldcg(x + t), __ldcg(y + t)));
 }
 
-__device__ void copy_range(const float *x, float *y, uint64_t n) {
-  const int tid = threadIdx.x;
+__device__ void copy_range(const float *x, float *y, uint64_t n, int tid) {
   if (x == y) return;
   if (((reinterpret_cast<uintptr_t>(x) ^ reinterpret_cast<uintptr_t>(y)) & 31u) != 0) {
-    for (uint64_t i = tid; i < n; i += kBlock) __stcg(y + i, __ldcg(x + i));
+    for (uint64_t i = tid; i < n; i += kCompute) __stcg(y + i, __ldcg(x + i));
     return;
   }
   const uint64_t head = head_elems(y, n);
-  for (uint64_t i = tid; i < head; i += kBlock) __stcg(y + i, __ldcg(x + i));
+  for (uint64_t i = tid; i < head; i += kCompute) __stcg(y + i, __ldcg(x + i));
   const float *xv = x + head;
   float *yv = y + head;
   const uint64_t nv = (n - head) >> 3;
   uint64_t i = tid;
-  for (; i + kBlock < nv; i += 2 * kBlock) {
+  for (; i + kCompute < nv; i += 2 * kCompute) {
     float a[8], b[8];
     ld8(xv + 8 * i, a);
-    ld8(xv + 8 * (i + kBlock), b);
+    ld8(xv + 8 * (i + kCompute), b);
     st8(yv + 8 * i, a);
-    st8(yv + 8 * (i + kBlock), b);
+    st8(yv + 8 * (i + kCompute), b);
   }
-  for (; i < nv; i += kBlock) {
+  for (; i < nv; i += kCompute) {
     float a[8];
     ld8(xv + 8 * i, a);
     st8(yv + 8 * i, a);
   }
-  for (uint64_t t = head + 8 * nv + tid; t < n; t += kBlock) __stcg(y + t, __ldcg(x + t));
+  for (uint64_t t = head + 8 * nv + tid; t < n; t += kCompute) __stcg(y + t, __ldcg(x + t));
 }
 
-// ---- release: completion of one unit (called by thread 0 after bar.sync) --
-// Memory-model pattern (as in cooperative-groups grid sync): the CTA's stores
-// are ordered before thread 0's gpu-scope fence by bar.sync; fence + relaxed
-// RMW = release; RMW observing the last decrement + fence = acquire.
-__device__ __forceinline__ void release_unit(const EpochArgs &a, uint32_t item, const DItem &it) {
-  __threadfence();
-  if (it.nchunks > 1) {
-    const unsigned c = atomicAdd(&a.chunk_done[item], 1u);
-    if (c + 1 != it.nchunks) return;
-    __threadfence();  // acquire the other chunks' stores before releasing them on
-  }
-  for (uint32_t i = 0; i < it.nsucc; ++i) {
-    const uint32_t s = __ldg(&a.succ[it.succ_off + i]);
-    if (atomicSub(&a.pending[s], 1) == 1) {
-      __threadfence();
-      const uint32_t nc = __ldg(&a.items[s].nchunks);
-      const unsigned long long pos = atomicAdd(&a.ctr->tail, (unsigned long long)nc);
-      for (uint32_t c = 0; c < nc; ++c)
-        st_relaxed_u64(&a.queue[pos + c], ((unsigned long long)s << 32) | c);
-    }
-  }
-}
-
+// ---- scheduler-warp helpers (lane 0 only) ---------------------------------
 __device__ __forceinline__ void raise_error(const EpochArgs &a, unsigned code) {
   atomicCAS(&a.ctr->error, 0u, code);
   atomicExch(&a.ctr->abort, 1u);
 }
 
-__global__ void __launch_bounds__(kBlock) scheduler_kernel(EpochArgs a) {
-  __shared__ unsigned long long s_unit;
-  __shared__ unsigned long long s_ticket;
-  __shared__ __align__(16) float s_fac[kMaxFactors];
-  const int tid = threadIdx.x;
-  uint64_t g0 = 0;
-  long long c0 = 0, c1 = 0, c2 = 0;
+// Pop the unit at ticket t (spinning until published), or kStop.
+__device__ __forceinline__ unsigned long long pop_unit(const EpochArgs &a, unsigned long long &t) {
+  t = atomicAdd(&a.ctr->head, 1ull);
+  if (t >= a.total_units) return kStop;
+  unsigned long long u = ld_acquire_u64(&a.queue[t]);
+  if (u == Q_EMPTY) {
+    const uint64_t start = globaltimer();
+    for (unsigned spin = 0;; ++spin) {
+      __nanosleep(spin < 64 ? 32 : 256);
+      u = ld_acquire_u64(&a.queue[t]);
+      if (u != Q_EMPTY) break;
+      if ((spin & 63) == 63) {
+        if (ld_relaxed_u32(&a.ctr->abort)) return kStop;
+        if (globaltimer() - start > a.watchdog_ns) {
+          raise_error(a, ERR_WATCHDOG);
+          return kStop;
+        }
+      }
+    }
+  }
+  if ((u >> 32) >= a.nitems) {
+    raise_error(a, ERR_BAD_UNIT);
+    return kStop;
+  }
+  return u;
+}
 
-  for (;;) {
-    if (tid == 0) {
-      if (a.trace) { g0 = globaltimer(); c0 = clock64(); }
-      unsigned long long u = kStop;
-      const unsigned long long t = atomicAdd(&a.ctr->head, 1ull);
-      if (t < a.total_units) {
-        u = ld_acquire_u64(&a.queue[t]);
-        if (u == Q_EMPTY) {
-          const uint64_t start = globaltimer();
-          for (unsigned spin = 0;; ++spin) {
-            __nanosleep(spin < 64 ? 32 : 256);
-            u = ld_acquire_u64(&a.queue[t]);
-            if (u != Q_EMPTY) break;
-            if ((spin & 63) == 63) {
-              if (ld_volatile_u32(&a.ctr->abort)) { u = kStop; break; }
-              if (globaltimer() - start > a.watchdog_ns) { raise_error(a, ERR_WATCHDOG); u = kStop; break; }
+// Completion of one unit.  Memory-model pattern (as in cooperative-groups
+// grid sync): the compute warps' stores are ordered before this thread's
+// gpu-scope fence by the named barrier; fence + relaxed RMW = release; an RMW
+// observing the last decrement + fence = acquire.
+__device__ __forceinline__ void release_unit(const EpochArgs &a, uint32_t item) {
+  const DItem &it = a.items[item];
+  const uint32_t nchunks = __ldg(&it.nchunks);
+  __threadfence();
+  if (nchunks > 1) {
+    const unsigned c = atomicAdd(&a.chunk_done[item], 1u);
+    if (c + 1 != nchunks) return;
+    __threadfence();  // acquire the other chunks' stores before releasing them on
+  }
+  const uint32_t nsucc = __ldg(&it.nsucc), off = __ldg(&it.succ_off);
+  for (uint32_t i = 0; i < nsucc; ++i) {
+    const uint32_t s = __ldg(&a.succ[off + i]);
+    if (atomicSub(&a.pending[s], 1) == 1) {
+      __threadfence();
+      const uint32_t nc = __ldg(&a.items[s].nchunks);
+      const unsigned long long pos = atomicAdd(&a.ctr->tail, (unsigned long long)nc);
+      for (uint32_t c = 0; c < nc; ++c) st_relaxed_u64(&a.queue[pos + c], ((unsigned long long)s << 32) | c);
+    }
+  }
+}
+
+// ---- mbarrier (compute warps -> scheduler warp: "unit done") -------------
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+// Non-blocking: has the phase with this parity completed?
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Scheduler-warp state (lane 0): the unit held in each slot and whether it
+// still awaits release; trace stamps of that unit.
+struct SlotState {
+  unsigned long long unit;
+  unsigned parity;      // parity of the slot's next EMPTY phase
+  bool unreleased;
+  uint64_t g0;          // trace: globaltimer at pop start
+  long long pop_cyc, body_c0;
+  unsigned long long ticket;
+};
+
+__device__ __forceinline__ void finish_slot(const EpochArgs &a, SlotState &s) {
+  const long long c1 = a.trace ? clock64() : 0;
+  release_unit(a, (uint32_t)(s.unit >> 32));
+  s.unreleased = false;
+  if (a.trace) {
+    const long long c2 = clock64();
+    a.trace[4 * s.ticket + 0] = s.g0;
+    a.trace[4 * s.ticket + 1] = (unsigned long long)s.pop_cyc;
+    a.trace[4 * s.ticket + 2] = (unsigned long long)(c1 - s.body_c0);
+    a.trace[4 * s.ticket + 3] = (unsigned long long)(c2 - c1);
+    a.trace_item[s.ticket] = (uint32_t)(s.unit >> 32);
+  }
+}
+
+// Block until the unit in slot s is done by the compute warps, then release it.
+__device__ __forceinline__ void drain_slot(const EpochArgs &a, SlotState &s, uint64_t *empty) {
+  if (!s.unreleased) return;
+  while (!mbar_test(empty, s.parity)) {
+  }
+  s.parity ^= 1;
+  finish_slot(a, s);
+}
+
+// If the unit in slot s is already done, release it now (non-blocking).
+__device__ __forceinline__ void poll_slot(const EpochArgs &a, SlotState &s, uint64_t *empty) {
+  if (s.unreleased && mbar_test(empty, s.parity)) {
+    s.parity ^= 1;
+    finish_slot(a, s);
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) scheduler_kernel(EpochArgs a) {
+  __shared__ unsigned long long s_unit[2];
+  __shared__ __align__(8) uint64_t s_empty[2];
+  __shared__ __align__(16) float s_fac[2][kMaxFactors];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_empty[0], kCompute / 32);
+    mbar_init(&s_empty[1], kCompute / 32);
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ================= scheduler warp =================
+    // Invariant: the scheduler never spins on the queue while a finished unit
+    // of this CTA is unreleased (it polls the other slot while waiting), so a
+    // CTA cannot starve the very successor it is waiting for.
+    SlotState st[2];
+    for (int b = 0; b < 2; ++b) {
+      st[b].unit = kStop;
+      st[b].parity = 0;
+      st[b].unreleased = false;
+    }
+    for (unsigned u = 0;; ++u) {
+      const int b = u & 1;
+      unsigned long long unit = kStop;
+      if (lane == 0) {
+        drain_slot(a, st[b], &s_empty[b]);        // slot b's previous unit (u-2)
+        const uint64_t g0 = a.trace ? globaltimer() : 0;
+        const long long c0 = a.trace ? clock64() : 0;
+        const unsigned long long t = atomicAdd(&a.ctr->head, 1ull);
+        if (t < a.total_units) {
+          unit = ld_acquire_u64(&a.queue[t]);
+          if (unit == Q_EMPTY) {
+            const uint64_t start = globaltimer();
+            for (unsigned spin = 0;; ++spin) {
+              poll_slot(a, st[b ^ 1], &s_empty[b ^ 1]);
+              __nanosleep(spin < 64 ? 32 : 256);
+              unit = ld_acquire_u64(&a.queue[t]);
+              if (unit != Q_EMPTY) break;
+              if ((spin & 63) == 63) {
+                if (ld_relaxed_u32(&a.ctr->abort)) {
+                  unit = kStop;
+                  break;
+                }
+                if (globaltimer() - start > a.watchdog_ns) {
+                  raise_error(a, ERR_WATCHDOG);
+                  unit = kStop;
+                  break;
+                }
+              }
             }
           }
+          if (unit != kStop && (unit >> 32) >= a.nitems) {
+            raise_error(a, ERR_BAD_UNIT);
+            unit = kStop;
+          }
         }
-        if (u != kStop && (u >> 32) >= a.nitems) { raise_error(a, ERR_BAD_UNIT); u = kStop; }
+        st[b].unit = unit;
+        st[b].unreleased = unit != kStop;
+        if (a.trace) {
+          st[b].g0 = g0;
+          st[b].body_c0 = clock64();
+          st[b].pop_cyc = st[b].body_c0 - c0;
+          st[b].ticket = t;
+        }
       }
-      s_unit = u;
-      s_ticket = t;
-      if (a.trace) c1 = clock64();
-    }
-    __syncthreads();
-    const unsigned long long u = s_unit;
-    if (u == kStop) break;
-    const uint32_t item = (uint32_t)(u >> 32);
-    const uint32_t chunk = (uint32_t)u;
-    const DItem it = a.items[item];
-    const uint64_t b = (uint64_t)chunk * a.chunk_elems;
-    const uint64_t e = min(it.n, b + a.chunk_elems);
-    switch (it.kind) {
-      case K_SCAL: {
-        const uint32_t k = it.k;
-        for (uint32_t j = tid; j < k; j += kBlock) s_fac[j] = __ldg(a.factors + it.arg + j);
-        __syncthreads();
-        scal_range(reinterpret_cast<float *>(it.x) + b, e - b, s_fac, k);
+      unit = __shfl_sync(0xffffffffu, unit, 0);
+      if (unit != kStop) {
+        const DItem &it = a.items[(uint32_t)(unit >> 32)];
+        if (__ldg(&it.kind) == K_SCAL) {
+          const uint32_t k = __ldg(&it.k), off = __ldg(&it.arg);
+          for (uint32_t j = lane; j < k; j += 32) s_fac[b][j] = __ldg(a.factors + off + j);
+        }
+      }
+      if (lane == 0) s_unit[b] = unit;
+      __syncwarp();
+      bar_arrive(kBarFull + b, kBlock);
+      if (unit == kStop) {
+        if (lane == 0) drain_slot(a, st[b ^ 1], &s_empty[b ^ 1]);   // unit u-1 still in flight
         break;
       }
+    }
+    return;
+  }
+
+  // ================= compute warps =================
+  const int tid = threadIdx.x - 32;
+  for (unsigned u = 0;; ++u) {
+    const int b = u & 1;
+    bar_sync(kBarFull + b, kBlock);
+    const unsigned long long unit = s_unit[b];
+    if (unit == kStop) break;
+    const uint32_t item = (uint32_t)(unit >> 32);
+    const uint32_t chunk = (uint32_t)unit;
+    const DItem it = a.items[item];
+    const uint64_t lo = (uint64_t)chunk * a.chunk_elems;
+    const uint64_t hi = min(it.n, lo + a.chunk_elems);
+    switch (it.kind) {
+      case K_SCAL:
+        scal_range<4>(reinterpret_cast<float *>(it.x) + lo, hi - lo, s_fac[b], it.k, tid);
+        break;
       case K_AXPY:
-        axpy_range(reinterpret_cast<const float *>(it.x) + b, reinterpret_cast<float *>(it.y) + b, e - b,
-                   __uint_as_float(it.arg));
+        axpy_range(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, hi - lo,
+                   __uint_as_float(it.arg), tid);
         break;
       case K_COPY:
-        copy_range(reinterpret_cast<const float *>(it.x) + b, reinterpret_cast<float *>(it.y) + b, e - b);
+        copy_range(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, hi - lo, tid);
         break;
       default:
         if (tid == 0) raise_error(a, ERR_BAD_KIND);
         break;
     }
-    __syncthreads();
-    if (tid == 0) {
-      if (a.trace) c2 = clock64();
-      release_unit(a, item, it);
-      if (a.trace) {
-        const unsigned long long t = s_ticket;
-        const long long c3 = clock64();
-        a.trace[4 * t + 0] = g0;
-        a.trace[4 * t + 1] = (unsigned long long)(c1 - c0);
-        a.trace[4 * t + 2] = (unsigned long long)(c2 - c1);
-        a.trace[4 * t + 3] = (unsigned long long)(c3 - c2);
-        a.trace_item[t] = item;
-      }
-    }
+    // this warp's stores precede the arrive (mbarrier.arrive releases at CTA
+    // scope; __syncwarp orders the other lanes' stores before lane 0's arrive)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s_empty[b]);
   }
 }
 
