@@ -136,6 +136,10 @@ int bt_data_partition(bt_runtime *rt, bt_handle h, uint32_t nparts);
  * partitioned / i out of range). */
 int bt_data_get_sub_data(bt_runtime *rt, bt_handle h, uint32_t i, bt_handle *out);
 
+/* All parts at once: out[i] = part i for i < nparts (nparts must equal the
+ * partition's count).  -EINVAL otherwise. */
+int bt_data_get_children(bt_runtime *rt, bt_handle h, bt_handle *out, uint32_t nparts);
+
 /* Undo bt_data_partition; later tasks on h are ordered after every earlier task
  * on any part.  -EINVAL if not partitioned, -EBUSY if a part is itself
  * partitioned or acquired. */

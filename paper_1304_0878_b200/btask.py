@@ -67,6 +67,7 @@ _SIGS = {
     "bt_data_lookup": (_c.c_int, [_c.c_void_p, _c.c_void_p, _P(bt_handle)]),
     "bt_data_partition": (_c.c_int, [_c.c_void_p, bt_handle, _c.c_uint32]),
     "bt_data_get_sub_data": (_c.c_int, [_c.c_void_p, bt_handle, _c.c_uint32, _P(bt_handle)]),
+    "bt_data_get_children": (_c.c_int, [_c.c_void_p, bt_handle, _P(bt_handle), _c.c_uint32]),
     "bt_data_unpartition": (_c.c_int, [_c.c_void_p, bt_handle]),
     "bt_data_set_rank": (_c.c_int, [_c.c_void_p, bt_handle, _c.c_int]),
     "bt_data_distribute_block": (_c.c_int, [_c.c_void_p, bt_handle]),
@@ -167,12 +168,14 @@ class Runtime:
         return self.sub_handles(h, nparts)
 
     def sub_handles(self, h: int, nparts: int) -> list:
+        out = np.zeros(nparts, np.uint64)
+        self._check(bt_data_get_children(self.rt, h, _u64p(out), nparts), "bt_data_get_children")
+        return out.tolist()
+
+    def sub_handle(self, h: int, i: int) -> int:
         out = bt_handle()
-        subs = []
-        for i in range(nparts):
-            self._check(bt_data_get_sub_data(self.rt, h, i, ctypes.byref(out)), "bt_data_get_sub_data")
-            subs.append(out.value)
-        return subs
+        self._check(bt_data_get_sub_data(self.rt, h, i, ctypes.byref(out)), "bt_data_get_sub_data")
+        return out.value
 
     def unpartition(self, h: int):
         self._check(bt_data_unpartition(self.rt, h), "bt_data_unpartition")

@@ -775,6 +775,16 @@ int bt_data_get_sub_data(bt_runtime *rt, bt_handle h, uint32_t i, bt_handle *out
   return 0;
 }
 
+int bt_data_get_children(bt_runtime *rt, bt_handle h, bt_handle *out, uint32_t nparts) {
+  if (!rt || !out) return -EINVAL;
+  uint32_t s = resolve(rt, h);
+  if (s == NONE) return fail(rt, -ENOENT, "attempt to use unregistered pointer");
+  const Slot &p = rt->slots[s];
+  if (!p.nparts || nparts != p.nparts) return fail(rt, -EINVAL, "handle has %u parts, not %u", p.nparts, nparts);
+  for (uint32_t i = 0; i < nparts; ++i) out[i] = make_handle(rt, p.first_child + i);
+  return 0;
+}
+
 int bt_data_unpartition(bt_runtime *rt, bt_handle h) {
   if (int r = check_live(rt)) return r;
   uint32_t s = resolve(rt, h);
