@@ -195,6 +195,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--ref-tiles", type=int, default=64)
+    ap.add_argument("--chunk-bytes", type=int, default=0, help="fixed work-unit size (0 = adaptive)")
+    ap.add_argument("--host-threads", type=int, default=0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -229,7 +231,8 @@ def main():
 
     stream = torch.cuda.current_stream(dev)
     flags = B.BT_FLAG_NO_FUSION if args.no_fusion else 0
-    rt = B.Runtime(device=local, stream=stream.cuda_stream, rank=0, nranks=1, flags=flags)
+    rt = B.Runtime(device=local, stream=stream.cuda_stream, rank=0, nranks=1, flags=flags,
+                   chunk_bytes=args.chunk_bytes, host_threads=args.host_threads)
 
     # ---- device-resident inputs (registered once, outside the timed region)
     x = synth_tile_values(torch, elems, 1000 + rank, dev)

@@ -23,14 +23,15 @@
 // Two insertion paths produce identical DAGs up to item numbering:
 //  * sequential (any codelet): add_scal / add_task;
 //  * parallel lanes for long runs of SCAL tasks: a SCAL touches one handle,
-//    so the stream decomposes by handle.  Lane p owns the handles with
-//    slot % P == p, processes their tasks in submission order into
-//    lane-local items ("tagged" ids, bit 31), then merge() renumbers them
-//    into the global item array.
+//    so the stream decomposes by handle.  Lane p owns the handles of slot
+//    blocks (slot >> 6) % P == p, sorts its tasks by handle (stable) and
+//    turns each handle's run into lane-local items ("tagged" ids, bit 31);
+//    merge() renumbers them into the global item array.
 #pragma once
 #include <stdint.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 #include <memory>
 #include <utility>
@@ -97,6 +98,8 @@ struct LaneEntry {
 };
 
 struct alignas(64) Lane {
+  vec<uint32_t> cnt;                  // lane_runs scratch: per local slot counters
+  vec<uint32_t> tasks;                // lane_runs scratch: task index per sorted factor
   vec<HItem> items;
   vec<uint64_t> edges;                // (pred << 32) | succ, ids possibly TAGged
   vec<float> fpool;
@@ -210,9 +213,16 @@ class Builder {
   void unpartition_state(DepState &parent, DepState *parts, uint32_t nparts);
 
   // ---- parallel lanes (SCAL runs) -------------------------------------
-  // Process one SCAL on slot e.slot owned by this lane (no other thread
-  // touches deps[e.slot] or the SCAL items whose slot0 is e.slot).
-  void lane_scal(Lane &L, DepState &st, const LaneEntry &e, uint64_t x, uint64_t n);
+  // Process all of a lane's entries at once: a stable counting sort by slot
+  // puts each handle's factors contiguously (submission order kept), then
+  // every run becomes items without further copies (factor lists point into
+  // the sorted lane pool).  `chunks[c]` / `counts[c]` are the entries bucketed
+  // by chunk c of the stream (chunk order = submission order); `loc` maps an
+  // owned slot to a dense local index < nlocal and `slot_of` back; `geom(s)`
+  // gives the slot's (device address, elements).
+  template <class Loc, class SlotOf, class Geom>
+  void lane_runs(Lane &L, const LaneEntry *const *chunks, const size_t *counts, int nchunks, DepState *deps,
+                 uint32_t nlocal, Loc &&loc, SlotOf &&slot_of, Geom &&geom);
   // Renumber lane items into the global arrays; deps[] of touched slots fixed.
   // Runs lane p's share on worker p via `par` (a fork/join runner).
   template <class Par>
@@ -325,6 +335,116 @@ void Builder::merge(std::vector<Lane> &lanes, DepState *deps, Par &&par) {
     if (record_tasks)
       for (uint64_t r : L.recorded) task_item[r >> 32] = fix((uint32_t)r);
   });
+}
+
+// ------------------------------------------------------------ lane_runs --
+template <class Loc, class SlotOf, class Geom>
+void Builder::lane_runs(Lane &L, const LaneEntry *const *chunks, const size_t *counts, int nchunks, DepState *deps,
+                        uint32_t nlocal, Loc &&loc, SlotOf &&slot_of, Geom &&geom) {
+  L.clear();
+  size_t n = 0;
+  for (int c = 0; c < nchunks; ++c) n += counts[c];
+  if (n == 0) return;
+  L.cnt.assign(nlocal + 1, 0);
+  uint32_t *cnt = L.cnt.data();
+  for (int c = 0; c < nchunks; ++c)
+    for (size_t j = 0; j < counts[c]; ++j) ++cnt[loc(chunks[c][j].slot) + 1];
+  for (uint32_t l = 1; l <= nlocal; ++l) cnt[l] += cnt[l - 1];
+  L.fpool.resize(n);
+  if (record_tasks) L.tasks.resize(n);
+  float *fs = L.fpool.data();
+  for (int c = 0; c < nchunks; ++c)
+    for (size_t j = 0; j < counts[c]; ++j) {
+      const LaneEntry &e = chunks[c][j];
+      const uint32_t pos = cnt[loc(e.slot)]++;
+      memcpy(fs + pos, &e.fbits, 4);
+      if (record_tasks) L.tasks[pos] = e.task;
+    }
+  // now cnt[l] = end of run l; start of run l = cnt[l-1] (0 for l = 0)
+  uint32_t b = 0;
+  for (uint32_t l = 0; l < nlocal; ++l) {
+    const uint32_t e_ = cnt[l];
+    if (e_ == b) continue;
+    const uint32_t s = slot_of(l);
+    DepState &st = deps[s];
+    fresh(st);
+    const uint32_t m = e_ - b;
+    uint32_t i = 0;
+    uint32_t prev = NONE;
+    if (fusion && st.ext == NONE && st.writer != NONE) {
+      const uint32_t w = st.writer;   // global: this run is the slot's only one in the batch
+      HItem &it = items[w];
+      if (it.kind == 1 && it.slot0 == s && __atomic_load_n(&it.nsucc, __ATOMIC_RELAXED) == 0 && it.k < max_fused) {
+        const uint32_t take = std::min(m, max_fused - it.k);
+        if (!(it.fofs & TAG) && it.k + take <= it.fcap) {
+          memcpy(&fpool[it.fofs + it.k], fs + b, 4ull * take);
+        } else {
+          const uint32_t cap = std::max<uint32_t>(8, 2 * (it.k + take));
+          const uint32_t ofs = (uint32_t)L.fpool.size();
+          L.fpool.resize(ofs + cap);
+          fs = L.fpool.data();
+          memcpy(fs + ofs, &fpool[it.fofs], 4ull * it.k);
+          memcpy(fs + ofs + it.k, fs + b, 4ull * take);
+          it.fofs = TAG | ofs;
+          it.fcap = cap;
+          L.relocated.push_back(w);
+        }
+        if (record_tasks)
+          for (uint32_t q = 0; q < take; ++q) {
+            task_item[L.tasks[b + q]] = w;
+            task_pos[L.tasks[b + q]] = it.k + q;
+          }
+        it.k += take;
+        i = take;
+        L.fused += take;
+        prev = w;
+      }
+    }
+    while (i < m) {
+      const uint32_t take = fusion ? std::min(m - i, max_fused) : 1u;
+      const uint32_t local = (uint32_t)L.items.size();
+      const uint32_t t = TAG | local;
+      const auto g = geom(s);
+      L.items.push_back(HItem{1, take, s, NONE, g.first, 0, g.second, 0, TAG | (b + i), take, 0, 0, NONE});
+      uint32_t np = 0;
+      auto link = [&](uint32_t p) {
+        if (p & TAG) ++L.items[p & ~TAG].nsucc;
+        else __atomic_fetch_add(&items[p].nsucc, 1u, __ATOMIC_RELAXED);
+        L.edges.push_back(((uint64_t)p << 32) | t);
+        ++np;
+      };
+      if (prev != NONE) {
+        link(prev);
+      } else {
+        // first item of the run: writer(s) and readers of the handle (W access)
+        if (st.writer != NONE) link(st.writer);
+        if (st.ext != NONE) {
+          const DepExt &x = exts[st.ext];
+          uint32_t seen_w = st.writer;
+          for (uint32_t q : x.writers)
+            if (q != seen_w) link(q);
+          for (uint32_t q : x.readers) {
+            bool dup = q == st.writer;
+            for (uint32_t r : x.writers) dup |= (r == q);
+            if (!dup) link(q);
+          }
+        }
+      }
+      L.items[local].npred = np;
+      if (record_tasks)
+        for (uint32_t q = 0; q < take; ++q) {
+          L.recorded.push_back(((uint64_t)L.tasks[b + i + q] << 32) | t);
+          task_pos[L.tasks[b + i + q]] = q;
+        }
+      L.fused += take - 1;
+      prev = t;
+      i += take;
+    }
+    st.writer = prev;
+    st.ext = NONE;
+    if (prev & TAG) L.touched.push_back(s);
+    b = e_;
+  }
 }
 
 }  // namespace bt

@@ -985,14 +985,23 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
   }
   DepState *deps = rt->deps.data();
   double tp1 = now_ms();
+  // lane l owns slot blocks (s >> 6) with (s >> 6) % P == l; dense local index
+  const uint32_t nlocal = (uint32_t)((((nslots + 63) >> 6) + P - 1) / P) * 64;
   rt->par([&](int l) {
-    Lane &L = rt->lanes[l];
-    L.clear();
-    for (int c = 0; c < P; ++c)
-      for (const LaneEntry &e : rt->buckets[(size_t)c * P + l]) {
-        const SlotHot &sh = hot[e.slot];
-        B.lane_scal(L, deps[e.slot], e, reinterpret_cast<uint64_t>(sh.dptr), sh.nx);
-      }
+    std::vector<const LaneEntry *> ptrs(P);
+    std::vector<size_t> cnts(P);
+    for (int c = 0; c < P; ++c) {
+      ptrs[c] = rt->buckets[(size_t)c * P + l].data();
+      cnts[c] = rt->buckets[(size_t)c * P + l].size();
+    }
+    const uint32_t up = (uint32_t)P, ul = (uint32_t)l;
+    B.lane_runs(
+        rt->lanes[l], ptrs.data(), cnts.data(), P, deps, nlocal,
+        [up](uint32_t s) { return ((s >> 6) / up) * 64 + (s & 63); },
+        [up, ul](uint32_t loc) { return ((loc >> 6) * up + ul) * 64 + (loc & 63); },
+        [hot](uint32_t s) {
+          return std::pair<uint64_t, uint64_t>(reinterpret_cast<uint64_t>(hot[s].dptr), hot[s].nx);
+        });
   });
   double tp2 = now_ms();
   B.merge(rt->lanes, deps, [&](const std::function<void(int)> &f) { rt->pool->run(f); });

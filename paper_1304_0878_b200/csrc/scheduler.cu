@@ -115,6 +115,23 @@ __device__ __forceinline__ void st8(float *p, const float (&r)[8]) {
 template <int NV>
 __device__ __forceinline__ void chain_apply(float (&v)[NV][8], const float *sf, uint32_t k) {
   uint32_t j = 0;
+  for (; j + 8 <= k; j += 8) {
+    const float4 f4a = *reinterpret_cast<const float4 *>(sf + j);
+    const float4 f4b = *reinterpret_cast<const float4 *>(sf + j + 4);
+    const float fs[8] = {f4a.x, f4a.y, f4a.z, f4a.w, f4b.x, f4b.y, f4b.z, f4b.w};
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const float2 ff = make_float2(fs[jj], fs[jj]);
+#pragma unroll
+      for (int a = 0; a < NV; ++a)
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+          const float2 t = __fmul2_rn(make_float2(v[a][q], v[a][q + 1]), ff);
+          v[a][q] = t.x;
+          v[a][q + 1] = t.y;
+        }
+    }
+  }
   for (; j + 4 <= k; j += 4) {
     const float4 f4 = *reinterpret_cast<const float4 *>(sf + j);
     const float fs[4] = {f4.x, f4.y, f4.z, f4.w};
