@@ -96,6 +96,10 @@ typedef struct bt_config {
   uint64_t epoch_tasks;   /* auto-flush an epoch after this many pending tasks; 0 = never */
   int host_threads;       /* dependency-builder threads (parallel SCAL runs); 0 = min(16, cores) */
   uint32_t parallel_min;  /* shortest SCAL run of a batch built in parallel; 0 = default (16384) */
+  int pipeline_rounds;    /* a long SCAL run is built and launched in this many rounds of
+                             handles, so the device starts while the host still builds;
+                             0 = default (4), 1 = off */
+  uint32_t pipeline_min;  /* shortest SCAL run that is pipelined; 0 = default (131072) */
 } bt_config;
 
 /* Fill *cfg with defaults.  Returns 0. */
@@ -230,6 +234,8 @@ typedef struct bt_stats {
   uint64_t upload_bytes;      /* DAG bytes copied host -> device */
   double host_build_ms;       /* time in the dependency builder (insert + pack) */
   double device_ms;           /* summed persistent-kernel time of completed epochs */
+  double device_span_ms;      /* summed device time from the first launch after a wait to the end
+                                 of that wait's work (overlapping launches counted once) */
   uint32_t grid;              /* persistent CTAs per launch */
   uint32_t block;             /* threads per CTA */
 } bt_stats;

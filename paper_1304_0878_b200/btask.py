@@ -30,14 +30,16 @@ class bt_config(ctypes.Structure):
     _fields_ = [("abi_version", ctypes.c_uint32), ("device", ctypes.c_int), ("stream", ctypes.c_void_p),
                 ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("flags", ctypes.c_uint32),
                 ("chunk_bytes", ctypes.c_uint32), ("max_fused", ctypes.c_uint32), ("ctas_per_sm", ctypes.c_int),
-                ("epoch_tasks", ctypes.c_uint64), ("host_threads", ctypes.c_int), ("parallel_min", ctypes.c_uint32)]
+                ("epoch_tasks", ctypes.c_uint64), ("host_threads", ctypes.c_int), ("parallel_min", ctypes.c_uint32),
+                ("pipeline_rounds", ctypes.c_int), ("pipeline_min", ctypes.c_uint32)]
 
 
 class bt_stats(ctypes.Structure):
     _fields_ = [("tasks_submitted", ctypes.c_uint64), ("tasks_local", ctypes.c_uint64), ("items", ctypes.c_uint64),
                 ("fused_tasks", ctypes.c_uint64), ("edges", ctypes.c_uint64), ("units", ctypes.c_uint64),
                 ("epochs", ctypes.c_uint64), ("upload_bytes", ctypes.c_uint64), ("host_build_ms", ctypes.c_double),
-                ("device_ms", ctypes.c_double), ("grid", ctypes.c_uint32), ("block", ctypes.c_uint32)]
+                ("device_ms", ctypes.c_double), ("device_span_ms", ctypes.c_double), ("grid", ctypes.c_uint32),
+                ("block", ctypes.c_uint32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -113,7 +115,7 @@ class Runtime:
 
     def __init__(self, device: int = -1, stream=None, rank: int = 0, nranks: int = 1, flags: int = 0,
                  chunk_bytes: int = 0, max_fused: int = 0, ctas_per_sm: int = 0, epoch_tasks: int = 0,
-                 host_threads: int = 0, parallel_min: int = 0):
+                 host_threads: int = 0, parallel_min: int = 0, pipeline_rounds: int = 0, pipeline_min: int = 0):
         cfg = bt_config()
         bt_config_init(ctypes.byref(cfg))
         cfg.device, cfg.rank, cfg.nranks, cfg.flags = device, rank, nranks, flags
@@ -121,6 +123,7 @@ class Runtime:
         cfg.chunk_bytes, cfg.max_fused, cfg.ctas_per_sm, cfg.epoch_tasks = chunk_bytes, max_fused, ctas_per_sm, \
             epoch_tasks
         cfg.host_threads, cfg.parallel_min = host_threads, parallel_min
+        cfg.pipeline_rounds, cfg.pipeline_min = pipeline_rounds, pipeline_min
         h = ctypes.c_void_p()
         rc = bt_init(ctypes.byref(cfg), ctypes.byref(h))
         if rc:

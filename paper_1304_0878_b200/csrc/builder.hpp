@@ -93,8 +93,6 @@ struct HItem {
 struct LaneEntry {
   uint32_t slot;
   uint32_t fbits;
-  uint32_t task;       // epoch task index
-  uint32_t pad;
 };
 
 struct alignas(64) Lane {
@@ -220,13 +218,15 @@ class Builder {
   // by chunk c of the stream (chunk order = submission order); `loc` maps an
   // owned slot to a dense local index < nlocal and `slot_of` back; `geom(s)`
   // gives the slot's (device address, elements).
+  // `ctasks[c]` (only read when record_tasks) holds the epoch task index of
+  // each entry of chunks[c].
   template <class Loc, class SlotOf, class Geom>
-  void lane_runs(Lane &L, const LaneEntry *const *chunks, const size_t *counts, int nchunks, DepState *deps,
-                 uint32_t nlocal, Loc &&loc, SlotOf &&slot_of, Geom &&geom);
+  void lane_runs(Lane &L, const LaneEntry *const *chunks, const uint32_t *const *ctasks, const size_t *counts,
+                 int nchunks, DepState *deps, uint32_t nlocal, Loc &&loc, SlotOf &&slot_of, Geom &&geom);
   // Renumber lane items into the global arrays; deps[] of touched slots fixed.
   // Runs lane p's share on worker p via `par` (a fork/join runner).
   template <class Par>
-  void merge(std::vector<Lane> &lanes, DepState *deps, Par &&par);
+  void merge(std::vector<Lane> &lanes, size_t nlanes, DepState *deps, Par &&par, int nworkers);
 
   const float *factors(const HItem &it) const { return &fpool[it.fofs]; }
 
@@ -298,8 +298,8 @@ class Builder {
 
 // ---------------------------------------------------------------- merge --
 template <class Par>
-void Builder::merge(std::vector<Lane> &lanes, DepState *deps, Par &&par) {
-  const size_t P = lanes.size();
+void Builder::merge(std::vector<Lane> &lanes, size_t nlanes, DepState *deps, Par &&par, int nworkers) {
+  const size_t P = nlanes;
   std::vector<uint32_t> ibase(P), fbase(P);
   std::vector<size_t> ebase(P);
   size_t ni = items.size(), nf = fpool.size(), ne = edges.size();
@@ -315,7 +315,8 @@ void Builder::merge(std::vector<Lane> &lanes, DepState *deps, Par &&par) {
   items.resize(ni);
   fpool.resize(nf);
   edges.resize(ne);
-  par([&](int p) {
+  par([&](int w) {
+   for (size_t p = (size_t)w; p < P; p += (size_t)nworkers) {
     Lane &L = lanes[p];
     const uint32_t ib = ibase[p], fb = fbase[p];
     auto fix = [ib](uint32_t id) { return (id & TAG) && id != NONE ? ib + (id & ~TAG) : id; };
@@ -334,13 +335,14 @@ void Builder::merge(std::vector<Lane> &lanes, DepState *deps, Par &&par) {
     for (uint32_t s : L.touched) deps[s].writer = fix(deps[s].writer);
     if (record_tasks)
       for (uint64_t r : L.recorded) task_item[r >> 32] = fix((uint32_t)r);
+   }
   });
 }
 
 // ------------------------------------------------------------ lane_runs --
 template <class Loc, class SlotOf, class Geom>
-void Builder::lane_runs(Lane &L, const LaneEntry *const *chunks, const size_t *counts, int nchunks, DepState *deps,
-                        uint32_t nlocal, Loc &&loc, SlotOf &&slot_of, Geom &&geom) {
+void Builder::lane_runs(Lane &L, const LaneEntry *const *chunks, const uint32_t *const *ctasks, const size_t *counts,
+                        int nchunks, DepState *deps, uint32_t nlocal, Loc &&loc, SlotOf &&slot_of, Geom &&geom) {
   L.clear();
   size_t n = 0;
   for (int c = 0; c < nchunks; ++c) n += counts[c];
@@ -358,7 +360,7 @@ void Builder::lane_runs(Lane &L, const LaneEntry *const *chunks, const size_t *c
       const LaneEntry &e = chunks[c][j];
       const uint32_t pos = cnt[loc(e.slot)]++;
       memcpy(fs + pos, &e.fbits, 4);
-      if (record_tasks) L.tasks[pos] = e.task;
+      if (record_tasks) L.tasks[pos] = ctasks[c][j];
     }
   // now cnt[l] = end of run l; start of run l = cnt[l-1] (0 for l = 0)
   uint32_t b = 0;

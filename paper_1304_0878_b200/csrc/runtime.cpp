@@ -42,8 +42,11 @@ constexpr uint64_t kMinChunkElems = 2048;           // adaptive chunking: lower 
 constexpr uint32_t kUnitsPerCta = 16;               // adaptive chunking: target work units per CTA
 constexpr uint32_t kDefaultMaxFused = 256;
 constexpr uint32_t kDefaultParallelMin = 16384;
+constexpr int kDefaultRounds = 4;
+constexpr uint32_t kDefaultPipelineMin = 131072;
+constexpr int kEpochRing = 8;                       // epoch buffers in flight (>= rounds + 2)
 constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;   // 20 s
-constexpr size_t kParallelPack = 1u << 15;          // items above which the pack runs on the pool
+constexpr size_t kParallelPack = 4096;              // items above which the pack runs on the pool
 
 const char *codelet_name(int c) {
   switch (c) {
@@ -66,7 +69,7 @@ struct SlotHot {
   uint32_t gen = 1;
   uint32_t flags = 0;
   int32_t rank = 0;
-  uint32_t pad = 0;
+  uint32_t grp = 0;           // builder group of the slot's 64-slot block (round * P + lane)
   float *dptr = nullptr;      // device address of element 0 (null: no local storage)
   uint64_t nx = 0;
 };
@@ -91,6 +94,7 @@ struct EpochBuf {
   size_t dcap = 0;
   cudaEvent_t start = nullptr, end = nullptr, done = nullptr;
   bool inflight = false;
+  uint64_t seq = 0;           // launch order
   uint64_t units = 0;
   bool traced = false;
   size_t ctr_readback = 0;    // offset of the Counters readback in hblob
@@ -122,9 +126,16 @@ struct bt_runtime {
   Builder builder;
   std::unique_ptr<Pool> pool;
   std::vector<Lane> lanes;
-  std::vector<vec<LaneEntry>> buckets;                  // [chunk * P + lane]
-  EpochBuf ep[2];
+  std::vector<vec<LaneEntry>> buckets;                  // [chunk][round * P + lane]
+  std::vector<vec<uint32_t>> bucket_tasks;              // task indices (record_tasks only)
+  int npool = 1, nrounds = 1;
+  EpochBuf ep[kEpochRing];
   int ep_cur = 0;
+  uint64_t ep_seq = 0;
+  cudaStream_t rstream[2] = {nullptr, nullptr};   // round streams (pipelined SCAL runs)
+  cudaEvent_t ev_fork = nullptr, ev_round[2] = {nullptr, nullptr};
+  cudaEvent_t span_start = nullptr, span_end = nullptr;
+  bool span_open = false;
   bt_stats stats{};
 
   // host-only snapshot storage
@@ -207,6 +218,8 @@ uint32_t alloc_slots(bt_runtime *rt, uint32_t count) {
     h = SlotHot();
     h.gen = gen;
     h.flags = F_LIVE;
+    const uint32_t k = (s + i) >> 6;    // block -> round k % R, lane (k / R) % P
+    h.grp = (k % (uint32_t)rt->nrounds) * (uint32_t)rt->npool + (k / (uint32_t)rt->nrounds) % (uint32_t)rt->npool;
     rt->slots[s + i] = Slot();
     rt->deps[s + i] = DepState();
   }
@@ -330,15 +343,16 @@ inline void range_of(size_t n, int P, int p, size_t &lo, size_t &hi) {
   hi = n * (size_t)(p + 1) / (size_t)P;
 }
 
-int flush_epoch(bt_runtime *rt) {
+int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   Builder &B = rt->builder;
   if (B.items.empty()) {
     B.next_epoch();
     return 0;
   }
+  if (!stream) stream = rt->stream;
   const double t0 = now_ms();
   EpochBuf &e = rt->ep[rt->ep_cur];
-  rt->ep_cur ^= 1;
+  rt->ep_cur = (rt->ep_cur + 1) % kEpochRing;
   if (int r = retire(rt, e)) return r;
 
   const size_t N = B.items.size();
@@ -479,9 +493,13 @@ int flush_epoch(bt_runtime *rt) {
   }
 
   char *d = e.dblob;
-  CUDA_TRY(rt, cudaMemcpyAsync(d, h, upload, cudaMemcpyHostToDevice, rt->stream));
-  if (U > U0) CUDA_TRY(rt, cudaMemsetAsync(d + o_queue + 8 * U0, 0xFF, 8 * (U - U0), rt->stream));
-  CUDA_TRY(rt, cudaMemsetAsync(d + o_cdone, 0, 4 * N, rt->stream));
+  if (!rt->span_open) {
+    CUDA_TRY(rt, cudaEventRecord(rt->span_start, stream));
+    rt->span_open = true;
+  }
+  CUDA_TRY(rt, cudaMemcpyAsync(d, h, upload, cudaMemcpyHostToDevice, stream));
+  if (U > U0) CUDA_TRY(rt, cudaMemsetAsync(d + o_queue + 8 * U0, 0xFF, 8 * (U - U0), stream));
+  CUDA_TRY(rt, cudaMemsetAsync(d + o_cdone, 0, 4 * N, stream));
 
   EpochArgs a{};
   a.items = reinterpret_cast<const DItem *>(d + o_items);
@@ -499,13 +517,14 @@ int flush_epoch(bt_runtime *rt) {
   a.nitems = (uint32_t)N;
   const int grid = (int)std::min<uint64_t>((uint64_t)rt->grid_max, U);
 
-  CUDA_TRY(rt, cudaEventRecord(e.start, rt->stream));
-  CUDA_TRY(rt, launch_epoch(a, grid, rt->stream));
-  CUDA_TRY(rt, cudaEventRecord(e.end, rt->stream));
-  CUDA_TRY(rt, cudaMemcpyAsync(h + o_readback, d + o_ctr, 64, cudaMemcpyDeviceToHost, rt->stream));
-  if (traced) CUDA_TRY(rt, cudaMemcpyAsync(h + o_trace_h, d + o_trace, 36 * U, cudaMemcpyDeviceToHost, rt->stream));
-  CUDA_TRY(rt, cudaEventRecord(e.done, rt->stream));
+  CUDA_TRY(rt, cudaEventRecord(e.start, stream));
+  CUDA_TRY(rt, launch_epoch(a, grid, stream));
+  CUDA_TRY(rt, cudaEventRecord(e.end, stream));
+  CUDA_TRY(rt, cudaMemcpyAsync(h + o_readback, d + o_ctr, 64, cudaMemcpyDeviceToHost, stream));
+  if (traced) CUDA_TRY(rt, cudaMemcpyAsync(h + o_trace_h, d + o_trace, 36 * U, cudaMemcpyDeviceToHost, stream));
+  CUDA_TRY(rt, cudaEventRecord(e.done, stream));
   e.inflight = true;
+  e.seq = ++rt->ep_seq;
   e.units = U;
   e.traced = traced;
   e.ctr_readback = o_readback;
@@ -526,12 +545,21 @@ int flush_epoch(bt_runtime *rt) {
 
 int wait_all(bt_runtime *rt) {
   if (int r = flush_epoch(rt)) return r;
+  if (rt->span_open) CUDA_TRY(rt, cudaEventRecord(rt->span_end, rt->stream));
   // retire in launch order (older first)
-  EpochBuf &older = rt->ep[rt->ep_cur];
-  EpochBuf &newer = rt->ep[rt->ep_cur ^ 1];
-  if (int r = retire(rt, older)) return r;
-  if (int r = retire(rt, newer)) return r;
+  for (;;) {
+    EpochBuf *next = nullptr;
+    for (auto &e : rt->ep)
+      if (e.inflight && (!next || e.seq < next->seq)) next = &e;
+    if (!next) break;
+    if (int r = retire(rt, *next)) return r;
+  }
   CUDA_TRY(rt, cudaStreamSynchronize(rt->stream));
+  if (rt->span_open) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, rt->span_start, rt->span_end) == cudaSuccess) rt->stats.device_span_ms += ms;
+    rt->span_open = false;
+  }
   return 0;
 }
 
@@ -564,6 +592,9 @@ int bt_init(const bt_config *cfg_in, bt_runtime **out) {
   if (cfg.chunk_bytes != 0 && cfg.chunk_bytes < 32) return -EINVAL;
   if (cfg.host_threads < 0) return -EINVAL;
   if (cfg.parallel_min == 0) cfg.parallel_min = kDefaultParallelMin;
+  if (cfg.pipeline_rounds == 0) cfg.pipeline_rounds = kDefaultRounds;
+  if (cfg.pipeline_rounds < 1 || cfg.pipeline_rounds > kEpochRing - 2) return -EINVAL;
+  if (cfg.pipeline_min == 0) cfg.pipeline_min = kDefaultPipelineMin;
 
   bt_runtime *rt = new (std::nothrow) bt_runtime();
   if (!rt) return -ENOMEM;
@@ -575,8 +606,11 @@ int bt_init(const bt_config *cfg_in, bt_runtime **out) {
   int threads = cfg.host_threads;
   if (threads == 0) threads = (int)std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency()));
   rt->pool.reset(new Pool(threads));
-  rt->lanes.resize(threads);
-  rt->buckets.resize((size_t)threads * threads);
+  rt->lanes.resize((size_t)threads * cfg.pipeline_rounds);   // [lane * R + round] when not pipelined
+  rt->npool = threads;
+  rt->nrounds = cfg.pipeline_rounds;
+  rt->buckets.resize((size_t)threads * threads * cfg.pipeline_rounds);   // [chunk][round * P + lane]
+  rt->bucket_tasks.resize(rt->buckets.size());
 
   if (!rt->host_only) {
     int ndev = 0;
@@ -626,6 +660,17 @@ int bt_init(const bt_config *cfg_in, bt_runtime **out) {
         return -ENOMEM;
       }
     }
+    if (cudaEventCreate(&rt->span_start) != cudaSuccess || cudaEventCreate(&rt->span_end) != cudaSuccess ||
+        cudaEventCreateWithFlags(&rt->ev_fork, cudaEventDisableTiming) != cudaSuccess) {
+      delete rt;
+      return -ENOMEM;
+    }
+    for (int i = 0; i < 2; ++i)
+      if (cudaStreamCreateWithFlags(&rt->rstream[i], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&rt->ev_round[i], cudaEventDisableTiming) != cudaSuccess) {
+        delete rt;
+        return -ENOMEM;
+      }
     // keep freed replicas in the pool (register/unregister loops reuse them)
     cudaMemPool_t mp;
     if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
@@ -653,6 +698,13 @@ int bt_shutdown(bt_runtime *rt) {
       if (e.end) cudaEventDestroy(e.end);
       if (e.done) cudaEventDestroy(e.done);
     }
+    for (int i = 0; i < 2; ++i) {
+      if (rt->rstream[i]) cudaStreamDestroy(rt->rstream[i]);
+      if (rt->ev_round[i]) cudaEventDestroy(rt->ev_round[i]);
+    }
+    if (rt->ev_fork) cudaEventDestroy(rt->ev_fork);
+    if (rt->span_start) cudaEventDestroy(rt->span_start);
+    if (rt->span_end) cudaEventDestroy(rt->span_end);
     if (rt->own_stream) cudaStreamDestroy(rt->stream);
   }
   delete rt;
@@ -894,21 +946,27 @@ int submit(bt_runtime *rt, int codelet, float scalar, bt_handle h0, bt_handle h1
   return 0;
 }
 
-// Lane owning slot s: blocks of 64 consecutive slots (768 bytes of DepState)
-// per lane, so that lanes never write the same cache line.
-inline uint32_t lane_of(uint32_t s, int P) { return (s >> 6) % (uint32_t)P; }
-
-// A run of SCAL tasks [i0, i1) built on the pool: phase 1 validates and
-// buckets tasks by owning lane (slot % P); phase 2 runs each lane's tasks in
-// submission order; merge renumbers.  Returns 1 (nothing changed) if any task
-// of the run would fail, so that the caller replays it sequentially and stops
-// at the first error exactly like bt_insert_task.
+// A run of SCAL tasks [i0, i1) built on the pool.  Handles are grouped in
+// blocks of 64 consecutive slots (768 bytes of DepState, so lanes never share
+// a cache line); block k belongs to round k % R and lane (k / R) % P.
+//   phase 1 (per chunk of the stream): validate, bucket by (round, lane);
+//   phase 2 (per round, per lane): stable per-handle sort, runs -> items;
+//   merge:  renumber the lanes' items into the epoch.
+// Pipelined (R > 1, GPU runtime, long run): each round is flushed as its own
+// epoch on one of two round streams as soon as it is built, so the device
+// runs round r while the host builds round r+1 (rounds touch disjoint
+// handles; a fork/join of events orders them after earlier work and before
+// later work on the runtime's stream).  Returns 1 (nothing changed) if any
+// task of the run would fail, so that the caller replays it sequentially and
+// stops at the first error exactly like bt_insert_task.
 int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scalars, const bt_handle *h0, size_t i0,
                       size_t i1) {
   const int P = rt->pool->size();
   const size_t n = i1 - i0;
   Builder &B = rt->builder;
-  const uint64_t tbase = B.ntasks;
+  const bool pipelined = !rt->host_only && rt->cfg.pipeline_rounds > 1 && n >= rt->cfg.pipeline_min;
+  const int R = rt->nrounds;              // groups are fixed per slot (SlotHot::grp); a
+  const uint32_t G = (uint32_t)(P * R);   // non-pipelined run builds all rounds, then merges
   const int myrank = rt->cfg.rank;
   const bool host_only = rt->host_only;
   std::vector<int> bad(P, 0);
@@ -916,44 +974,55 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
   const size_t nslots = rt->hot.size();
   const SlotHot *hot = rt->hot.data();
   static const bool dbg = getenv("BT_DEBUG_TIMING") != nullptr;
+  // task indices are epoch-relative; a pipelined run starts a fresh epoch
+  if (pipelined && !B.items.empty())
+    if (int r = flush_epoch(rt)) return r;
+  const uint64_t tbase = B.ntasks;
+  const bool record = B.record_tasks;
   double tp0 = now_ms();
   rt->par([&](int c) {
     size_t lo, hi;
     range_of(n, P, c, lo, hi);
     // this chunk's buckets, moved to the stack while filling (no false sharing
     // of vector headers between threads)
-    std::vector<vec<LaneEntry>> mine(P);
-    for (int l = 0; l < P; ++l) {
-      mine[l].swap(rt->buckets[(size_t)c * P + l]);
-      mine[l].clear();
+    std::vector<vec<LaneEntry>> mine(G);
+    std::vector<vec<uint32_t>> mine_t(record ? G : 0);
+    for (uint32_t g = 0; g < G; ++g) {
+      mine[g].swap(rt->buckets[(size_t)c * G + g]);
+      mine[g].clear();
+      if (record) {
+        mine_t[g].swap(rt->bucket_tasks[(size_t)c * G + g]);
+        mine_t[g].clear();
+      }
     }
     struct Restore {
       std::vector<vec<LaneEntry>> &m;
+      std::vector<vec<uint32_t>> &mt;
       bt_runtime *rt;
-      int c, P;
+      int c;
+      uint32_t G;
       ~Restore() {
-        for (int l = 0; l < P; ++l) m[l].swap(rt->buckets[(size_t)c * P + l]);
+        for (uint32_t g = 0; g < G; ++g) m[g].swap(rt->buckets[(size_t)c * G + g]);
+        for (uint32_t g = 0; g < (uint32_t)mt.size(); ++g) mt[g].swap(rt->bucket_tasks[(size_t)c * G + g]);
       }
-    } restore{mine, rt, c, P};
+    } restore{mine, mine_t, rt, c, G};
     uint64_t rem = 0;
     for (size_t j = lo; j < hi; ++j) {
-      if (codelets[i0 + j] != BT_CL_SCAL) {
-        bad[c] = 1;
-        return;
-      }
       const bt_handle h = h0[i0 + j];
-      const uint64_t idx = h & 0xFFFFFFFFull;
-      if (idx == 0 || idx > nslots) {
+      const uint32_t s = (uint32_t)(h & 0xFFFFFFFFull) - 1u;   // handle index 0 wraps to UINT32_MAX
+      if (__builtin_expect(codelets[i0 + j] != BT_CL_SCAL || s >= nslots, 0)) {
         bad[c] = 1;
         return;
       }
-      const uint32_t s = (uint32_t)(idx - 1);
       const SlotHot &sh = hot[s];
-      if (sh.gen != (uint32_t)(h >> 32) || (sh.flags & (F_LIVE | F_PARTITIONED | F_BLOCKED)) != F_LIVE) {
+      if (__builtin_expect(sh.gen != (uint32_t)(h >> 32) ||
+                               (sh.flags & (F_LIVE | F_PARTITIONED | F_BLOCKED)) != F_LIVE ||
+                               (!sh.dptr && !host_only),
+                           0)) {
         bad[c] = 1;
         return;
       }
-      if (sh.rank != myrank) {
+      if (__builtin_expect(sh.rank != myrank, 0)) {
         if (sh.rank < 0) {
           bad[c] = 1;
           return;
@@ -961,16 +1030,11 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
         ++rem;
         continue;
       }
-      if (!sh.dptr && !host_only) {
-        bad[c] = 1;
-        return;
-      }
       LaneEntry e;
       e.slot = s;
       memcpy(&e.fbits, &scalars[i0 + j], 4);
-      e.task = (uint32_t)(tbase + j);
-      e.pad = 0;
-      mine[lane_of(s, P)].push_back(e);
+      mine[sh.grp].push_back(e);
+      if (record) mine_t[sh.grp].push_back((uint32_t)(tbase + j));
     }
     remote[c] = rem;
   });
@@ -983,35 +1047,66 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
     B.task_item.resize(tbase + n, NONE);
     B.task_pos.resize(tbase + n, 0);
   }
-  DepState *deps = rt->deps.data();
-  double tp1 = now_ms();
-  // lane l owns slot blocks (s >> 6) with (s >> 6) % P == l; dense local index
-  const uint32_t nlocal = (uint32_t)((((nslots + 63) >> 6) + P - 1) / P) * 64;
-  rt->par([&](int l) {
-    std::vector<const LaneEntry *> ptrs(P);
-    std::vector<size_t> cnts(P);
-    for (int c = 0; c < P; ++c) {
-      ptrs[c] = rt->buckets[(size_t)c * P + l].data();
-      cnts[c] = rt->buckets[(size_t)c * P + l].size();
-    }
-    const uint32_t up = (uint32_t)P, ul = (uint32_t)l;
-    B.lane_runs(
-        rt->lanes[l], ptrs.data(), cnts.data(), P, deps, nlocal,
-        [up](uint32_t s) { return ((s >> 6) / up) * 64 + (s & 63); },
-        [up, ul](uint32_t loc) { return ((loc >> 6) * up + ul) * 64 + (loc & 63); },
-        [hot](uint32_t s) {
-          return std::pair<uint64_t, uint64_t>(reinterpret_cast<uint64_t>(hot[s].dptr), hot[s].nx);
-        });
-  });
-  double tp2 = now_ms();
-  B.merge(rt->lanes, deps, [&](const std::function<void(int)> &f) { rt->pool->run(f); });
-  if (dbg) fprintf(stderr, "scal_run_parallel n=%zu P=%d phase1 %.3f ms phase2 %.3f ms merge %.3f ms\n", n, P,
-                   tp1 - tp0, tp2 - tp1, now_ms() - tp2);
   uint64_t rem = 0;
   for (int c = 0; c < P; ++c) rem += remote[c];
-  B.ntasks += n;
   rt->stats.tasks_submitted += n;
   rt->stats.tasks_local += n - rem;
+  if (pipelined) {
+    CUDA_TRY(rt, cudaEventRecord(rt->ev_fork, rt->stream));
+    for (int i = 0; i < 2; ++i) CUDA_TRY(rt, cudaStreamWaitEvent(rt->rstream[i], rt->ev_fork, 0));
+  }
+  DepState *deps = rt->deps.data();
+  const double tp1 = now_ms();
+  double t_p2 = 0, t_merge = 0, t_flush = 0;
+  // group (r, l) owns slot blocks k = q*G + l*R + r; dense local index q*64 + (s & 63)
+  const uint32_t nlocal = (uint32_t)((((nslots + 63) >> 6) + G - 1) / G) * 64;
+  const int rounds = pipelined ? R : 1;
+  for (int rr = 0; rr < rounds; ++rr) {
+    const double ta = now_ms();
+    rt->par([&](int l) {
+      // non-pipelined: this lane builds its groups of every round in one go
+      for (int r = pipelined ? rr : 0; r < (pipelined ? rr + 1 : R); ++r) {
+        const uint32_t g = (uint32_t)(r * P + l);
+        std::vector<const LaneEntry *> ptrs(P);
+        std::vector<const uint32_t *> tptr(P);
+        std::vector<size_t> cnts(P);
+        for (int c = 0; c < P; ++c) {
+          ptrs[c] = rt->buckets[(size_t)c * G + g].data();
+          tptr[c] = record ? rt->bucket_tasks[(size_t)c * G + g].data() : nullptr;
+          cnts[c] = rt->buckets[(size_t)c * G + g].size();
+        }
+        Lane &L = rt->lanes[(size_t)l * (pipelined ? 1 : R) + (pipelined ? 0 : r)];
+        B.lane_runs(
+            L, ptrs.data(), tptr.data(), cnts.data(), P, deps, nlocal,
+            [G](uint32_t s) { return ((s >> 6) / G) * 64 + (s & 63); },
+            [G, lr = (uint32_t)(l * R + r)](uint32_t loc) { return ((loc >> 6) * G + lr) * 64 + (loc & 63); },
+            [hot](uint32_t s) {
+              return std::pair<uint64_t, uint64_t>(reinterpret_cast<uint64_t>(hot[s].dptr), hot[s].nx);
+            });
+      }
+    });
+    const double tb = now_ms();
+    B.merge(rt->lanes, pipelined ? P : P * R, deps, [&](const std::function<void(int)> &f) { rt->pool->run(f); }, P);
+    const double tc = now_ms();
+    if (pipelined) {
+      B.ntasks = tbase + n;   // the round's epoch accounts the run (its items carry the tasks)
+      cudaStream_t st = rt->rstream[rr & 1];
+      if (int e = flush_epoch(rt, st)) return e;
+      CUDA_TRY(rt, cudaEventRecord(rt->ev_round[rr & 1], st));
+    }
+    t_p2 += tb - ta;
+    t_merge += tc - tb;
+    t_flush += now_ms() - tc;
+  }
+  if (pipelined) {
+    for (int i = 0; i < std::min(R, 2); ++i) CUDA_TRY(rt, cudaStreamWaitEvent(rt->stream, rt->ev_round[i], 0));
+  } else {
+    B.ntasks = tbase + n;
+  }
+  if (dbg)
+    fprintf(stderr,
+            "scal_run_parallel n=%zu P=%d R=%d phase1 %.3f ms phase2 %.3f ms merge %.3f ms flush %.3f ms\n", n, P, R,
+            tp1 - tp0, t_p2, t_merge, t_flush);
   return 0;
 }
 

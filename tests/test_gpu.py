@@ -244,3 +244,36 @@ def test_trace_timestamps(B):
     t, item = tr
     assert t.shape == (4000, 4) and np.all(t[:, 0] > 0)
     assert sorted(item.tolist()) == list(range(4000))
+
+
+@pytest.mark.parametrize("rounds,threads", [(2, 2), (3, 4), (4, 3)])
+def test_pipelined_rounds(B, rounds, threads):
+    """Long SCAL runs built and launched in rounds on two streams (forced on
+    small runs), interleaved with AXPY/COPY tasks and further SCAL runs."""
+    rng = np.random.default_rng(91 + rounds)
+    nbuf, nparts, n = 3, 300, 300 * 64
+    bufs = [W.unit_interval_floats(rng, n) for _ in range(nbuf)]
+    rows = []
+    for blk in range(5):
+        for _ in range(int(rng.integers(2000, 4000))):
+            b = int(rng.integers(0, nbuf))
+            rows.append((W.SCAL, np.float32(rng.uniform(0.9, 1.1)), b, int(rng.integers(0, nparts)), -1, -1))
+        for _ in range(int(rng.integers(1, 20))):
+            b0, b1 = rng.choice(nbuf, 2, replace=False)
+            t = int(rng.integers(0, nparts))
+            rows.append((W.AXPY if rng.random() < .5 else W.COPY, np.float32(0.25), int(b0), t, int(b1), t))
+    tasks = W._tasks(len(rows))
+    for i, r in enumerate(rows):
+        tasks[i] = r
+    p = W.Program(bufs, [nparts] * nbuf, tasks)
+    for fusion in (True, False):
+        compare_program(p, flags=0 if fusion else B.BT_FLAG_NO_FUSION, pipeline_rounds=rounds, pipeline_min=500,
+                        parallel_min=500, host_threads=threads)
+
+
+def test_c5_shape_pipelined_default(B):
+    """The bench's path (default rounds) on a reduced C5: 1024 tiles x 64 sweeps."""
+    p = W.c5_sharded(nx=1024 * 4096, ntiles=1024, sweeps=64)
+    out, stats = run_gpu(p, pipeline_min=1024)
+    assert_bits_equal(out[0], oracle.scal_chain(p.buffers[0], p.meta["factors"]), "C5 reduced, pipelined")
+    assert stats["epochs"] >= 4
