@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libbtask.so")
+LIB_PATH = os.environ.get("BT_LIB_PATH") or os.path.join(_PKG, "libbtask.so")   # override: experiments only
 
 BT_ABI_VERSION = 1
 BT_R, BT_W, BT_RW = 1, 2, 3

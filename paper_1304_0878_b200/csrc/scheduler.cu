@@ -326,6 +326,20 @@ __device__ __forceinline__ bool mbar_test(uint64_t *bar, unsigned parity) {
   return ok != 0;
 }
 
+// Blocking: suspend (mbarrier.try_wait) until the phase with this parity completes;
+// a busy test_wait loop would steal issue slots from the compute warps.
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  const unsigned addr = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  }
+}
+
 // Scheduler-warp state (lane 0): the unit held in each slot and whether it
 // still awaits release; trace stamps of that unit.
 struct SlotState {
@@ -354,8 +368,7 @@ __device__ __forceinline__ void finish_slot(const EpochArgs &a, SlotState &s) {
 // Block until the unit in slot s is done by the compute warps, then release it.
 __device__ __forceinline__ void drain_slot(const EpochArgs &a, SlotState &s, uint64_t *empty) {
   if (!s.unreleased) return;
-  while (!mbar_test(empty, s.parity)) {
-  }
+  mbar_wait(empty, s.parity);
   s.parity ^= 1;
   finish_slot(a, s);
 }
