@@ -115,6 +115,31 @@ __device__ __forceinline__ void st8(float *p, const float (&r)[8]) {
 template <int NV>
 __device__ __forceinline__ void chain_apply(float (&v)[NV][8], const float *sf, uint32_t k) {
   uint32_t j = 0;
+#ifndef BT_FACTOR_UNROLL16
+#define BT_FACTOR_UNROLL16 1
+#endif
+#if BT_FACTOR_UNROLL16
+  for (; j + 16 <= k; j += 16) {
+    const float4 f4a = *reinterpret_cast<const float4 *>(sf + j);
+    const float4 f4b = *reinterpret_cast<const float4 *>(sf + j + 4);
+    const float4 f4c = *reinterpret_cast<const float4 *>(sf + j + 8);
+    const float4 f4d = *reinterpret_cast<const float4 *>(sf + j + 12);
+    const float fs[16] = {f4a.x, f4a.y, f4a.z, f4a.w, f4b.x, f4b.y, f4b.z, f4b.w,
+                          f4c.x, f4c.y, f4c.z, f4c.w, f4d.x, f4d.y, f4d.z, f4d.w};
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+      const float2 ff = make_float2(fs[jj], fs[jj]);
+#pragma unroll
+      for (int a = 0; a < NV; ++a)
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+          const float2 t = __fmul2_rn(make_float2(v[a][q], v[a][q + 1]), ff);
+          v[a][q] = t.x;
+          v[a][q + 1] = t.y;
+        }
+    }
+  }
+#endif
   for (; j + 8 <= k; j += 8) {
     const float4 f4a = *reinterpret_cast<const float4 *>(sf + j);
     const float4 f4b = *reinterpret_cast<const float4 *>(sf + j + 4);
@@ -381,7 +406,10 @@ __device__ __forceinline__ void poll_slot(const EpochArgs &a, SlotState &s, uint
   }
 }
 
-__global__ void __launch_bounds__(kBlock) scheduler_kernel(EpochArgs a) {
+#ifndef BT_MIN_CTAS
+#define BT_MIN_CTAS 3   // 3 x 288 threads per SM: caps registers at 75 (measured best, profiles/r01_summary.md)
+#endif
+__global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel(EpochArgs a) {
   __shared__ unsigned long long s_unit[2];
   __shared__ __align__(8) uint64_t s_empty[2];
   __shared__ __align__(16) float s_fac[2][kMaxFactors];
