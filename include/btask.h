@@ -94,7 +94,7 @@ typedef struct bt_config {
   uint32_t max_fused;     /* max SCAL tasks fused into one work item; 0 = default (256) */
   int ctas_per_sm;        /* persistent CTAs per SM; 0 = maximum occupancy */
   uint64_t epoch_tasks;   /* auto-flush an epoch after this many pending tasks; 0 = never */
-  int host_threads;       /* dependency-builder threads (parallel SCAL runs); 0 = min(16, cores) */
+  int host_threads;       /* dependency-builder threads (parallel SCAL runs); 0 = min(16, cores - 2) */
   uint32_t parallel_min;  /* shortest SCAL run of a batch built in parallel; 0 = default (16384) */
   int pipeline_rounds;    /* a long SCAL run is built and launched in this many rounds of
                              handles, so the device starts while the host still builds;

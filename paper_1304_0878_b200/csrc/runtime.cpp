@@ -604,7 +604,11 @@ int bt_init(const bt_config *cfg_in, bt_runtime **out) {
   rt->builder.max_fused = cfg.max_fused;
   rt->builder.record_tasks = rt->host_only;
   int threads = cfg.host_threads;
-  if (threads == 0) threads = (int)std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency()));
+  if (threads == 0) {
+    // leave two cores to the CUDA driver / caller threads (measured: 14 of 16 beats 16 of 16)
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    threads = (int)std::min<unsigned>(16, hw > 4 ? hw - 2 : hw);
+  }
   rt->pool.reset(new Pool(threads));
   rt->lanes.resize((size_t)threads * cfg.pipeline_rounds);   // [lane * R + round] when not pipelined
   rt->npool = threads;
