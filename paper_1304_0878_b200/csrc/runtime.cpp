@@ -28,7 +28,7 @@
 #include "pool.hpp"
 
 namespace bt {
-cudaError_t launch_epoch(const EpochArgs &args, int grid, cudaStream_t stream);
+cudaError_t launch_epoch(const EpochArgs &args, int grid, cudaStream_t stream, bool release_warp);
 cudaError_t scheduler_occupancy(int *blocks_per_sm, int *block);
 int max_factors();
 }  // namespace bt
@@ -47,6 +47,7 @@ constexpr uint32_t kDefaultPipelineMin = 131072;
 constexpr int kEpochRing = 8;                       // epoch buffers in flight (>= rounds + 2)
 constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;   // 20 s
 constexpr size_t kParallelPack = 4096;              // items above which the pack runs on the pool
+constexpr uint64_t kReleaseWarpBelow = 16384;       // work units smaller than this use the "rw" kernel
 
 const char *codelet_name(int c) {
   switch (c) {
@@ -518,7 +519,11 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   const int grid = (int)std::min<uint64_t>((uint64_t)rt->grid_max, U);
 
   CUDA_TRY(rt, cudaEventRecord(e.start, stream));
-  CUDA_TRY(rt, launch_epoch(a, grid, stream));
+  // small work units are scheduling-bound: use the kernel with a dedicated
+  // release warp; large ones are body-bound: keep all 8 warps computing
+  static const char *kv = getenv("BT_KERNEL");   // "rw" / "sw": experiments only
+  const bool rw = kv ? (kv[0] == 'r') : CE < kReleaseWarpBelow;
+  CUDA_TRY(rt, launch_epoch(a, grid, stream, rw));
   CUDA_TRY(rt, cudaEventRecord(e.end, stream));
   CUDA_TRY(rt, cudaMemcpyAsync(h + o_readback, d + o_ctr, 64, cudaMemcpyDeviceToHost, stream));
   if (traced) CUDA_TRY(rt, cudaMemcpyAsync(h + o_trace_h, d + o_trace, 36 * U, cudaMemcpyDeviceToHost, stream));

@@ -10,8 +10,8 @@
 //                        release when an item's last chunk is done, decrement
 //                                each successor's pending counter; a successor
 //                                reaching 0 is ready: its chunks are appended
-//                                to the queue (atomicAdd(tail) + stores after a
-//                                gpu-scope fence).
+//                                to the queue (atomicAdd(tail), fence.acq_rel,
+//                                relaxed stores).
 //   warps 1..8 (compute) run the task body on the unit's elements:
 //            SCAL   x[i] = x[i]*f_1*...*f_k   (k sequential RN multiplies in
 //                   submission order: PAPER.md:157-158; a fused chain of k
@@ -43,8 +43,14 @@
 
 namespace bt {
 
-constexpr int kCompute = 256;                  // compute threads (8 warps)
-constexpr int kBlock = 32 + kCompute;          // + 1 scheduler warp
+// Two kernel variants share one block size (288 threads, 3 CTAs per SM):
+//  "sw" (single scheduler warp + 8 compute warps, 2 slots): best for large
+//       work units (FP32- or HBM-bound bodies; C3, C5);
+//  "rw" (pop warp + release warp + 7 compute warps, 4 slots): best for small
+//       units where scheduling dominates (C2, C4).
+constexpr int kBlock = 288;
+constexpr int kComputeSW = 256, kSlotsSW = 2;
+constexpr int kComputeRW = 224, kSlotsRW = 4;
 constexpr int kMaxFactors = 1024;              // upper bound of bt_config.max_fused
 constexpr unsigned long long kStop = ~0ull - 1;
 // named barrier ids (0 is __syncthreads): FULL[slot] = 1 + slot
@@ -54,9 +60,6 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
-}
-__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned *p) {
   unsigned v;
@@ -197,44 +200,45 @@ __device__ __forceinline__ uint64_t head_elems(const float *p, uint64_t n) {
   return h < n ? h : n;
 }
 
-template <int U>
+template <int U, int C>
 __device__ void scal_range(float *x, uint64_t n, const float *sf, uint32_t k, int tid) {
   const uint64_t head = head_elems(x, n);
-  for (uint64_t i = tid; i < head; i += kCompute) __stcg(x + i, chain_scalar(__ldcg(x + i), sf, k));
+  for (uint64_t i = tid; i < head; i += C) __stcg(x + i, chain_scalar(__ldcg(x + i), sf, k));
   float *xv = x + head;
   const uint64_t nv = (n - head) >> 3;
   uint64_t i = tid;
-  for (; i + (U - 1) * kCompute < nv; i += U * kCompute) {
+  for (; i + (U - 1) * C < nv; i += U * C) {
     float v[U][8];
 #pragma unroll
-    for (int a = 0; a < U; ++a) ld8(xv + 8 * (i + a * kCompute), v[a]);
+    for (int a = 0; a < U; ++a) ld8(xv + 8 * (i + a * C), v[a]);
     chain_apply<U>(v, sf, k);
 #pragma unroll
-    for (int a = 0; a < U; ++a) st8(xv + 8 * (i + a * kCompute), v[a]);
+    for (int a = 0; a < U; ++a) st8(xv + 8 * (i + a * C), v[a]);
   }
-  for (; i < nv; i += kCompute) {
+  for (; i < nv; i += C) {
     float v[1][8];
     ld8(xv + 8 * i, v[0]);
     chain_apply<1>(v, sf, k);
     st8(xv + 8 * i, v[0]);
   }
-  for (uint64_t t = head + 8 * nv + tid; t < n; t += kCompute) __stcg(x + t, chain_scalar(__ldcg(x + t), sf, k));
+  for (uint64_t t = head + 8 * nv + tid; t < n; t += C) __stcg(x + t, chain_scalar(__ldcg(x + t), sf, k));
 }
 
 // AXPY: y[i] = fl(fl(a*x[i]) + y[i]) (two roundings, no FFMA).
 __device__ __forceinline__ float axpy1(float a, float x, float y) { return __fadd_rn(__fmul_rn(a, x), y); }
 
+template <int C>
 __device__ void axpy_range(const float *x, float *y, uint64_t n, float a, int tid) {
   if (((reinterpret_cast<uintptr_t>(x) ^ reinterpret_cast<uintptr_t>(y)) & 31u) != 0) {
-    for (uint64_t i = tid; i < n; i += kCompute) __stcg(y + i, axpy1(a, __ldcg(x + i), __ldcg(y + i)));
+    for (uint64_t i = tid; i < n; i += C) __stcg(y + i, axpy1(a, __ldcg(x + i), __ldcg(y + i)));
     return;
   }
   const uint64_t head = head_elems(y, n);
-  for (uint64_t i = tid; i < head; i += kCompute) __stcg(y + i, axpy1(a, __ldcg(x + i), __ldcg(y + i)));
+  for (uint64_t i = tid; i < head; i += C) __stcg(y + i, axpy1(a, __ldcg(x + i), __ldcg(y + i)));
   const float *xv = x + head;
   float *yv = y + head;
   const uint64_t nv = (n - head) >> 3;
-  for (uint64_t i = tid; i < nv; i += kCompute) {
+  for (uint64_t i = tid; i < nv; i += C) {
     float xr[8], yr[8];
     ld8(xv + 8 * i, xr);
     ld8(yv + 8 * i, yr);
@@ -242,34 +246,35 @@ __device__ void axpy_range(const float *x, float *y, uint64_t n, float a, int ti
     for (int q = 0; q < 8; ++q) yr[q] = axpy1(a, xr[q], yr[q]);
     st8(yv + 8 * i, yr);
   }
-  for (uint64_t t = head + 8 * nv + tid; t < n; t += kCompute) __stcg(y + t, axpy1(a, __ldcg(x + t), __ldcg(y + t)));
+  for (uint64_t t = head + 8 * nv + tid; t < n; t += C) __stcg(y + t, axpy1(a, __ldcg(x + t), __ldcg(y + t)));
 }
 
+template <int C>
 __device__ void copy_range(const float *x, float *y, uint64_t n, int tid) {
   if (x == y) return;
   if (((reinterpret_cast<uintptr_t>(x) ^ reinterpret_cast<uintptr_t>(y)) & 31u) != 0) {
-    for (uint64_t i = tid; i < n; i += kCompute) __stcg(y + i, __ldcg(x + i));
+    for (uint64_t i = tid; i < n; i += C) __stcg(y + i, __ldcg(x + i));
     return;
   }
   const uint64_t head = head_elems(y, n);
-  for (uint64_t i = tid; i < head; i += kCompute) __stcg(y + i, __ldcg(x + i));
+  for (uint64_t i = tid; i < head; i += C) __stcg(y + i, __ldcg(x + i));
   const float *xv = x + head;
   float *yv = y + head;
   const uint64_t nv = (n - head) >> 3;
   uint64_t i = tid;
-  for (; i + kCompute < nv; i += 2 * kCompute) {
+  for (; i + C < nv; i += 2 * C) {
     float a[8], b[8];
     ld8(xv + 8 * i, a);
-    ld8(xv + 8 * (i + kCompute), b);
+    ld8(xv + 8 * (i + C), b);
     st8(yv + 8 * i, a);
-    st8(yv + 8 * (i + kCompute), b);
+    st8(yv + 8 * (i + C), b);
   }
-  for (; i < nv; i += kCompute) {
+  for (; i < nv; i += C) {
     float a[8];
     ld8(xv + 8 * i, a);
     st8(yv + 8 * i, a);
   }
-  for (uint64_t t = head + 8 * nv + tid; t < n; t += kCompute) __stcg(y + t, __ldcg(x + t));
+  for (uint64_t t = head + 8 * nv + tid; t < n; t += C) __stcg(y + t, __ldcg(x + t));
 }
 
 // ---- scheduler-warp helpers (lane 0 only) ---------------------------------
@@ -305,26 +310,38 @@ __device__ __forceinline__ unsigned long long pop_unit(const EpochArgs &a, unsig
   return u;
 }
 
-// Completion of one unit.  Memory-model pattern (as in cooperative-groups
-// grid sync): the compute warps' stores are ordered before this thread's
-// gpu-scope fence by the named barrier; fence + relaxed RMW = release; an RMW
-// observing the last decrement + fence = acquire.
+// Completion of one unit (scheduler lane 0).  Memory-model pattern: the
+// compute warps' stores are ordered before this thread by the CTA-scope
+// mbarrier (release/acquire), then every counter update is an acq_rel RMW at
+// gpu scope: it releases everything this thread has observed (cumulativity)
+// and acquires what the other predecessors / chunks released with theirs; a
+// ready successor's units are published by relaxed stores after one
+// fence.acq_rel (no sequentially-consistent fence anywhere).
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned *p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 __device__ __forceinline__ void release_unit(const EpochArgs &a, uint32_t item) {
   const DItem &it = a.items[item];
   const uint32_t nchunks = __ldg(&it.nchunks);
-  __threadfence();
-  if (nchunks > 1) {
-    const unsigned c = atomicAdd(&a.chunk_done[item], 1u);
-    if (c + 1 != nchunks) return;
-    __threadfence();  // acquire the other chunks' stores before releasing them on
-  }
   const uint32_t nsucc = __ldg(&it.nsucc), off = __ldg(&it.succ_off);
+  if (nchunks > 1) {
+    const unsigned c = atom_add_acq_rel(&a.chunk_done[item], 1u);
+    if (c + 1 != nchunks) return;
+  }
   for (uint32_t i = 0; i < nsucc; ++i) {
     const uint32_t s = __ldg(&a.succ[off + i]);
-    if (atomicSub(&a.pending[s], 1) == 1) {
-      __threadfence();
+    if (atom_add_acq_rel(reinterpret_cast<unsigned *>(&a.pending[s]), 0xFFFFFFFFu) == 1u) {
       const uint32_t nc = __ldg(&a.items[s].nchunks);
       const unsigned long long pos = atomicAdd(&a.ctr->tail, (unsigned long long)nc);
+      fence_acq_rel_gpu();   // one release fence covers the nc relaxed publications
+#pragma unroll 1
       for (uint32_t c = 0; c < nc; ++c) st_relaxed_u64(&a.queue[pos + c], ((unsigned long long)s << 32) | c);
     }
   }
@@ -409,7 +426,191 @@ __device__ __forceinline__ void poll_slot(const EpochArgs &a, SlotState &s, uint
 #ifndef BT_MIN_CTAS
 #define BT_MIN_CTAS 3   // 3 x 288 threads per SM: caps registers at 75 (measured best, profiles/r01_summary.md)
 #endif
-__global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel(EpochArgs a) {
+
+__device__ __forceinline__ unsigned ld_acquire_cta_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p))
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta_u32(unsigned *p, unsigned v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v)
+               : "memory");
+}
+
+// Compute warps: run units slot after slot until the STOP unit.
+template <int C, int S>
+__device__ __forceinline__ void compute_loop(const EpochArgs &a, const unsigned long long *s_unit,
+                                             float (*s_fac)[kMaxFactors], uint64_t *s_empty, int lane) {
+  const int tid = threadIdx.x - (kBlock - C);
+  for (unsigned u = 0;; ++u) {
+    const int b = (int)(u % S);
+    bar_sync(kBarFull + b, 32 + C);   // FULL[b]: the pop warp + the compute warps
+    const unsigned long long unit = s_unit[b];
+    if (unit == kStop) break;
+    const uint32_t item = (uint32_t)(unit >> 32);
+    const uint32_t chunk = (uint32_t)unit;
+    const DItem it = a.items[item];
+    const uint64_t lo = (uint64_t)chunk * a.chunk_elems;
+    const uint64_t hi = min(it.n, lo + a.chunk_elems);
+    switch (it.kind) {
+      case K_SCAL:
+        scal_range<4, C>(reinterpret_cast<float *>(it.x) + lo, hi - lo, s_fac[b], it.k, tid);
+        break;
+      case K_AXPY:
+        axpy_range<C>(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, hi - lo,
+                      __uint_as_float(it.arg), tid);
+        break;
+      case K_COPY:
+        copy_range<C>(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, hi - lo,
+                      tid);
+        break;
+      default:
+        if (tid == 0) raise_error(a, ERR_BAD_KIND);
+        break;
+    }
+    // this warp's stores precede the arrive (mbarrier.arrive releases at CTA
+    // scope; __syncwarp orders the other lanes' stores before lane 0's arrive)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s_empty[b]);
+  }
+}
+
+// Pop the unit at a fresh ticket (lane 0), spinning until it is published.
+__device__ __forceinline__ unsigned long long pop_ticket(const EpochArgs &a, unsigned long long &t) {
+  t = atomicAdd(&a.ctr->head, 1ull);
+  if (t >= a.total_units) return kStop;
+  unsigned long long unit = ld_acquire_u64(&a.queue[t]);
+  if (unit == Q_EMPTY) {
+    const uint64_t start = globaltimer();
+    for (unsigned spin = 0;; ++spin) {
+      __nanosleep(spin < 64 ? 32 : 256);
+      unit = ld_acquire_u64(&a.queue[t]);
+      if (unit != Q_EMPTY) break;
+      if ((spin & 63) == 63) {
+        if (ld_relaxed_u32(&a.ctr->abort)) return kStop;
+        if (globaltimer() - start > a.watchdog_ns) {
+          raise_error(a, ERR_WATCHDOG);
+          return kStop;
+        }
+      }
+    }
+  }
+  if ((unit >> 32) >= a.nitems) {
+    raise_error(a, ERR_BAD_UNIT);
+    return kStop;
+  }
+  return unit;
+}
+
+__device__ __forceinline__ void stage_factors(const EpochArgs &a, unsigned long long unit, float *dst, int lane) {
+  if (unit == kStop) return;
+  const DItem &it = a.items[(uint32_t)(unit >> 32)];
+  if (__ldg(&it.kind) == K_SCAL) {
+    const uint32_t k = __ldg(&it.k), off = __ldg(&it.arg);
+    for (uint32_t j = lane; j < k; j += 32) dst[j] = __ldg(a.factors + off + j);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// "rw": three roles per CTA.  Warp 0 pops units into kSlots shared-memory slots
+// (FULL[b]: a named barrier with the compute warps); warps 2..8 compute;
+// warp 1 releases finished units (EMPTY[b]: an mbarrier the compute warps
+// arrive on), up to kSlots at once on different lanes so their dependency
+// RMWs overlap.  Popping, computing and releasing overlap; the pop warp only
+// waits for a slot whose previous unit is released.  A CTA spinning for an
+// unpublished unit never holds finished-but-unreleased work (the release warp
+// runs independently), so it cannot starve the successor it waits for.
+__global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(EpochArgs a) {
+  constexpr int kCompute = kComputeRW, kSlots = kSlotsRW;
+  __shared__ unsigned long long s_unit[kSlots];
+  __shared__ __align__(8) uint64_t s_empty[kSlots];
+  __shared__ __align__(16) float s_fac[kSlots][kMaxFactors];
+  __shared__ unsigned s_popped, s_released;
+  __shared__ unsigned long long s_ticket[kSlots], s_g0[kSlots];
+  __shared__ long long s_popc[kSlots], s_c1[kSlots];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < kSlots; ++b) mbar_init(&s_empty[b], kCompute / 32);
+    s_popped = 0;
+    s_released = 0;
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ================= pop warp =================
+    for (unsigned u = 0;; ++u) {
+      const int b = (int)(u % kSlots);
+      if (u >= kSlots)   // the slot's previous unit must be released
+        while (ld_acquire_cta_u32(&s_released) + kSlots <= u) __nanosleep(32);
+      unsigned long long unit = kStop;
+      if (lane == 0) {
+        unsigned long long t = 0;
+        const uint64_t g0 = a.trace ? globaltimer() : 0;
+        const long long c0 = a.trace ? clock64() : 0;
+        unit = pop_ticket(a, t);
+        if (a.trace) {
+          s_ticket[b] = t;
+          s_g0[b] = g0;
+          s_c1[b] = clock64();
+          s_popc[b] = s_c1[b] - c0;
+        }
+      }
+      unit = __shfl_sync(0xffffffffu, unit, 0);
+      stage_factors(a, unit, s_fac[b], lane);
+      if (lane == 0) s_unit[b] = unit;
+      __syncwarp();
+      if (lane == 0) st_release_cta_u32(&s_popped, u + 1);
+      bar_arrive(kBarFull + b, 32 + kCompute);
+      if (unit == kStop) break;
+    }
+    return;
+  }
+  if (warp == 1) {
+    // ================= release warp =================
+    for (unsigned u = 0;;) {
+      while (ld_acquire_cta_u32(&s_popped) <= u) __nanosleep(32);
+      if (s_unit[u % kSlots] == kStop) break;
+      mbar_wait(&s_empty[u % kSlots], (u / kSlots) & 1u);
+      // batch the following units that are already done
+      unsigned m = 1;
+      if (lane == 0) {
+        const unsigned popped = ld_acquire_cta_u32(&s_popped);
+        while (m < kSlots) {
+          const unsigned v = u + m;
+          if (v >= popped || s_unit[v % kSlots] == kStop || !mbar_test(&s_empty[v % kSlots], (v / kSlots) & 1u))
+            break;
+          ++m;
+        }
+      }
+      m = __shfl_sync(0xffffffffu, m, 0);
+      if (lane < (int)m) {
+        const unsigned v = u + lane;
+        const int b = (int)(v % kSlots);
+        const unsigned long long unit = s_unit[b];
+        const long long c1 = a.trace ? clock64() : 0;
+        release_unit(a, (uint32_t)(unit >> 32));
+        if (a.trace) {
+          const unsigned long long t = s_ticket[b];
+          a.trace[4 * t + 0] = s_g0[b];
+          a.trace[4 * t + 1] = (unsigned long long)s_popc[b];
+          a.trace[4 * t + 2] = (unsigned long long)(c1 - s_c1[b]);
+          a.trace[4 * t + 3] = (unsigned long long)(clock64() - c1);
+          a.trace_item[t] = (uint32_t)(unit >> 32);
+        }
+      }
+      __syncwarp();
+      u += m;
+      if (lane == 0) st_release_cta_u32(&s_released, u);
+    }
+    return;
+  }
+  compute_loop<kCompute, kSlots>(a, s_unit, s_fac, s_empty, lane);
+}
+
+// "sw": one scheduler warp pops and releases, 8 compute warps, 2 slots.
+__global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sw(EpochArgs a) {
+  constexpr int kCompute = kComputeSW;
   __shared__ unsigned long long s_unit[2];
   __shared__ __align__(8) uint64_t s_empty[2];
   __shared__ __align__(16) float s_fac[2][kMaxFactors];
@@ -421,7 +622,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel(EpochArg
   __syncthreads();
 
   if (warp == 0) {
-    // ================= scheduler warp =================
+    // ================= scheduler warp (pop + release) =================
     // Invariant: the scheduler never spins on the queue while a finished unit
     // of this CTA is unreleased (it polls the other slot while waiting), so a
     // CTA cannot starve the very successor it is waiting for.
@@ -476,16 +677,10 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel(EpochArg
         }
       }
       unit = __shfl_sync(0xffffffffu, unit, 0);
-      if (unit != kStop) {
-        const DItem &it = a.items[(uint32_t)(unit >> 32)];
-        if (__ldg(&it.kind) == K_SCAL) {
-          const uint32_t k = __ldg(&it.k), off = __ldg(&it.arg);
-          for (uint32_t j = lane; j < k; j += 32) s_fac[b][j] = __ldg(a.factors + off + j);
-        }
-      }
+      stage_factors(a, unit, s_fac[b], lane);
       if (lane == 0) s_unit[b] = unit;
       __syncwarp();
-      bar_arrive(kBarFull + b, kBlock);
+      bar_arrive(kBarFull + b, 32 + kCompute);
       if (unit == kStop) {
         if (lane == 0) drain_slot(a, st[b ^ 1], &s_empty[b ^ 1]);   // unit u-1 still in flight
         break;
@@ -493,50 +688,23 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel(EpochArg
     }
     return;
   }
-
-  // ================= compute warps =================
-  const int tid = threadIdx.x - 32;
-  for (unsigned u = 0;; ++u) {
-    const int b = u & 1;
-    bar_sync(kBarFull + b, kBlock);
-    const unsigned long long unit = s_unit[b];
-    if (unit == kStop) break;
-    const uint32_t item = (uint32_t)(unit >> 32);
-    const uint32_t chunk = (uint32_t)unit;
-    const DItem it = a.items[item];
-    const uint64_t lo = (uint64_t)chunk * a.chunk_elems;
-    const uint64_t hi = min(it.n, lo + a.chunk_elems);
-    switch (it.kind) {
-      case K_SCAL:
-        scal_range<4>(reinterpret_cast<float *>(it.x) + lo, hi - lo, s_fac[b], it.k, tid);
-        break;
-      case K_AXPY:
-        axpy_range(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, hi - lo,
-                   __uint_as_float(it.arg), tid);
-        break;
-      case K_COPY:
-        copy_range(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, hi - lo, tid);
-        break;
-      default:
-        if (tid == 0) raise_error(a, ERR_BAD_KIND);
-        break;
-    }
-    // this warp's stores precede the arrive (mbarrier.arrive releases at CTA
-    // scope; __syncwarp orders the other lanes' stores before lane 0's arrive)
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&s_empty[b]);
-  }
+  compute_loop<kCompute, kSlotsSW>(a, s_unit, s_fac, s_empty, lane);
 }
 
 // Host-side launcher (called from runtime.cpp).
-cudaError_t launch_epoch(const EpochArgs &args, int grid, cudaStream_t stream) {
-  scheduler_kernel<<<grid, kBlock, 0, stream>>>(args);
+cudaError_t launch_epoch(const EpochArgs &args, int grid, cudaStream_t stream, bool release_warp) {
+  if (release_warp) scheduler_kernel_rw<<<grid, kBlock, 0, stream>>>(args);
+  else scheduler_kernel_sw<<<grid, kBlock, 0, stream>>>(args);
   return cudaGetLastError();
 }
 
 cudaError_t scheduler_occupancy(int *blocks_per_sm, int *block) {
   *block = kBlock;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, scheduler_kernel, kBlock, 0);
+  int a = 0, b = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, scheduler_kernel_rw, kBlock, 0);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, scheduler_kernel_sw, kBlock, 0);
+  *blocks_per_sm = a < b ? a : b;
+  return e;
 }
 
 int max_factors() { return kMaxFactors; }

@@ -73,9 +73,11 @@ def test_subnormal_inputs_not_flushed(B):
 
 
 @pytest.mark.parametrize("fusion", [True, False])
-@pytest.mark.parametrize("chunk_bytes", [0, 32, 96])
+@pytest.mark.parametrize("chunk_bytes", [0, 32, 96, 65536])
 def test_random_programs(B, fusion, chunk_bytes):
-    """>= 200 random programs, byte-identical to submission order."""
+    """>= 200 random programs, byte-identical to submission order.
+    Work units below 64 KiB run on the release-warp kernel ("rw"), larger ones
+    (chunk_bytes=65536) on the single-scheduler-warp kernel ("sw")."""
     flags = 0 if fusion else B.BT_FLAG_NO_FUSION
     for seed in range(70):
         p = W.random_small_program(seed, max_tasks=10)
