@@ -522,7 +522,8 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   // small work units are scheduling-bound: use the kernel with a dedicated
   // release warp; large ones are body-bound: keep all 8 warps computing
   static const char *kv = getenv("BT_KERNEL");   // "rw" / "sw": experiments only
-  const bool rw = kv ? (kv[0] == 'r') : CE < kReleaseWarpBelow;
+  const uint64_t avg_unit = (sampled / cnt * N) / std::max<uint64_t>(1, U);   // elements per work unit
+  const bool rw = kv ? (kv[0] == 'r') : avg_unit < kReleaseWarpBelow;
   CUDA_TRY(rt, launch_epoch(a, grid, stream, rw));
   CUDA_TRY(rt, cudaEventRecord(e.end, stream));
   CUDA_TRY(rt, cudaMemcpyAsync(h + o_readback, d + o_ctr, 64, cudaMemcpyDeviceToHost, stream));
