@@ -7,6 +7,10 @@ namespace bt {
 
 // Work-item kinds (equal to the public BT_CL_* codelet ids).
 enum : uint32_t { K_SCAL = 1, K_AXPY = 2, K_COPY = 3 };
+// DItem::kind bit: the item has exactly one predecessor, so the completion of
+// that predecessor makes it ready without touching its pending counter.
+constexpr uint32_t K_SINGLE_PRED = 1u << 8;
+constexpr uint32_t K_MASK = 0xFFu;
 
 // One work item of an epoch: a task, or a fused chain of SCAL tasks on the
 // same (sub)handle.  48 bytes, read-only during the kernel.
@@ -14,7 +18,7 @@ struct alignas(16) DItem {
   uint64_t x;         // device address of operand 0 (float*)
   uint64_t y;         // device address of operand 1 (AXPY/COPY), else 0
   uint64_t n;         // elements of each operand
-  uint32_t kind;      // K_*
+  uint32_t kind;      // K_* | K_SINGLE_PRED
   uint32_t k;         // SCAL: number of chained factors (>= 1); else 1
   uint32_t arg;       // SCAL: offset of the k factors in EpochArgs::factors;
                       // AXPY: float bits of a
@@ -30,7 +34,9 @@ struct alignas(64) Counters {
   unsigned long long tail;    // next free queue position
   unsigned int error;         // nonzero: a CTA detected a fault (see ERR_*)
   unsigned int abort;         // set with error: every CTA leaves its loop
-  unsigned long long spare[5];
+  unsigned long long done;    // units completed and released
+  unsigned long long trace_next;  // next trace record (BT_FLAG_TIMESTAMPS)
+  unsigned long long spare[3];
 };
 static_assert(sizeof(Counters) == 64, "Counters layout");
 

@@ -312,9 +312,9 @@ int retire(bt_runtime *rt, EpochBuf &e) {
     return fail(rt, -EIO, "device scheduler fault (code %u%s)", c->error,
                 c->error == ERR_WATCHDOG ? ": watchdog, a unit was never released" : "");
   }
-  if (c->head < e.units) {
+  if (c->done != e.units) {
     rt->poisoned = -EIO;
-    return fail(rt, -EIO, "device scheduler ended early (%llu of %llu units)", (unsigned long long)c->head,
+    return fail(rt, -EIO, "device scheduler ended early (%llu of %llu units)", (unsigned long long)c->done,
                 (unsigned long long)e.units);
   }
   if (e.traced) {
@@ -451,7 +451,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
       d.x = it.x;
       d.y = it.y;
       d.n = it.n;
-      d.kind = it.kind;
+      d.kind = it.kind | (it.npred == 1 ? K_SINGLE_PRED : 0u);
       d.k = it.k;
       if (it.kind == K_SCAL) {
         if (!rt->cursor[i]) {

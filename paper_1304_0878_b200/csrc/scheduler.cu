@@ -327,24 +327,52 @@ __device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned l
 }
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
-__device__ __forceinline__ void release_unit(const EpochArgs &a, uint32_t item) {
+// CTA-local continuation mailbox ("rw" kernel): one ready successor may be
+// handed to this CTA's own pop warp instead of the global queue, so a chain
+// of dependent tasks stays on one SM (its tile stays in L2) and skips the
+// queue round trip.  state: 0 empty, 2 being written, 1 full.
+struct Mailbox {
+  unsigned long long *unit;
+  unsigned *state;
+};
+
+__device__ __forceinline__ bool mailbox_put(const Mailbox &mb, unsigned long long unit) {
+  if (!mb.unit || atomicCAS(mb.state, 0u, 2u) != 0u) return false;
+  *reinterpret_cast<volatile unsigned long long *>(mb.unit) = unit;
+  __threadfence_block();
+  *reinterpret_cast<volatile unsigned *>(mb.state) = 1u;
+  return true;
+}
+
+__device__ __forceinline__ void release_unit(const EpochArgs &a, uint32_t item, const Mailbox &mb = Mailbox{}) {
   const DItem &it = a.items[item];
   const uint32_t nchunks = __ldg(&it.nchunks);
   const uint32_t nsucc = __ldg(&it.nsucc), off = __ldg(&it.succ_off);
   if (nchunks > 1) {
     const unsigned c = atom_add_acq_rel(&a.chunk_done[item], 1u);
-    if (c + 1 != nchunks) return;
+    if (c + 1 != nchunks) {
+      atomicAdd(&a.ctr->done, 1ull);
+      return;
+    }
   }
   for (uint32_t i = 0; i < nsucc; ++i) {
     const uint32_t s = __ldg(&a.succ[off + i]);
-    if (atom_add_acq_rel(reinterpret_cast<unsigned *>(&a.pending[s]), 0xFFFFFFFFu) == 1u) {
+    const uint32_t skind = __ldg(&a.items[s].kind);
+    // a single-predecessor successor is ready now (no counter); with more
+    // predecessors the acq_rel RMW both releases ours and acquires theirs
+    const bool ready = mb.unit && (skind & K_SINGLE_PRED)
+                           ? true
+                           : atom_add_acq_rel(reinterpret_cast<unsigned *>(&a.pending[s]), 0xFFFFFFFFu) == 1u;
+    if (ready) {
       const uint32_t nc = __ldg(&a.items[s].nchunks);
+      if (nc == 1 && mailbox_put(mb, (unsigned long long)s << 32)) continue;   // run it here
       const unsigned long long pos = atomicAdd(&a.ctr->tail, (unsigned long long)nc);
       fence_acq_rel_gpu();   // one release fence covers the nc relaxed publications
 #pragma unroll 1
       for (uint32_t c = 0; c < nc; ++c) st_relaxed_u64(&a.queue[pos + c], ((unsigned long long)s << 32) | c);
     }
   }
+  atomicAdd(&a.ctr->done, 1ull);
 }
 
 // ---- mbarrier (compute warps -> scheduler warp: "unit done") -------------
@@ -453,7 +481,7 @@ __device__ __forceinline__ void compute_loop(const EpochArgs &a, const unsigned 
     const DItem it = a.items[item];
     const uint64_t lo = (uint64_t)chunk * a.chunk_elems;
     const uint64_t hi = min(it.n, lo + a.chunk_elems);
-    switch (it.kind) {
+    switch (it.kind & K_MASK) {
       case K_SCAL:
         scal_range<4, C>(reinterpret_cast<float *>(it.x) + lo, hi - lo, s_fac[b], it.k, tid);
         break;
@@ -506,7 +534,7 @@ __device__ __forceinline__ unsigned long long pop_ticket(const EpochArgs &a, uns
 __device__ __forceinline__ void stage_factors(const EpochArgs &a, unsigned long long unit, float *dst, int lane) {
   if (unit == kStop) return;
   const DItem &it = a.items[(uint32_t)(unit >> 32)];
-  if (__ldg(&it.kind) == K_SCAL) {
+  if ((__ldg(&it.kind) & K_MASK) == K_SCAL) {
     const uint32_t k = __ldg(&it.k), off = __ldg(&it.arg);
     for (uint32_t j = lane; j < k; j += 32) dst[j] = __ldg(a.factors + off + j);
   }
@@ -526,7 +554,8 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
   __shared__ unsigned long long s_unit[kSlots];
   __shared__ __align__(8) uint64_t s_empty[kSlots];
   __shared__ __align__(16) float s_fac[kSlots][kMaxFactors];
-  __shared__ unsigned s_popped, s_released;
+  __shared__ unsigned s_popped, s_released, s_mb_state;
+  __shared__ unsigned long long s_mb_unit;
   __shared__ unsigned long long s_ticket[kSlots], s_g0[kSlots];
   __shared__ long long s_popc[kSlots], s_c1[kSlots];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -534,23 +563,74 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
     for (int b = 0; b < kSlots; ++b) mbar_init(&s_empty[b], kCompute / 32);
     s_popped = 0;
     s_released = 0;
+    s_mb_state = 0;
   }
   __syncthreads();
 
   if (warp == 0) {
     // ================= pop warp =================
+    unsigned long long ticket = 0;
+    bool have_ticket = false;
     for (unsigned u = 0;; ++u) {
       const int b = (int)(u % kSlots);
       if (u >= kSlots)   // the slot's previous unit must be released
         while (ld_acquire_cta_u32(&s_released) + kSlots <= u) __nanosleep(32);
       unsigned long long unit = kStop;
       if (lane == 0) {
-        unsigned long long t = 0;
         const uint64_t g0 = a.trace ? globaltimer() : 0;
         const long long c0 = a.trace ? clock64() : 0;
-        unit = pop_ticket(a, t);
+        // 1) a continuation from this CTA's release warp, 2) the unit at our
+        // ticket (taken once, kept across continuations), 3) termination: no
+        // queue work left for us and nothing of ours in flight, or every unit
+        // of the epoch done.
+        const uint64_t start = globaltimer();
+        for (unsigned spin = 0;; ++spin) {
+          if (*reinterpret_cast<volatile unsigned *>(&s_mb_state) == 1u) {
+            __threadfence_block();
+            unit = *reinterpret_cast<volatile unsigned long long *>(&s_mb_unit);
+            __threadfence_block();
+            *reinterpret_cast<volatile unsigned *>(&s_mb_state) = 0u;
+            break;
+          }
+          if (!have_ticket) {
+            ticket = atomicAdd(&a.ctr->head, 1ull);
+            have_ticket = true;
+          }
+          if (ticket < a.total_units) {
+            const unsigned long long v = ld_acquire_u64(&a.queue[ticket]);
+            if (v != Q_EMPTY) {
+              unit = v;
+              have_ticket = false;
+              if ((unit >> 32) >= a.nitems) {
+                raise_error(a, ERR_BAD_UNIT);
+                unit = kStop;
+              }
+              break;
+            }
+          } else if (ld_acquire_cta_u32(&s_released) == u &&
+                     *reinterpret_cast<volatile unsigned *>(&s_mb_state) == 0u) {
+            unit = kStop;      // all our units released, no continuation pending
+            break;
+          }
+          if ((spin & 15) == 15) {
+            if (atomicAdd(&a.ctr->done, 0ull) == a.total_units) {
+              unit = kStop;
+              break;
+            }
+            if (ld_relaxed_u32(&a.ctr->abort)) {
+              unit = kStop;
+              break;
+            }
+            if (globaltimer() - start > a.watchdog_ns) {
+              raise_error(a, ERR_WATCHDOG);
+              unit = kStop;
+              break;
+            }
+          }
+          __nanosleep(spin < 64 ? 32 : 256);
+        }
         if (a.trace) {
-          s_ticket[b] = t;
+          s_ticket[b] = unit == kStop ? 0 : atomicAdd(&a.ctr->trace_next, 1ull);
           s_g0[b] = g0;
           s_c1[b] = clock64();
           s_popc[b] = s_c1[b] - c0;
@@ -589,7 +669,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
         const int b = (int)(v % kSlots);
         const unsigned long long unit = s_unit[b];
         const long long c1 = a.trace ? clock64() : 0;
-        release_unit(a, (uint32_t)(unit >> 32));
+        release_unit(a, (uint32_t)(unit >> 32), Mailbox{&s_mb_unit, &s_mb_state});
         if (a.trace) {
           const unsigned long long t = s_ticket[b];
           a.trace[4 * t + 0] = s_g0[b];
