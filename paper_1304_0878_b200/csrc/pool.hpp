@@ -21,7 +21,7 @@ namespace bt {
 
 class Pool {
  public:
-  explicit Pool(int n, int spin_us = 20000) : n_(n < 1 ? 1 : n), spin_us_(spin_us) {
+  explicit Pool(int n, int spin_us = 5000) : n_(n < 1 ? 1 : n), spin_us_(spin_us) {
     for (int i = 1; i < n_; ++i) threads_.emplace_back([this, i] { loop(i); });
   }
   ~Pool() {
