@@ -48,6 +48,7 @@ constexpr int kEpochRing = 8;                       // epoch buffers in flight (
 constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;   // 20 s
 constexpr size_t kParallelPack = 4096;              // items above which the pack runs on the pool
 constexpr uint64_t kReleaseWarpBelow = 16384;       // work units smaller than this use the "rw" kernel
+constexpr uint64_t kUploadChunk = 64ull << 20;      // registrations >= this upload in chunks on a copy stream
 
 const char *codelet_name(int c) {
   switch (c) {
@@ -102,6 +103,28 @@ struct EpochBuf {
   size_t trace_off_h = 0;     // offset of the trace copy in hblob
 };
 
+// Host <-> device coherence of one host-homed registered vector (PAPER.md:
+// 97-99 "transferring data between main memory and GPUs as needed").
+//  * register uploads large vectors in chunks on a copy stream; an epoch
+//    waits only for the chunks its tasks touch, so the first tasks start
+//    while the rest is still in flight;
+//  * write-back: when an epoch writes a range of the vector for the first
+//    time since registration, that range is copied back to the host buffer
+//    right after the epoch (on a second copy stream), so unregister finds the
+//    host copy current.  A range written twice marks the vector dirty and
+//    unregister copies the whole vector back after everything else.
+struct UploadChunk {
+  uint64_t lo, hi;            // device byte range
+  cudaEvent_t ev;             // recorded after its H2D copy
+};
+struct RootCache {
+  uint64_t dlo = 0, dhi = 0;  // device byte range of the replica
+  std::vector<UploadChunk> uploads;
+  std::vector<std::pair<uint64_t, uint64_t>> written;   // device byte ranges written by epochs
+  bool dirty = false;         // a write not covered by an eager write-back
+  bool wb = false;            // eager write-backs issued
+};
+
 }  // namespace
 
 struct bt_runtime {
@@ -137,6 +160,20 @@ struct bt_runtime {
   cudaEvent_t ev_fork = nullptr, ev_round[2] = {nullptr, nullptr};
   cudaEvent_t span_start = nullptr, span_end = nullptr;
   bool span_open = false;
+  cudaStream_t h2d = nullptr, d2h = nullptr;        // copy streams (chunked upload, write-back)
+  std::unordered_map<uint32_t, RootCache> caches;   // host-homed roots with a replica
+  std::vector<cudaEvent_t> ev_free;
+  cudaEvent_t get_event() {
+    if (!ev_free.empty()) {
+      cudaEvent_t e = ev_free.back();
+      ev_free.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    return e;
+  }
+  void put_event(cudaEvent_t e) { ev_free.push_back(e); }
   bt_stats stats{};
 
   // host-only snapshot storage
@@ -219,8 +256,8 @@ uint32_t alloc_slots(bt_runtime *rt, uint32_t count) {
     h = SlotHot();
     h.gen = gen;
     h.flags = F_LIVE;
-    const uint32_t k = (s + i) >> 6;    // block -> round k % R, lane (k / R) % P
-    h.grp = (k % (uint32_t)rt->nrounds) * (uint32_t)rt->npool + (k / (uint32_t)rt->nrounds) % (uint32_t)rt->npool;
+    const uint32_t k = (s + i) >> 6;    // 64-slot block -> lane k % P, round (k / P) % R
+    h.grp = ((k / (uint32_t)rt->npool) % (uint32_t)rt->nrounds) * (uint32_t)rt->npool + k % (uint32_t)rt->npool;
     rt->slots[s + i] = Slot();
     rt->deps[s + i] = DepState();
   }
@@ -371,6 +408,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   // (a SCAL item whose factor list equals the previous item's reuses it).
   struct RangeAcc {
     uint64_t units = 0, ready = 0, succ = 0, fac = 0;
+    uint64_t wlo = ~0ull, whi = 0, alo = ~0ull, ahi = 0;   // written / all operand byte ranges
   };
   std::vector<RangeAcc> acc(P);
   rt->cursor.resize(N);   // per item: 1 = reuses the previous item's factor list
@@ -385,6 +423,16 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
       a.units += nc;
       if (it.npred == 0) a.ready += nc;
       a.succ += it.nsucc;
+      const uint64_t bytes = 4 * it.n;
+      const uint64_t w = it.kind == K_SCAL ? it.x : it.y;
+      a.wlo = std::min(a.wlo, w);
+      a.whi = std::max(a.whi, w + bytes);
+      a.alo = std::min(a.alo, it.x);
+      a.ahi = std::max(a.ahi, it.x + bytes);
+      if (it.kind != K_SCAL) {
+        a.alo = std::min(a.alo, it.y);
+        a.ahi = std::max(a.ahi, it.y + bytes);
+      }
       uint32_t reuse = 0;
       if (it.kind == K_SCAL) {
         if (prev && prev->k == it.k && memcmp(B.factors(*prev), B.factors(it), 4ull * it.k) == 0) reuse = 1;
@@ -405,6 +453,10 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     tot.ready += acc[p].ready;
     tot.succ += acc[p].succ;
     tot.fac += acc[p].fac;
+    tot.wlo = std::min(tot.wlo, acc[p].wlo);
+    tot.whi = std::max(tot.whi, acc[p].whi);
+    tot.alo = std::min(tot.alo, acc[p].alo);
+    tot.ahi = std::max(tot.ahi, acc[p].ahi);
   }
   const uint64_t U = tot.units, U0 = tot.ready, F = tot.fac;
   if (tot.succ != E) return fail(rt, -EIO, "internal: successor count mismatch");
@@ -518,6 +570,13 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   a.nitems = (uint32_t)N;
   const int grid = (int)std::min<uint64_t>((uint64_t)rt->grid_max, U);
 
+  // host-homed data this epoch touches must have arrived (chunked uploads)
+  for (auto &kv2 : rt->caches) {
+    RootCache &c = kv2.second;
+    if (c.uploads.empty() || tot.ahi <= c.dlo || tot.alo >= c.dhi) continue;
+    for (const UploadChunk &u : c.uploads)
+      if (u.lo < tot.ahi && tot.alo < u.hi) CUDA_TRY(rt, cudaStreamWaitEvent(stream, u.ev, 0));
+  }
   CUDA_TRY(rt, cudaEventRecord(e.start, stream));
   // small work units are scheduling-bound: use the kernel with a dedicated
   // release warp; large ones are body-bound: keep all 8 warps computing
@@ -526,6 +585,27 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   const bool rw = kv ? (kv[0] == 'r') : avg_unit < kReleaseWarpBelow;
   CUDA_TRY(rt, launch_epoch(a, grid, stream, rw));
   CUDA_TRY(rt, cudaEventRecord(e.end, stream));
+  // write-back of host-homed ranges written for the first time since registration
+  bool wb_waited = false;
+  for (auto &kv2 : rt->caches) {
+    RootCache &c = kv2.second;
+    const uint64_t lo = std::max(tot.wlo, c.dlo), hi = std::min(tot.whi, c.dhi);
+    if (lo >= hi) continue;
+    bool again = false;
+    for (const auto &wr : c.written) again |= (wr.first < hi && lo < wr.second);
+    c.written.emplace_back(lo, hi);
+    if (again || c.dirty) {
+      c.dirty = true;
+      continue;
+    }
+    if (!wb_waited) {
+      CUDA_TRY(rt, cudaStreamWaitEvent(rt->d2h, e.end, 0));
+      wb_waited = true;
+    }
+    char *host = static_cast<char *>(rt->slots[kv2.first].hptr) + (lo - c.dlo);
+    CUDA_TRY(rt, cudaMemcpyAsync(host, reinterpret_cast<const void *>(lo), hi - lo, cudaMemcpyDeviceToHost, rt->d2h));
+    c.wb = true;
+  }
   CUDA_TRY(rt, cudaMemcpyAsync(h + o_readback, d + o_ctr, 64, cudaMemcpyDeviceToHost, stream));
   if (traced) CUDA_TRY(rt, cudaMemcpyAsync(h + o_trace_h, d + o_trace, 36 * U, cudaMemcpyDeviceToHost, stream));
   CUDA_TRY(rt, cudaEventRecord(e.done, stream));
@@ -561,6 +641,13 @@ int wait_all(bt_runtime *rt) {
     if (int r = retire(rt, *next)) return r;
   }
   CUDA_TRY(rt, cudaStreamSynchronize(rt->stream));
+  for (auto &kv2 : rt->caches) {   // every epoch that needed an upload chunk has run
+    for (const UploadChunk &u : kv2.second.uploads) {
+      CUDA_TRY(rt, cudaEventSynchronize(u.ev));
+      rt->put_event(u.ev);
+    }
+    kv2.second.uploads.clear();
+  }
   if (rt->span_open) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, rt->span_start, rt->span_end) == cudaSuccess) rt->stats.device_span_ms += ms;
@@ -675,6 +762,11 @@ int bt_init(const bt_config *cfg_in, bt_runtime **out) {
       delete rt;
       return -ENOMEM;
     }
+    if (cudaStreamCreateWithFlags(&rt->h2d, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&rt->d2h, cudaStreamNonBlocking) != cudaSuccess) {
+      delete rt;
+      return -ENOMEM;
+    }
     for (int i = 0; i < 2; ++i)
       if (cudaStreamCreateWithFlags(&rt->rstream[i], cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&rt->ev_round[i], cudaEventDisableTiming) != cudaSuccess) {
@@ -713,6 +805,9 @@ int bt_shutdown(bt_runtime *rt) {
       if (rt->ev_round[i]) cudaEventDestroy(rt->ev_round[i]);
     }
     if (rt->ev_fork) cudaEventDestroy(rt->ev_fork);
+    for (cudaEvent_t ev : rt->ev_free) cudaEventDestroy(ev);
+    if (rt->h2d) cudaStreamDestroy(rt->h2d);
+    if (rt->d2h) cudaStreamDestroy(rt->d2h);
     if (rt->span_start) cudaEventDestroy(rt->span_start);
     if (rt->span_end) cudaEventDestroy(rt->span_end);
     if (rt->own_stream) cudaStreamDestroy(rt->stream);
@@ -761,10 +856,12 @@ int bt_vector_data_register(bt_runtime *rt, bt_handle *out, int home_node, void 
         return fail(rt, -ENOMEM, "cannot allocate the device replica (%zu bytes)", nx * 4);
       }
       owns = true;
-      e = cudaMemcpyAsync(dptr, ptr, nx * 4, cudaMemcpyHostToDevice, rt->stream);
-      if (e != cudaSuccess) {
-        cudaFreeAsync(dptr, rt->stream);
-        return cuda_fail(rt, e, "register upload");
+      if (nx * 4 < kUploadChunk) {
+        e = cudaMemcpyAsync(dptr, ptr, nx * 4, cudaMemcpyHostToDevice, rt->stream);
+        if (e != cudaSuccess) {
+          cudaFreeAsync(dptr, rt->stream);
+          return cuda_fail(rt, e, "register upload");
+        }
       }
     }
   }
@@ -781,6 +878,26 @@ int bt_vector_data_register(bt_runtime *rt, bt_handle *out, int home_node, void 
   if (ptr) {
     rt->ranges[lo] = {hi, s};
     rt->by_ptr[lo] = s;
+  }
+  if (owns) {   // host-homed replica: coherence state, chunked upload of large vectors
+    RootCache &c = rt->caches[s];
+    c = RootCache();
+    c.dlo = reinterpret_cast<uint64_t>(dptr);
+    c.dhi = c.dlo + nx * 4;
+    if (nx * 4 >= kUploadChunk) {
+      cudaEvent_t ev_alloc = rt->get_event();
+      CUDA_TRY(rt, cudaEventRecord(ev_alloc, rt->stream));        // after cudaMallocAsync
+      CUDA_TRY(rt, cudaStreamWaitEvent(rt->h2d, ev_alloc, 0));
+      rt->put_event(ev_alloc);
+      for (uint64_t off = 0; off < nx * 4; off += kUploadChunk) {
+        const uint64_t len = std::min<uint64_t>(kUploadChunk, nx * 4 - off);
+        CUDA_TRY(rt, cudaMemcpyAsync(reinterpret_cast<char *>(dptr) + off, static_cast<const char *>(ptr) + off, len,
+                                     cudaMemcpyHostToDevice, rt->h2d));
+        UploadChunk u{c.dlo + off, c.dlo + off + len, rt->get_event()};
+        CUDA_TRY(rt, cudaEventRecord(u.ev, rt->h2d));
+        c.uploads.push_back(u);
+      }
+    }
   }
   ++rt->live_roots;
   *out = make_handle(rt, s);
@@ -818,6 +935,11 @@ int bt_data_partition(bt_runtime *rt, bt_handle h, uint32_t nparts) {
     ch.nx = base + (t < extra ? 1 : 0);
     ch.dptr = ph.dptr ? ph.dptr + off : nullptr;
     ch.rank = ph.rank;
+    // pipelined rounds take contiguous quarters of the parts (so round r
+    // needs only its own upload chunks and writes back one contiguous range);
+    // lanes still own whole 64-slot blocks
+    const uint32_t round = (uint32_t)((uint64_t)t * (uint32_t)rt->nrounds / nparts);
+    ch.grp = round * (uint32_t)rt->npool + ((c0 + t) >> 6) % (uint32_t)rt->npool;
   }
   p.nparts = nparts;
   p.first_child = c0;
@@ -958,7 +1080,8 @@ int submit(bt_runtime *rt, int codelet, float scalar, bt_handle h0, bt_handle h1
 
 // A run of SCAL tasks [i0, i1) built on the pool.  Handles are grouped in
 // blocks of 64 consecutive slots (768 bytes of DepState, so lanes never share
-// a cache line); block k belongs to round k % R and lane (k / R) % P.
+// a cache line); block k belongs to lane k % P; the round of a slot is fixed
+// at allocation (SlotHot::grp): contiguous quarters of a partition's parts.
 //   phase 1 (per chunk of the stream): validate, bucket by (round, lane);
 //   phase 2 (per round, per lane): stable per-handle sort, runs -> items;
 //   merge:  renumber the lanes' items into the epoch.
@@ -1068,8 +1191,9 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
   DepState *deps = rt->deps.data();
   const double tp1 = now_ms();
   double t_p2 = 0, t_merge = 0, t_flush = 0;
-  // group (r, l) owns slot blocks k = q*G + l*R + r; dense local index q*64 + (s & 63)
-  const uint32_t nlocal = (uint32_t)((((nslots + 63) >> 6) + G - 1) / G) * 64;
+  // lane l owns slot blocks k with k % P == l (in every round); dense local
+  // index over the lane's blocks: (k / P) * 64 + (s & 63)
+  const uint32_t nlocal = (uint32_t)((((nslots + 63) >> 6) + P - 1) / P) * 64;
   const int rounds = pipelined ? R : 1;
   for (int rr = 0; rr < rounds; ++rr) {
     const double ta = now_ms();
@@ -1088,8 +1212,8 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
         Lane &L = rt->lanes[(size_t)l * (pipelined ? 1 : R) + (pipelined ? 0 : r)];
         B.lane_runs(
             L, ptrs.data(), tptr.data(), cnts.data(), P, deps, nlocal,
-            [G](uint32_t s) { return ((s >> 6) / G) * 64 + (s & 63); },
-            [G, lr = (uint32_t)(l * R + r)](uint32_t loc) { return ((loc >> 6) * G + lr) * 64 + (loc & 63); },
+            [up = (uint32_t)P](uint32_t s) { return ((s >> 6) / up) * 64 + (s & 63); },
+            [up = (uint32_t)P, ul = (uint32_t)l](uint32_t loc) { return ((loc >> 6) * up + ul) * 64 + (loc & 63); },
             [hot](uint32_t s) {
               return std::pair<uint64_t, uint64_t>(reinterpret_cast<uint64_t>(hot[s].dptr), hot[s].nx);
             });
@@ -1209,6 +1333,30 @@ int bt_task_wait_for_all(bt_runtime *rt) {
   return wait_all(rt);
 }
 
+}  // extern "C"
+
+namespace {
+// Make the host copy of device bytes [lo, hi) of host-homed root `root`
+// current (caller has run wait_all): untouched since registration -> nothing;
+// every write covered by an eager write-back -> wait for those copies;
+// otherwise copy the range back after them (same copy stream).
+int sync_to_host(bt_runtime *rt, uint32_t root, uint64_t lo, uint64_t hi) {
+  auto it = rt->caches.find(root);
+  if (it == rt->caches.end()) return 0;
+  RootCache &c = it->second;
+  bool touched = false;
+  for (const auto &wr : c.written) touched |= (wr.first < hi && lo < wr.second);
+  if (touched && c.dirty) {
+    char *host = static_cast<char *>(rt->slots[root].hptr) + (lo - c.dlo);
+    CUDA_TRY(rt, cudaMemcpyAsync(host, reinterpret_cast<const void *>(lo), hi - lo, cudaMemcpyDeviceToHost, rt->d2h));
+  }
+  if (touched || c.wb) CUDA_TRY(rt, cudaStreamSynchronize(rt->d2h));
+  return 0;
+}
+}  // namespace
+
+extern "C" {
+
 int bt_data_acquire(bt_runtime *rt, bt_handle h, int mode) {
   if (int r = check_live(rt)) return r;
   uint32_t s = resolve(rt, h);
@@ -1223,9 +1371,8 @@ int bt_data_acquire(bt_runtime *rt, bt_handle h, int mode) {
   if (sh.rank != rt->cfg.rank || !sh.dptr) return fail(rt, -EINVAL, "data not stored on this rank");
   cudaSetDevice(rt->device);
   if (int r = wait_all(rt)) return r;
-  CUDA_TRY(rt, cudaMemcpyAsync(static_cast<float *>(root.hptr) + sl.offset, sh.dptr, sh.nx * 4,
-                               cudaMemcpyDeviceToHost, rt->stream));
-  CUDA_TRY(rt, cudaStreamSynchronize(rt->stream));
+  const uint64_t lo = reinterpret_cast<uint64_t>(sh.dptr);
+  if (int r = sync_to_host(rt, sl.root, lo, lo + sh.nx * 4)) return r;
   rt->slots[s].acquired = mode;
   set_blocked(rt, s, true);
   return 0;
@@ -1264,9 +1411,10 @@ int bt_data_unregister(bt_runtime *rt, bt_handle h) {
     cudaSetDevice(rt->device);
     if (int r = wait_all(rt)) return r;
     if (sl.home_node == 0 && sl.hptr && sh.dptr) {
-      CUDA_TRY(rt, cudaMemcpyAsync(sl.hptr, sh.dptr, sh.nx * 4, cudaMemcpyDeviceToHost, rt->stream));
-      CUDA_TRY(rt, cudaStreamSynchronize(rt->stream));
+      const uint64_t lo = reinterpret_cast<uint64_t>(sh.dptr);
+      if (int r = sync_to_host(rt, s, lo, lo + sh.nx * 4)) return r;
     }
+    rt->caches.erase(s);
     if (sl.owns_dev) CUDA_TRY(rt, cudaFreeAsync(sh.dptr, rt->stream));
   }
   if (sl.hptr) {

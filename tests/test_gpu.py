@@ -279,3 +279,69 @@ def test_c5_shape_pipelined_default(B):
     out, stats = run_gpu(p, pipeline_min=1024)
     assert_bits_equal(out[0], oracle.scal_chain(p.buffers[0], p.meta["factors"]), "C5 reduced, pipelined")
     assert stats["epochs"] >= 4
+
+
+# ---- host <-> device coherence: chunked upload, eager write-back, dirty path ----
+
+def _sweeps(B, rt, subs, factors):
+    n = len(subs)
+    c = np.full(n * len(factors), B.BT_CL_SCAL, np.int32)
+    s = np.repeat(factors.astype(np.float32), n)
+    h0 = np.tile(np.asarray(subs, np.uint64), len(factors))
+    rt.insert_batch(c, s, h0)
+
+
+def test_large_host_buffer_pipelined_writeback(B):
+    """64 MiB host buffer: chunked upload, pipelined rounds, eager write-back of
+    each round's range; unregister must leave the exact result in the buffer."""
+    rng = np.random.default_rng(31)
+    x0 = W.unit_interval_floats(rng, 1 << 24)
+    f = W.sweep_factors(rng, 12)
+    x = x0.copy()
+    with B.Runtime(pipeline_min=1024) as rt:
+        h = rt.register_array(x)
+        subs = rt.partition(h, 1024)
+        _sweeps(B, rt, subs, f)
+        rt.wait()
+        rt.unpartition(h)
+        rt.unregister(h)
+    assert_bits_equal(x, oracle.scal_chain(x0, f), "write-back")
+
+
+def test_large_host_buffer_written_twice_and_acquire(B):
+    """A range written by two epochs (dirty): unregister copies everything back;
+    an acquire in between sees the first batch's result."""
+    rng = np.random.default_rng(32)
+    x0 = W.unit_interval_floats(rng, 1 << 24)
+    f1, f2 = W.sweep_factors(rng, 5), W.sweep_factors(rng, 7)
+    x = x0.copy()
+    with B.Runtime(pipeline_min=1024) as rt:
+        h = rt.register_array(x)
+        subs = rt.partition(h, 512)
+        _sweeps(B, rt, subs, f1)
+        rt.wait()
+        rt.acquire(subs[3], B.BT_R)
+        lo = 3 * (1 << 24) // 512
+        mid = oracle.scal_chain(x0, f1)
+        assert_bits_equal(x[lo:lo + (1 << 24) // 512], mid[lo:lo + (1 << 24) // 512], "acquire after batch 1")
+        rt.release(subs[3])
+        _sweeps(B, rt, subs, f2)
+        rt.wait()
+        rt.unpartition(h)
+        rt.unregister(h)
+    assert_bits_equal(x, oracle.scal_chain(mid, f2), "dirty write-back")
+
+
+def test_large_host_buffer_untouched_and_axpy(B):
+    rng = np.random.default_rng(33)
+    a0 = W.unit_interval_floats(rng, 1 << 24)
+    b0 = W.unit_interval_floats(rng, 1 << 24)
+    a, b = a0.copy(), b0.copy()
+    with B.Runtime() as rt:
+        ha, hb = rt.register_array(a), rt.register_array(b)
+        rt.axpy(0.5, ha, hb)               # reads a (chunked upload), writes b
+        rt.wait()
+        rt.unregister(ha)
+        rt.unregister(hb)
+    assert_bits_equal(a, a0, "untouched")
+    assert_bits_equal(b, (np.float32(0.5) * a0 + b0).astype(np.float32), "axpy")
