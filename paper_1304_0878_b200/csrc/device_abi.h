@@ -36,7 +36,9 @@ struct alignas(64) Counters {
   unsigned int abort;         // set with error: every CTA leaves its loop
   unsigned long long done;    // units completed and released
   unsigned long long trace_next;  // next trace record (BT_FLAG_TIMESTAMPS)
-  unsigned long long spare[3];
+  unsigned int exited;        // CTAs that left the kernel (the last one reports to the host)
+  unsigned int pad;
+  unsigned long long spare[2];
 };
 static_assert(sizeof(Counters) == 64, "Counters layout");
 
@@ -53,6 +55,7 @@ struct EpochArgs {
   const float *factors;
   unsigned long long *queue;    // total_units slots
   Counters *ctr;
+  Counters *host_ctr;           // mapped pinned host memory: the last CTA copies *ctr here
   unsigned long long *trace;    // 4 timestamps per unit, or null
   uint32_t *trace_item;         // item per unit, or null
   uint64_t total_units;

@@ -99,7 +99,8 @@ struct EpochBuf {
   uint64_t seq = 0;           // launch order
   uint64_t units = 0;
   bool traced = false;
-  size_t ctr_readback = 0;    // offset of the Counters readback in hblob
+  Counters *hctr = nullptr;     // mapped pinned: written by the kernel's last CTA
+  Counters *hctr_dev = nullptr;
   size_t trace_off_h = 0;     // offset of the trace copy in hblob
 };
 
@@ -343,7 +344,7 @@ int retire(bt_runtime *rt, EpochBuf &e) {
   if (err != cudaSuccess) return cuda_fail(rt, err, "epoch completion");
   float ms = 0.f;
   if (cudaEventElapsedTime(&ms, e.start, e.end) == cudaSuccess) rt->stats.device_ms += ms;
-  const Counters *c = reinterpret_cast<const Counters *>(e.hblob + e.ctr_readback);
+  const Counters *c = e.hctr;
   if (c->error != ERR_NONE) {
     rt->poisoned = -EIO;
     return fail(rt, -EIO, "device scheduler fault (code %u%s)", c->error,
@@ -562,6 +563,12 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   a.factors = reinterpret_cast<const float *>(d + o_fac);
   a.queue = reinterpret_cast<unsigned long long *>(d + o_queue);
   a.ctr = reinterpret_cast<Counters *>(d + o_ctr);
+  if (!e.hctr) {
+    CUDA_TRY(rt, cudaHostAlloc((void **)&e.hctr, sizeof(Counters), cudaHostAllocMapped | cudaHostAllocPortable));
+    CUDA_TRY(rt, cudaHostGetDevicePointer((void **)&e.hctr_dev, e.hctr, 0));
+  }
+  memset(e.hctr, 0, sizeof(Counters));
+  a.host_ctr = e.hctr_dev;
   a.trace = traced ? reinterpret_cast<unsigned long long *>(d + o_trace) : nullptr;
   a.trace_item = traced ? reinterpret_cast<uint32_t *>(d + o_trace + 32 * U) : nullptr;
   a.total_units = U;
@@ -606,14 +613,12 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     CUDA_TRY(rt, cudaMemcpyAsync(host, reinterpret_cast<const void *>(lo), hi - lo, cudaMemcpyDeviceToHost, rt->d2h));
     c.wb = true;
   }
-  CUDA_TRY(rt, cudaMemcpyAsync(h + o_readback, d + o_ctr, 64, cudaMemcpyDeviceToHost, stream));
   if (traced) CUDA_TRY(rt, cudaMemcpyAsync(h + o_trace_h, d + o_trace, 36 * U, cudaMemcpyDeviceToHost, stream));
   CUDA_TRY(rt, cudaEventRecord(e.done, stream));
   e.inflight = true;
   e.seq = ++rt->ep_seq;
   e.units = U;
   e.traced = traced;
-  e.ctr_readback = o_readback;
   e.trace_off_h = o_trace_h;
 
   rt->stats.items += N;
@@ -795,6 +800,7 @@ int bt_shutdown(bt_runtime *rt) {
     cudaStreamSynchronize(rt->stream);
     for (auto &e : rt->ep) {
       if (e.hblob) cudaFreeHost(e.hblob);
+      if (e.hctr) cudaFreeHost(e.hctr);
       if (e.dblob) cudaFree(e.dblob);
       if (e.start) cudaEventDestroy(e.start);
       if (e.end) cudaEventDestroy(e.end);

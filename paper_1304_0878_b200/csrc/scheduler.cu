@@ -540,6 +540,26 @@ __device__ __forceinline__ void stage_factors(const EpochArgs &a, unsigned long 
   }
 }
 
+// The last CTA to leave copies the epoch counters to mapped host memory, so
+// the host checks completion without a device-to-host copy (which would queue
+// behind the write-back copies on the copy engine).
+__device__ __forceinline__ void report_exit(const EpochArgs &a) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&a.ctr->exited, 1u) == gridDim.x - 1) {
+      __threadfence();
+      volatile Counters *h = a.host_ctr;
+      h->head = atomicAdd(&a.ctr->head, 0ull);
+      h->tail = atomicAdd(&a.ctr->tail, 0ull);
+      h->done = atomicAdd(&a.ctr->done, 0ull);
+      h->error = atomicAdd(&a.ctr->error, 0u);
+      h->exited = gridDim.x;
+      __threadfence_system();
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // "rw": three roles per CTA.  Warp 0 pops units into kSlots shared-memory slots
 // (FULL[b]: a named barrier with the compute warps); warps 2..8 compute;
@@ -644,9 +664,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
       bar_arrive(kBarFull + b, 32 + kCompute);
       if (unit == kStop) break;
     }
-    return;
-  }
-  if (warp == 1) {
+  } else if (warp == 1) {
     // ================= release warp =================
     for (unsigned u = 0;;) {
       while (ld_acquire_cta_u32(&s_popped) <= u) __nanosleep(32);
@@ -683,9 +701,10 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
       u += m;
       if (lane == 0) st_release_cta_u32(&s_released, u);
     }
-    return;
+  } else {
+    compute_loop<kCompute, kSlots>(a, s_unit, s_fac, s_empty, lane);
   }
-  compute_loop<kCompute, kSlots>(a, s_unit, s_fac, s_empty, lane);
+  report_exit(a);
 }
 
 // "sw": one scheduler warp pops and releases, 8 compute warps, 2 slots.
@@ -766,9 +785,10 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sw(Epoch
         break;
       }
     }
-    return;
+  } else {
+    compute_loop<kCompute, kSlotsSW>(a, s_unit, s_fac, s_empty, lane);
   }
-  compute_loop<kCompute, kSlotsSW>(a, s_unit, s_fac, s_empty, lane);
+  report_exit(a);
 }
 
 // Host-side launcher (called from runtime.cpp).
