@@ -30,6 +30,7 @@
 namespace bt {
 cudaError_t launch_epoch(const EpochArgs &args, int grid, cudaStream_t stream, bool release_warp);
 cudaError_t scheduler_occupancy(int *blocks_per_sm, int *block);
+cudaError_t launch_stage(void *dst, const void *src_mapped, size_t bytes, cudaStream_t stream);
 int max_factors();
 }  // namespace bt
 
@@ -90,7 +91,8 @@ struct Slot {
 };
 
 struct EpochBuf {
-  char *hblob = nullptr;
+  char *hblob = nullptr;       // pinned + mapped
+  char *hblob_dev = nullptr;   // its device-side address
   size_t hcap = 0;
   char *dblob = nullptr;
   size_t dcap = 0;
@@ -316,7 +318,8 @@ int ensure_host(bt_runtime *rt, EpochBuf &e, size_t need) {
   if (e.hblob) cudaFreeHost(e.hblob);
   e.hblob = nullptr;
   size_t cap = std::max(need, e.hcap + e.hcap / 2);
-  CUDA_TRY(rt, cudaHostAlloc((void **)&e.hblob, cap, cudaHostAllocPortable));
+  CUDA_TRY(rt, cudaHostAlloc((void **)&e.hblob, cap, cudaHostAllocPortable | cudaHostAllocMapped));
+  CUDA_TRY(rt, cudaHostGetDevicePointer((void **)&e.hblob_dev, e.hblob, 0));
   e.hcap = cap;
   return 0;
 }
@@ -476,7 +479,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   const size_t dneed = o_trace + (traced ? 36 * U : 0);
   const size_t o_readback = align_up(upload, 64);
   const size_t o_trace_h = o_readback + 64;
-  const size_t hneed = o_trace_h + (traced ? 36 * U : 0);
+  const size_t hneed = align_up(o_trace_h + (traced ? 36 * U : 0), 16);
   if (int r = ensure_host(rt, e, hneed)) return r;
   if (int r = ensure_dev(rt, e, dneed)) return r;
 
@@ -551,7 +554,10 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     CUDA_TRY(rt, cudaEventRecord(rt->span_start, stream));
     rt->span_open = true;
   }
-  CUDA_TRY(rt, cudaMemcpyAsync(d, h, upload, cudaMemcpyHostToDevice, stream));
+  bool uploads_pending = false;
+  for (auto &kv2 : rt->caches) uploads_pending |= !kv2.second.uploads.empty();
+  if (uploads_pending) CUDA_TRY(rt, launch_stage(d, e.hblob_dev, upload, stream));   // copy engine is busy
+  else CUDA_TRY(rt, cudaMemcpyAsync(d, h, upload, cudaMemcpyHostToDevice, stream));
   if (U > U0) CUDA_TRY(rt, cudaMemsetAsync(d + o_queue + 8 * U0, 0xFF, 8 * (U - U0), stream));
   CUDA_TRY(rt, cudaMemsetAsync(d + o_cdone, 0, 4 * N, stream));
 

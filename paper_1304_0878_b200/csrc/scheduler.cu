@@ -791,6 +791,22 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sw(Epoch
   report_exit(a);
 }
 
+// Copy an epoch blob from mapped pinned host memory with SM loads.  Used
+// instead of a copy-engine memcpy while large chunked uploads occupy the
+// host-to-device copy engine (the blob would queue behind gigabytes).
+__global__ void __launch_bounds__(256) stage_kernel(uint4 *dst, const uint4 *src, size_t n16) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+cudaError_t launch_stage(void *dst, const void *src_mapped, size_t bytes, cudaStream_t stream) {
+  const size_t n16 = (bytes + 15) / 16;
+  const int grid = (int)((n16 + 255) / 256 < 1184 ? (n16 + 255) / 256 : 1184);
+  stage_kernel<<<grid > 0 ? grid : 1, 256, 0, stream>>>(static_cast<uint4 *>(dst), static_cast<const uint4 *>(src_mapped),
+                                                        n16);
+  return cudaGetLastError();
+}
+
 // Host-side launcher (called from runtime.cpp).
 cudaError_t launch_epoch(const EpochArgs &args, int grid, cudaStream_t stream, bool release_warp) {
   if (release_warp) scheduler_kernel_rw<<<grid, kBlock, 0, stream>>>(args);
