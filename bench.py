@@ -197,6 +197,7 @@ def main():
     ap.add_argument("--ref-tiles", type=int, default=64)
     ap.add_argument("--chunk-bytes", type=int, default=0, help="fixed work-unit size (0 = adaptive)")
     ap.add_argument("--host-threads", type=int, default=0)
+    ap.add_argument("--rounds", type=int, default=0, help="pipelined rounds per SCAL run (0 = library default)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -248,7 +249,7 @@ def main():
     threads = args.host_threads or max(1, min(16, (os.cpu_count() or 2) // int(
         os.environ.get("LOCAL_WORLD_SIZE", "1")) - 2))
     rt = B.Runtime(device=local_dev, stream=stream.cuda_stream, rank=0, nranks=1, flags=flags,
-                   chunk_bytes=args.chunk_bytes, host_threads=threads)
+                   chunk_bytes=args.chunk_bytes, host_threads=threads, pipeline_rounds=args.rounds)
 
     # ---- device-resident inputs (registered once, outside the timed region)
     x = synth_tile_values(torch, elems, 1000 + rank, dev)
