@@ -30,7 +30,8 @@
 namespace bt {
 cudaError_t launch_epoch(const EpochArgs &args, int grid, cudaStream_t stream, bool release_warp);
 cudaError_t scheduler_occupancy(int *blocks_per_sm, int *block);
-cudaError_t launch_stage(void *dst, const void *src_mapped, size_t bytes, cudaStream_t stream);
+cudaError_t launch_stage(void *dst, const void *src_mapped, size_t bytes, unsigned long long *q_empty, size_t nq,
+                         uint32_t *zero, size_t nz, cudaStream_t stream);
 int max_factors();
 }  // namespace bt
 
@@ -50,6 +51,7 @@ constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;   // 20 s
 constexpr size_t kParallelPack = 4096;              // items above which the pack runs on the pool
 constexpr uint64_t kReleaseWarpBelow = 16384;       // work units smaller than this use the "rw" kernel
 constexpr uint64_t kUploadChunk = 64ull << 20;      // registrations >= this upload in chunks on a copy stream
+constexpr size_t kStageBelow = 1u << 20;            // epoch blobs up to this size are pulled by the set-up kernel
 
 const char *codelet_name(int c) {
   switch (c) {
@@ -554,12 +556,15 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     CUDA_TRY(rt, cudaEventRecord(rt->span_start, stream));
     rt->span_open = true;
   }
+  // small blobs (and any blob while chunked uploads occupy the copy engine)
+  // are pulled by the set-up kernel from mapped memory; large ones by a memcpy
   bool uploads_pending = false;
   for (auto &kv2 : rt->caches) uploads_pending |= !kv2.second.uploads.empty();
-  if (uploads_pending) CUDA_TRY(rt, launch_stage(d, e.hblob_dev, upload, stream));   // copy engine is busy
-  else CUDA_TRY(rt, cudaMemcpyAsync(d, h, upload, cudaMemcpyHostToDevice, stream));
-  if (U > U0) CUDA_TRY(rt, cudaMemsetAsync(d + o_queue + 8 * U0, 0xFF, 8 * (U - U0), stream));
-  CUDA_TRY(rt, cudaMemsetAsync(d + o_cdone, 0, 4 * N, stream));
+  const bool sm_copy = uploads_pending || upload <= kStageBelow;
+  if (!sm_copy) CUDA_TRY(rt, cudaMemcpyAsync(d, h, upload, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(rt, launch_stage(d, sm_copy ? e.hblob_dev : nullptr, upload,
+                            reinterpret_cast<unsigned long long *>(d + o_queue) + U0, U - U0,
+                            reinterpret_cast<uint32_t *>(d + o_cdone), N, stream));
 
   EpochArgs a{};
   a.items = reinterpret_cast<const DItem *>(d + o_items);

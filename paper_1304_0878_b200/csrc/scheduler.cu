@@ -791,19 +791,30 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sw(Epoch
   report_exit(a);
 }
 
-// Copy an epoch blob from mapped pinned host memory with SM loads.  Used
-// instead of a copy-engine memcpy while large chunked uploads occupy the
-// host-to-device copy engine (the blob would queue behind gigabytes).
-__global__ void __launch_bounds__(256) stage_kernel(uint4 *dst, const uint4 *src, size_t n16) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
-    dst[i] = src[i];
+// Epoch set-up in one launch: copy the epoch blob from mapped pinned host
+// memory with SM loads (optional: used for small blobs, and while chunked
+// uploads occupy the host-to-device copy engine, where a memcpy would queue
+// behind gigabytes), mark the not-yet-published queue slots EMPTY and zero
+// the per-item chunk counters (replaces two memsets).
+__global__ void __launch_bounds__(256) stage_kernel(uint4 *dst, const uint4 *src, size_t n16,
+                                                    unsigned long long *q_empty, size_t nq, uint32_t *zero,
+                                                    size_t nz) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  for (size_t i = tid; i < n16; i += stride) dst[i] = src[i];
+  for (size_t i = tid; i < nq; i += stride) q_empty[i] = Q_EMPTY;
+  for (size_t i = tid; i < nz; i += stride) zero[i] = 0u;
 }
 
-cudaError_t launch_stage(void *dst, const void *src_mapped, size_t bytes, cudaStream_t stream) {
-  const size_t n16 = (bytes + 15) / 16;
-  const int grid = (int)((n16 + 255) / 256 < 1184 ? (n16 + 255) / 256 : 1184);
-  stage_kernel<<<grid > 0 ? grid : 1, 256, 0, stream>>>(static_cast<uint4 *>(dst), static_cast<const uint4 *>(src_mapped),
-                                                        n16);
+cudaError_t launch_stage(void *dst, const void *src_mapped, size_t bytes, unsigned long long *q_empty, size_t nq,
+                         uint32_t *zero, size_t nz, cudaStream_t stream) {
+  const size_t n16 = src_mapped ? (bytes + 15) / 16 : 0;
+  size_t work = n16 > nq ? n16 : nq;
+  if (nz > work) work = nz;
+  const size_t blocks = (work + 255) / 256;
+  const int grid = (int)(blocks < 1184 ? (blocks > 0 ? blocks : 1) : 1184);
+  stage_kernel<<<grid, 256, 0, stream>>>(static_cast<uint4 *>(dst), static_cast<const uint4 *>(src_mapped), n16,
+                                         q_empty, nq, zero, nz);
   return cudaGetLastError();
 }
 
