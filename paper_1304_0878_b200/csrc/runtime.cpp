@@ -556,6 +556,10 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     CUDA_TRY(rt, cudaEventRecord(rt->span_start, stream));
     rt->span_open = true;
   }
+  // the set-up kernel copies whole 16-byte words: the word holding the last
+  // initially-ready unit may extend into queue[U0], which must read EMPTY
+  // (it also writes EMPTY there; both writes agree)
+  if (U > U0) q[U0] = Q_EMPTY;
   // small blobs (and any blob while chunked uploads occupy the copy engine)
   // are pulled by the set-up kernel from mapped memory; large ones by a memcpy
   bool uploads_pending = false;
