@@ -46,7 +46,7 @@ constexpr uint32_t kDefaultMaxFused = 256;
 constexpr uint32_t kDefaultParallelMin = 16384;
 constexpr int kDefaultRounds = 4;
 constexpr uint32_t kDefaultPipelineMin = 131072;
-constexpr int kEpochRing = 8;                       // epoch buffers in flight (>= rounds + 2)
+constexpr int kEpochRing = 12;                      // epoch buffers in flight (>= rounds + 2)
 constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;   // 20 s
 constexpr size_t kParallelPack = 4096;              // items above which the pack runs on the pool
 constexpr uint64_t kReleaseWarpBelow = 16384;       // work units smaller than this use the "rw" kernel

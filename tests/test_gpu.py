@@ -345,3 +345,20 @@ def test_large_host_buffer_untouched_and_axpy(B):
         rt.unregister(hb)
     assert_bits_equal(a, a0, "untouched")
     assert_bits_equal(b, (np.float32(0.5) * a0 + b0).astype(np.float32), "axpy")
+
+
+def test_stress_random_configurations(B):
+    """Random programs under random runtime configurations (work-unit size,
+    fusion, builder threads, pipelining thresholds, epoch auto-flush): every
+    path of the builder and both kernels against the oracle."""
+    rng = np.random.default_rng(2024)
+    for trial in range(60):
+        p = W.random_small_program(9000 + trial, max_tasks=int(rng.integers(5, 80)),
+                                   max_handles=int(rng.integers(1, 6)), max_elems=int(rng.integers(8, 20000)))
+        kw = dict(chunk_bytes=int(rng.choice([0, 32, 64, 512, 4096, 65536])),
+                  flags=0 if rng.random() < 0.7 else B.BT_FLAG_NO_FUSION,
+                  host_threads=int(rng.integers(1, 6)), parallel_min=int(rng.integers(1, 8)),
+                  pipeline_min=int(rng.integers(1, 16)), pipeline_rounds=int(rng.integers(1, 5)),
+                  max_fused=int(rng.choice([0, 1, 2, 3, 7])),
+                  epoch_tasks=int(rng.choice([0, 0, 3, 11])))
+        compare_program(p, **kw)
