@@ -45,6 +45,7 @@ constexpr uint32_t kUnitsPerCta = 16;               // adaptive chunking: target
 constexpr uint32_t kDefaultMaxFused = 256;
 constexpr uint32_t kDefaultParallelMin = 16384;
 constexpr int kDefaultRounds = 4;
+constexpr int kRoundsUploading = 8;                 // rounds for partitions of data still being uploaded
 constexpr uint32_t kDefaultPipelineMin = 131072;
 constexpr int kEpochRing = 12;                      // epoch buffers in flight (>= rounds + 2)
 constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;   // 20 s
@@ -157,7 +158,9 @@ struct bt_runtime {
   std::vector<Lane> lanes;
   std::vector<vec<LaneEntry>> buckets;                  // [chunk][round * P + lane]
   std::vector<vec<uint32_t>> bucket_tasks;              // task indices (record_tasks only)
-  int npool = 1, nrounds = 1;
+  int npool = 1;
+  int nrounds = 1;        // bucket rounds (max over round policies)
+  int rounds_default = 1; // rounds of a partition of device-resident data
   EpochBuf ep[kEpochRing];
   int ep_cur = 0;
   uint64_t ep_seq = 0;
@@ -262,7 +265,7 @@ uint32_t alloc_slots(bt_runtime *rt, uint32_t count) {
     h.gen = gen;
     h.flags = F_LIVE;
     const uint32_t k = (s + i) >> 6;    // 64-slot block -> lane k % P, round (k / P) % R
-    h.grp = ((k / (uint32_t)rt->npool) % (uint32_t)rt->nrounds) * (uint32_t)rt->npool + k % (uint32_t)rt->npool;
+    h.grp = ((k / (uint32_t)rt->npool) % (uint32_t)rt->rounds_default) * (uint32_t)rt->npool + k % (uint32_t)rt->npool;
     rt->slots[s + i] = Slot();
     rt->deps[s + i] = DepState();
   }
@@ -723,10 +726,12 @@ int bt_init(const bt_config *cfg_in, bt_runtime **out) {
     threads = (int)std::min<unsigned>(16, hw > 4 ? hw - 2 : hw);
   }
   rt->pool.reset(new Pool(threads));
-  rt->lanes.resize((size_t)threads * cfg.pipeline_rounds);   // [lane * R + round] when not pipelined
+
   rt->npool = threads;
-  rt->nrounds = cfg.pipeline_rounds;
-  rt->buckets.resize((size_t)threads * threads * cfg.pipeline_rounds);   // [chunk][round * P + lane]
+  rt->rounds_default = cfg.pipeline_rounds;
+  rt->nrounds = std::max(cfg.pipeline_rounds, cfg.pipeline_rounds > 1 ? kRoundsUploading : 1);
+  rt->lanes.resize((size_t)threads * rt->nrounds);                  // [lane * R + round] when not pipelined
+  rt->buckets.resize((size_t)threads * threads * rt->nrounds);      // [chunk][round * P + lane]
   rt->bucket_tasks.resize(rt->buckets.size());
 
   if (!rt->host_only) {
@@ -945,6 +950,13 @@ int bt_data_partition(bt_runtime *rt, bt_handle h, uint32_t nparts) {
   SlotHot &ph = rt->hot[s];
   Slot &p = rt->slots[s];
   const uint64_t base = ph.nx / nparts, extra = ph.nx % nparts;
+  // data still arriving by chunked upload: finer rounds, so computation and
+  // write-back follow the upload more closely (the e2e path is PCIe-bound)
+  uint32_t rounds = (uint32_t)rt->rounds_default;
+  {
+    auto it = rt->caches.find(p.root);
+    if (it != rt->caches.end() && !it->second.uploads.empty() && rounds > 1) rounds = (uint32_t)rt->nrounds;
+  }
   for (uint32_t t = 0; t < nparts; ++t) {
     SlotHot &ch = rt->hot[c0 + t];
     Slot &c = rt->slots[c0 + t];
@@ -959,7 +971,7 @@ int bt_data_partition(bt_runtime *rt, bt_handle h, uint32_t nparts) {
     // pipelined rounds take contiguous quarters of the parts (so round r
     // needs only its own upload chunks and writes back one contiguous range);
     // lanes still own whole 64-slot blocks
-    const uint32_t round = (uint32_t)((uint64_t)t * (uint32_t)rt->nrounds / nparts);
+    const uint32_t round = (uint32_t)((uint64_t)t * rounds / nparts);
     ch.grp = round * (uint32_t)rt->npool + ((c0 + t) >> 6) % (uint32_t)rt->npool;
   }
   p.nparts = nparts;
