@@ -1228,7 +1228,12 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
   // index over the lane's blocks: (k / P) * 64 + (s & 63)
   const uint32_t nlocal = (uint32_t)((((nslots + 63) >> 6) + P - 1) / P) * 64;
   const int rounds = pipelined ? R : 1;
+  std::vector<size_t> round_size(R, 0);
+  for (int c = 0; c < P; ++c)
+    for (int r = 0; r < R; ++r)
+      for (int l = 0; l < P; ++l) round_size[r] += rt->buckets[(size_t)c * G + (size_t)r * P + l].size();
   for (int rr = 0; rr < rounds; ++rr) {
+    if (pipelined && round_size[rr] == 0) continue;   // rounds of another round policy
     const double ta = now_ms();
     rt->par([&](int l) {
       // non-pipelined: this lane builds its groups of every round in one go
