@@ -796,7 +796,10 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sw(Epoch
 // uploads occupy the host-to-device copy engine, where a memcpy would queue
 // behind gigabytes), mark the not-yet-published queue slots EMPTY and zero
 // the per-item chunk counters (replaces two memsets).
-__global__ void __launch_bounds__(256) stage_kernel(uint4 *dst, const uint4 *src, size_t n16,
+// Small blocks (64 threads, <= 32 registers) so that the set-up of round r+1
+// fits beside round r's persistent CTAs (3 x 288 threads x 72 registers per
+// SM) instead of waiting for them to exit.
+__global__ void __launch_bounds__(64, 32) stage_kernel(uint4 *dst, const uint4 *src, size_t n16,
                                                     unsigned long long *q_empty, size_t nq, uint32_t *zero,
                                                     size_t nz) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -811,10 +814,10 @@ cudaError_t launch_stage(void *dst, const void *src_mapped, size_t bytes, unsign
   const size_t n16 = src_mapped ? (bytes + 15) / 16 : 0;
   size_t work = n16 > nq ? n16 : nq;
   if (nz > work) work = nz;
-  const size_t blocks = (work + 255) / 256;
-  const int grid = (int)(blocks < 1184 ? (blocks > 0 ? blocks : 1) : 1184);
-  stage_kernel<<<grid, 256, 0, stream>>>(static_cast<uint4 *>(dst), static_cast<const uint4 *>(src_mapped), n16,
-                                         q_empty, nq, zero, nz);
+  const size_t blocks = (work + 63) / 64;
+  const int grid = (int)(blocks < 296 ? (blocks > 0 ? blocks : 1) : 296);
+  stage_kernel<<<grid, 64, 0, stream>>>(static_cast<uint4 *>(dst), static_cast<const uint4 *>(src_mapped), n16,
+                                        q_empty, nq, zero, nz);
   return cudaGetLastError();
 }
 
