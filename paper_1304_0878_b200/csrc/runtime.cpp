@@ -53,6 +53,7 @@ constexpr size_t kParallelPack = 4096;              // items above which the pac
 constexpr uint64_t kReleaseWarpBelow = 16384;       // work units smaller than this use the "rw" kernel
 constexpr uint64_t kUploadChunk = 64ull << 20;      // registrations >= this upload in chunks on a copy stream
 constexpr size_t kStageBelow = 1u << 20;            // epoch blobs up to this size are pulled by the set-up kernel
+constexpr uint64_t kDagChunkElems = 16384;          // work-unit cap (64 KiB) for epochs with dependencies
 
 const char *codelet_name(int c) {
   switch (c) {
@@ -411,7 +412,11 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   const size_t stride = std::max<size_t>(1, N / 4096);
   uint64_t sampled = 0, cnt = 0;
   for (size_t i = 0; i < N; i += stride, ++cnt) sampled += B.items[i].n;
-  const uint64_t CE = chunk_elems_for(rt, sampled / cnt * N);
+  uint64_t CE = chunk_elems_for(rt, sampled / cnt * N);
+  // a DAG's ready width can be far below the item count (C3: ~16 ready 4 MiB
+  // tasks): smaller units keep all SMs busy (measured: 64 KiB units 14.6 ms
+  // vs 256 KiB 17.2 ms on C3, tools/c3_chunks.py)
+  if (E > 0 && !rt->cfg.chunk_bytes) CE = std::min(CE, kDagChunkElems);
 
   // Pass A (per range): units, initially ready units, successors, factors
   // (a SCAL item whose factor list equals the previous item's reuses it).
