@@ -362,3 +362,27 @@ def test_stress_random_configurations(B):
                   max_fused=int(rng.choice([0, 1, 2, 3, 7])),
                   epoch_tasks=int(rng.choice([0, 0, 3, 11])))
         compare_program(p, **kw)
+
+
+def test_c_example_program(B, tmp_path):
+    """examples/vector_scal.c: the paper's running example written in C
+    against include/btask.h, linked with libbtask.so."""
+    import os
+    import re
+    import struct
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib_dir = os.path.join(root, "paper_1304_0878_b200")
+    exe = str(tmp_path / "vector_scal")
+    subprocess.check_call(["gcc", "-O2", "-Wall", "-I", os.path.join(root, "include"),
+                           os.path.join(root, "examples", "vector_scal.c"), "-L", lib_dir, "-lbtask",
+                           f"-Wl,-rpath,{lib_dir}", "-o", exe])
+    out = subprocess.check_output([exe], text=True, timeout=120)
+    from tests.golden import load
+    pins = load("scal_pins.txt")
+    last = float(re.search(r"vector\[1023\] = (\S+)", out).group(1))
+    assert f"{struct.unpack('<I', struct.pack('<f', last))[0]:08X}" == pins["c1_last"][0][0]
+    assert "attempt to use unregistered pointer" in out
+    big0 = float(re.search(r"big\[0\] = (\S+)", out).group(1))
+    assert f"{struct.unpack('<I', struct.pack('<f', big0))[0]:08X}" == pins["chain_k16"][0][0]
+    assert "1025 tasks in 65 items (960 fused)" in out   # 1 + 16 x 64 tasks; chains fuse per tile
