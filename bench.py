@@ -171,16 +171,30 @@ def cpu_baseline(np, seconds_target=12.0):
     p = W.sweep_program(x.shape[0], ntile, f, x)
     off0, len0, off1, len1 = oracle.model.resolve(p)
     t = p.tasks
-    reps, t0 = 0, time.perf_counter()
-    while True:
-        oracle.run_tasks([x], t["codelet"], t["scalar"], t["b0"], off0, len0, t["b1"], off1, len1)
-        reps += 1
-        if time.perf_counter() - t0 > seconds_target:
-            break
-    dt = time.perf_counter() - t0
+    # single-threaded by definition (submission order), pinned to one core
+    old_aff = os.sched_getaffinity(0)
+    core = min(old_aff)
+    os.sched_setaffinity(0, {core})
+    try:
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            oracle.run_tasks([x], t["codelet"], t["scalar"], t["b0"], off0, len0, t["b1"], off1, len1)
+            reps += 1
+            if time.perf_counter() - t0 > seconds_target:
+                break
+        dt = time.perf_counter() - t0
+    finally:
+        os.sched_setaffinity(0, old_aff)
+    cpu = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            cpu = next(l.split(":", 1)[1].strip() for l in fh if l.startswith("model name"))
+    except Exception:
+        pass
     return {"value": 8.0 * ntile * tile * reps / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
             "sample": f"{reps} x ({ntile} tiles x {tile} floats x {C5['sweeps']} sweeps, task-major), "
-                      f"{dt:.1f} s single-threaded",
+                      f"{dt:.1f} s single-threaded pinned to core {core}",
+            "host": {"cpu": cpu, "nproc": os.cpu_count()},
             "tasks_per_s": reps * ntile * C5["sweeps"] / dt}
 
 
