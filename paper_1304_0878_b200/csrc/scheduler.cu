@@ -467,10 +467,114 @@ __device__ __forceinline__ void st_release_cta_u32(unsigned *p, unsigned v) {
 }
 
 // Compute warps: run units slot after slot until the STOP unit.
+#ifndef BT_BULK
+#define BT_BULK 0
+#endif
+#if BT_BULK
+// ---- SCAL chain through shared memory with 1-D bulk copies (TMA engine) ----
+// Each compute warp streams its sub-blocks of the unit through two 2 KiB
+// shared-memory stages: lane 0 issues cp.async.bulk global->shared for the
+// next sub-block (completion on an mbarrier with expect_tx) and
+// cp.async.bulk shared->global for the finished one, so the warps' FMUL2
+// stream never waits on a global load.
+#ifndef BT_BULK_SB
+#define BT_BULK_SB 512
+#endif
+constexpr int kSB = BT_BULK_SB;               // floats per sub-block (2 KiB)
+constexpr int kSBQ = kSB / 128;               // float4s per lane per sub-block
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load(float *smem, const float *gmem, unsigned bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store(float *gmem, const float *smem, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem),
+               "r"((unsigned)__cvta_generic_to_shared(smem)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+
+// x: 32-byte aligned start of the vector part, nv: 8-float vectors.
+// buf: this warp's 2 x kSB floats; bar: its 2 mbarriers; ph: their phase bits.
+template <int W>
+__device__ void scal_bulk(float *x, uint64_t nv, const float *sf, uint32_t k, int w, int lane, float *buf,
+                          uint64_t *bar, unsigned &ph) {
+  const uint64_t nflt = 8 * nv;
+  const uint64_t nsb = (nflt + kSB - 1) / kSB;
+  if ((uint64_t)w >= nsb) return;
+  auto sb_bytes = [&](uint64_t j) -> unsigned {
+    const uint64_t lo = j * kSB;
+    return (unsigned)(4 * (nflt - lo < (uint64_t)kSB ? nflt - lo : (uint64_t)kSB));
+  };
+  fence_proxy_async();   // generic-proxy writes acquired earlier -> visible to the bulk loads
+  if (lane == 0) {
+    mbar_expect_tx(&bar[0], sb_bytes(w));
+    bulk_load(buf, x + (uint64_t)w * kSB, sb_bytes(w), &bar[0]);
+  }
+  int st = 0;
+  for (uint64_t j = w; j < nsb; j += W, st ^= 1) {
+    const uint64_t jn = j + W;
+    if (jn < nsb && lane == 0) {
+      bulk_wait_read();   // the stage we refill has been read by its bulk store
+      mbar_expect_tx(&bar[st ^ 1], sb_bytes(jn));
+      bulk_load(buf + (st ^ 1) * kSB, x + jn * kSB, sb_bytes(jn), &bar[st ^ 1]);
+    }
+    mbar_wait(&bar[st], (ph >> st) & 1u);
+    ph ^= 1u << st;
+    float *sb = buf + st * kSB;
+    const unsigned bytes = sb_bytes(j);
+    const int nq = (int)(bytes / 16);          // float4s in this sub-block (multiple of 2)
+    float v[kSBQ / 2][8];
+#pragma unroll
+    for (int q = 0; q < kSBQ; ++q) {
+      const int idx = q * 32 + lane;
+      float4 f = idx < nq ? reinterpret_cast<const float4 *>(sb)[idx] : make_float4(1.f, 1.f, 1.f, 1.f);
+      v[q >> 1][(q & 1) * 4 + 0] = f.x;
+      v[q >> 1][(q & 1) * 4 + 1] = f.y;
+      v[q >> 1][(q & 1) * 4 + 2] = f.z;
+      v[q >> 1][(q & 1) * 4 + 3] = f.w;
+    }
+    chain_apply<kSBQ / 2>(v, sf, k);
+#pragma unroll
+    for (int q = 0; q < kSBQ; ++q) {
+      const int idx = q * 32 + lane;
+      if (idx < nq)
+        reinterpret_cast<float4 *>(sb)[idx] =
+            make_float4(v[q >> 1][(q & 1) * 4 + 0], v[q >> 1][(q & 1) * 4 + 1], v[q >> 1][(q & 1) * 4 + 2],
+                        v[q >> 1][(q & 1) * 4 + 3]);
+    }
+    fence_proxy_async();   // this lane's shared-memory writes -> visible to the bulk store
+    __syncwarp();
+    if (lane == 0) bulk_store(x + j * kSB, sb, bytes);
+  }
+  if (lane == 0) {
+    bulk_wait_all();       // the unit's results are in global memory
+    fence_proxy_async();   // ... and ordered before the generic-proxy release that follows
+  }
+  __syncwarp();
+}
+#endif
+
 template <int C, int S>
 __device__ __forceinline__ void compute_loop(const EpochArgs &a, const unsigned long long *s_unit,
-                                             float (*s_fac)[kMaxFactors], uint64_t *s_empty, int lane) {
+                                             float (*s_fac)[kMaxFactors], uint64_t *s_empty, int lane,
+                                             float *s_bulk = nullptr, uint64_t *s_bulk_bar = nullptr) {
   const int tid = threadIdx.x - (kBlock - C);
+#if BT_BULK
+  const int cw = tid >> 5;
+  unsigned bulk_ph = 0;
+#endif
   for (unsigned u = 0;; ++u) {
     const int b = (int)(u % S);
     bar_sync(kBarFull + b, 32 + C);   // FULL[b]: the pop warp + the compute warps
@@ -483,6 +587,20 @@ __device__ __forceinline__ void compute_loop(const EpochArgs &a, const unsigned 
     const uint64_t hi = min(it.n, lo + a.chunk_elems);
     switch (it.kind & K_MASK) {
       case K_SCAL:
+#if BT_BULK
+        if (s_bulk) {
+          float *xs = reinterpret_cast<float *>(it.x) + lo;
+          const uint64_t n = hi - lo;
+          const uint64_t head = head_elems(xs, n);
+          for (uint64_t i = tid; i < head; i += C) __stcg(xs + i, chain_scalar(__ldcg(xs + i), s_fac[b], it.k));
+          const uint64_t nv = (n - head) >> 3;
+          scal_bulk<C / 32>(xs + head, nv, s_fac[b], it.k, cw, lane, s_bulk + cw * 2 * kSB, s_bulk_bar + 2 * cw,
+                            bulk_ph);
+          for (uint64_t t = head + 8 * nv + tid; t < n; t += C)
+            __stcg(xs + t, chain_scalar(__ldcg(xs + t), s_fac[b], it.k));
+          break;
+        }
+#endif
         scal_range<4, C>(reinterpret_cast<float *>(it.x) + lo, hi - lo, s_fac[b], it.k, tid);
         break;
       case K_AXPY:
@@ -713,10 +831,21 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sw(Epoch
   __shared__ unsigned long long s_unit[2];
   __shared__ __align__(8) uint64_t s_empty[2];
   __shared__ __align__(16) float s_fac[2][kMaxFactors];
+#if BT_BULK
+  __shared__ __align__(128) float s_bulk[kCompute / 32][2][kSB];
+  __shared__ __align__(8) uint64_t s_bulk_bar[kCompute / 32][2];
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     mbar_init(&s_empty[0], kCompute / 32);
     mbar_init(&s_empty[1], kCompute / 32);
+#if BT_BULK
+    for (int w = 0; w < kCompute / 32; ++w) {
+      mbar_init(&s_bulk_bar[w][0], 1);
+      mbar_init(&s_bulk_bar[w][1], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#endif
   }
   __syncthreads();
 
@@ -786,7 +915,11 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sw(Epoch
       }
     }
   } else {
+#if BT_BULK
+    compute_loop<kCompute, kSlotsSW>(a, s_unit, s_fac, s_empty, lane, &s_bulk[0][0][0], &s_bulk_bar[0][0]);
+#else
     compute_loop<kCompute, kSlotsSW>(a, s_unit, s_fac, s_empty, lane);
+#endif
   }
   report_exit(a);
 }
