@@ -386,3 +386,39 @@ def test_c_example_program(B, tmp_path):
     big0 = float(re.search(r"big\[0\] = (\S+)", out).group(1))
     assert f"{struct.unpack('<I', struct.pack('<f', big0))[0]:08X}" == pins["chain_k16"][0][0]
     assert "1025 tasks in 65 items (960 fused)" in out   # 1 + 16 x 64 tasks; chains fuse per tile
+
+
+@pytest.mark.slow
+def test_bench_launch_configuration_c5(B):
+    """bench.py's exact path at full size: device-homed 4 GiB tensor, 16,384
+    tiles, the C5 task stream through bt_insert_task_batch with the default
+    configuration (pipelined rounds on the "sw" kernel), two steps; sampled
+    elements against the oracle."""
+    import importlib.util
+    import os
+    import torch
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    n, T, S = 1 << 30, 16384, 64
+    f = W.sweep_factors(np.random.default_rng(W.SEED_BASE + 4), S)
+    x = bench.synth_tile_values(torch, n, 1000, torch.device("cuda", 0))
+    rng = np.random.default_rng(5)
+    idx = np.unique(np.concatenate([rng.integers(0, n, 1 << 18), np.arange(T) * (n // T), [n - 1]]))
+    x0 = x[torch.from_numpy(idx).cuda()].cpu().numpy()
+    stream = torch.cuda.current_stream()
+    with B.Runtime(stream=stream.cuda_stream) as rt:
+        h = rt.register_tensor(x)
+        subs = rt.partition(h, T)
+        c, s, h0 = bench.rank_tasks(np, subs, f)
+        for _ in range(2):
+            rt.insert_batch(c, s, h0)
+            rt.wait()
+        st = rt.stats()
+        rt.unpartition(h)
+        rt.unregister(h)
+    assert st["epochs"] >= 8 and st["items"] == 2 * T
+    got = x[torch.from_numpy(idx).cuda()].cpu().numpy()
+    exp = oracle.scal_chain(oracle.scal_chain(x0, f), f)
+    assert_bits_equal(got, exp, "bench configuration, two steps")

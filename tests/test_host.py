@@ -259,6 +259,22 @@ def test_error_conventions(B):
         rt.unregister(h)                                  # double unregister
     assert ei.value.code == -errno.ENOENT
     rt.unregister(hy)
+    # degenerate sizes (nx == 0, nparts == 0 or > nx) are rejected
+    z = np.ones(3, np.float32)
+    with pytest.raises(B.BtError) as ei:
+        rt.register(z.ctypes.data, 0)
+    assert ei.value.code == -errno.EINVAL
+    hz = rt.register_array(z)
+    for bad in (0, 4):
+        with pytest.raises(B.BtError) as ei:
+            rt.partition(hz, bad)
+        assert ei.value.code == -errno.EINVAL
+    assert len(rt.partition(hz, 3)) == 3          # one element per part is fine
+    with pytest.raises(B.BtError) as ei:
+        rt.partition(hz, 2)                        # already partitioned
+    assert ei.value.code == -errno.EBUSY
+    rt.unpartition(hz)
+    rt.unregister(hz)
     # re-registration of the same memory is allowed after unregister
     h2 = rt.register_array(x)
     rt.unregister(h2)
