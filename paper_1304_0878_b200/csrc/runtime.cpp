@@ -196,6 +196,7 @@ struct bt_runtime {
 
   // pack scratch
   std::vector<uint32_t> succ_off, cursor;
+  size_t hcap_max = 0, dcap_max = 0;     // largest epoch buffers allocated so far
 
   template <class F>
   void par(F &&f) {
@@ -319,11 +320,15 @@ int check_live(bt_runtime *rt) {
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// Epoch buffers grow to the largest size any ring slot has needed so far, so
+// each slot allocates about once instead of growing step by step (pinned and
+// device allocations cost milliseconds each).
 int ensure_host(bt_runtime *rt, EpochBuf &e, size_t need) {
   if (e.hcap >= need) return 0;
   if (e.hblob) cudaFreeHost(e.hblob);
   e.hblob = nullptr;
-  size_t cap = std::max(need, e.hcap + e.hcap / 2);
+  size_t cap = std::max({need, e.hcap + e.hcap / 2, rt->hcap_max});
+  rt->hcap_max = cap;
   CUDA_TRY(rt, cudaHostAlloc((void **)&e.hblob, cap, cudaHostAllocPortable | cudaHostAllocMapped));
   CUDA_TRY(rt, cudaHostGetDevicePointer((void **)&e.hblob_dev, e.hblob, 0));
   e.hcap = cap;
@@ -334,7 +339,8 @@ int ensure_dev(bt_runtime *rt, EpochBuf &e, size_t need) {
   if (e.dcap >= need) return 0;
   if (e.dblob) cudaFree(e.dblob);
   e.dblob = nullptr;
-  size_t cap = std::max(need, e.dcap + e.dcap / 2);
+  size_t cap = std::max({need, e.dcap + e.dcap / 2, rt->dcap_max});
+  rt->dcap_max = cap;
   cudaError_t err = cudaMalloc((void **)&e.dblob, cap);
   if (err != cudaSuccess) {
     cudaGetLastError();
