@@ -344,10 +344,31 @@ __device__ __forceinline__ bool mailbox_put(const Mailbox &mb, unsigned long lon
   return true;
 }
 
-__device__ __forceinline__ void release_unit(const EpochArgs &a, uint32_t item, const Mailbox &mb = Mailbox{}) {
+// Release metadata of a unit: read-only descriptors, so the release warp
+// loads them while the unit is still being computed (off the critical path).
+struct RelMeta {
+  uint32_t nchunks, nsucc, off;
+  uint32_t s0, s0kind, s0nc;   // first successor (valid if nsucc > 0)
+};
+__device__ __forceinline__ RelMeta release_meta(const EpochArgs &a, uint32_t item) {
+  RelMeta m;
   const DItem &it = a.items[item];
-  const uint32_t nchunks = __ldg(&it.nchunks);
-  const uint32_t nsucc = __ldg(&it.nsucc), off = __ldg(&it.succ_off);
+  m.nchunks = __ldg(&it.nchunks);
+  m.nsucc = __ldg(&it.nsucc);
+  m.off = __ldg(&it.succ_off);
+  m.s0 = m.s0kind = m.s0nc = 0;
+  if (m.nsucc) {
+    m.s0 = __ldg(&a.succ[m.off]);
+    m.s0kind = __ldg(&a.items[m.s0].kind);
+    m.s0nc = __ldg(&a.items[m.s0].nchunks);
+  }
+  return m;
+}
+
+__device__ __forceinline__ void release_unit(const EpochArgs &a, uint32_t item, const Mailbox &mb = Mailbox{},
+                                             const RelMeta *pre = nullptr) {
+  const RelMeta m = pre ? *pre : release_meta(a, item);
+  const uint32_t nchunks = m.nchunks, nsucc = m.nsucc, off = m.off;
   if (nchunks > 1) {
     const unsigned c = atom_add_acq_rel(&a.chunk_done[item], 1u);
     if (c + 1 != nchunks) {
@@ -356,15 +377,15 @@ __device__ __forceinline__ void release_unit(const EpochArgs &a, uint32_t item, 
     }
   }
   for (uint32_t i = 0; i < nsucc; ++i) {
-    const uint32_t s = __ldg(&a.succ[off + i]);
-    const uint32_t skind = __ldg(&a.items[s].kind);
+    const uint32_t s = i == 0 ? m.s0 : __ldg(&a.succ[off + i]);
+    const uint32_t skind = i == 0 ? m.s0kind : __ldg(&a.items[s].kind);
     // a single-predecessor successor is ready now (no counter); with more
     // predecessors the acq_rel RMW both releases ours and acquires theirs
     const bool ready = mb.unit && (skind & K_SINGLE_PRED)
                            ? true
                            : atom_add_acq_rel(reinterpret_cast<unsigned *>(&a.pending[s]), 0xFFFFFFFFu) == 1u;
     if (ready) {
-      const uint32_t nc = __ldg(&a.items[s].nchunks);
+      const uint32_t nc = i == 0 ? m.s0nc : __ldg(&a.items[s].nchunks);
       if (nc == 1 && mailbox_put(mb, (unsigned long long)s << 32)) continue;   // run it here
       const unsigned long long pos = atomicAdd(&a.ctr->tail, (unsigned long long)nc);
       fence_acq_rel_gpu();   // one release fence covers the nc relaxed publications
@@ -568,7 +589,8 @@ __device__ void scal_bulk(float *x, uint64_t nv, const float *sf, uint32_t k, in
 
 template <int C, int S>
 __device__ __forceinline__ void compute_loop(const EpochArgs &a, const unsigned long long *s_unit,
-                                             float (*s_fac)[kMaxFactors], uint64_t *s_empty, int lane,
+                                             const DItem *s_item, float (*s_fac)[kMaxFactors], uint64_t *s_empty,
+                                             int lane,
                                              float *s_bulk = nullptr, uint64_t *s_bulk_bar = nullptr) {
   const int tid = threadIdx.x - (kBlock - C);
 #if BT_BULK
@@ -580,9 +602,8 @@ __device__ __forceinline__ void compute_loop(const EpochArgs &a, const unsigned 
     bar_sync(kBarFull + b, 32 + C);   // FULL[b]: the pop warp + the compute warps
     const unsigned long long unit = s_unit[b];
     if (unit == kStop) break;
-    const uint32_t item = (uint32_t)(unit >> 32);
     const uint32_t chunk = (uint32_t)unit;
-    const DItem it = a.items[item];
+    const DItem it = s_item[b];                  // staged by the pop warp
     const uint64_t lo = (uint64_t)chunk * a.chunk_elems;
     const uint64_t hi = min(it.n, lo + a.chunk_elems);
     switch (it.kind & K_MASK) {
@@ -649,12 +670,16 @@ __device__ __forceinline__ unsigned long long pop_ticket(const EpochArgs &a, uns
   return unit;
 }
 
-__device__ __forceinline__ void stage_factors(const EpochArgs &a, unsigned long long unit, float *dst, int lane) {
+// Stage a unit for the compute warps: its item descriptor (48 bytes, lanes
+// 0-2) and, for SCAL, its factor list into shared memory.
+__device__ __forceinline__ void stage_unit(const EpochArgs &a, unsigned long long unit, DItem *item_dst,
+                                           float *fac_dst, int lane) {
   if (unit == kStop) return;
-  const DItem &it = a.items[(uint32_t)(unit >> 32)];
-  if ((__ldg(&it.kind) & K_MASK) == K_SCAL) {
-    const uint32_t k = __ldg(&it.k), off = __ldg(&it.arg);
-    for (uint32_t j = lane; j < k; j += 32) dst[j] = __ldg(a.factors + off + j);
+  const DItem *it = a.items + (uint32_t)(unit >> 32);
+  if (lane < 3) reinterpret_cast<uint4 *>(item_dst)[lane] = __ldg(reinterpret_cast<const uint4 *>(it) + lane);
+  if ((__ldg(&it->kind) & K_MASK) == K_SCAL) {
+    const uint32_t k = __ldg(&it->k), off = __ldg(&it->arg);
+    for (uint32_t j = lane; j < k; j += 32) fac_dst[j] = __ldg(a.factors + off + j);
   }
 }
 
@@ -690,6 +715,7 @@ __device__ __forceinline__ void report_exit(const EpochArgs &a) {
 __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(EpochArgs a) {
   constexpr int kCompute = kComputeRW, kSlots = kSlotsRW;
   __shared__ unsigned long long s_unit[kSlots];
+  __shared__ DItem s_item[kSlots];
   __shared__ __align__(8) uint64_t s_empty[kSlots];
   __shared__ __align__(16) float s_fac[kSlots][kMaxFactors];
   __shared__ unsigned s_popped, s_released, s_mb_state;
@@ -775,7 +801,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
         }
       }
       unit = __shfl_sync(0xffffffffu, unit, 0);
-      stage_factors(a, unit, s_fac[b], lane);
+      stage_unit(a, unit, &s_item[b], s_fac[b], lane);
       if (lane == 0) s_unit[b] = unit;
       __syncwarp();
       if (lane == 0) st_release_cta_u32(&s_popped, u + 1);
@@ -787,6 +813,9 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
     for (unsigned u = 0;;) {
       while (ld_acquire_cta_u32(&s_popped) <= u) __nanosleep(32);
       if (s_unit[u % kSlots] == kStop) break;
+      // unit u's release metadata, loaded while it is being computed
+      RelMeta pre{};
+      if (lane == 0) pre = release_meta(a, (uint32_t)(s_unit[u % kSlots] >> 32));
       mbar_wait(&s_empty[u % kSlots], (u / kSlots) & 1u);
       // batch the following units that are already done
       unsigned m = 1;
@@ -805,7 +834,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
         const int b = (int)(v % kSlots);
         const unsigned long long unit = s_unit[b];
         const long long c1 = a.trace ? clock64() : 0;
-        release_unit(a, (uint32_t)(unit >> 32), Mailbox{&s_mb_unit, &s_mb_state});
+        release_unit(a, (uint32_t)(unit >> 32), Mailbox{&s_mb_unit, &s_mb_state}, lane == 0 ? &pre : nullptr);
         if (a.trace) {
           const unsigned long long t = s_ticket[b];
           a.trace[4 * t + 0] = s_g0[b];
@@ -820,7 +849,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
       if (lane == 0) st_release_cta_u32(&s_released, u);
     }
   } else {
-    compute_loop<kCompute, kSlots>(a, s_unit, s_fac, s_empty, lane);
+    compute_loop<kCompute, kSlots>(a, s_unit, s_item, s_fac, s_empty, lane);
   }
   report_exit(a);
 }
@@ -829,6 +858,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
 __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sw(EpochArgs a) {
   constexpr int kCompute = kComputeSW;
   __shared__ unsigned long long s_unit[2];
+  __shared__ DItem s_item[2];
   __shared__ __align__(8) uint64_t s_empty[2];
   __shared__ __align__(16) float s_fac[2][kMaxFactors];
 #if BT_BULK
@@ -905,7 +935,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sw(Epoch
         }
       }
       unit = __shfl_sync(0xffffffffu, unit, 0);
-      stage_factors(a, unit, s_fac[b], lane);
+      stage_unit(a, unit, &s_item[b], s_fac[b], lane);
       if (lane == 0) s_unit[b] = unit;
       __syncwarp();
       bar_arrive(kBarFull + b, 32 + kCompute);
@@ -916,9 +946,9 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sw(Epoch
     }
   } else {
 #if BT_BULK
-    compute_loop<kCompute, kSlotsSW>(a, s_unit, s_fac, s_empty, lane, &s_bulk[0][0][0], &s_bulk_bar[0][0]);
+    compute_loop<kCompute, kSlotsSW>(a, s_unit, s_item, s_fac, s_empty, lane, &s_bulk[0][0][0], &s_bulk_bar[0][0]);
 #else
-    compute_loop<kCompute, kSlotsSW>(a, s_unit, s_fac, s_empty, lane);
+    compute_loop<kCompute, kSlotsSW>(a, s_unit, s_item, s_fac, s_empty, lane);
 #endif
   }
   report_exit(a);
