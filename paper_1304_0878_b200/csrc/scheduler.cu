@@ -365,8 +365,7 @@ __device__ __forceinline__ RelMeta release_meta(const EpochArgs &a, uint32_t ite
   return m;
 }
 
-// Returns true if the first successor was handed to this CTA's mailbox.
-__device__ __forceinline__ bool release_unit(const EpochArgs &a, uint32_t item, const Mailbox &mb = Mailbox{},
+__device__ __forceinline__ void release_unit(const EpochArgs &a, uint32_t item, const Mailbox &mb = Mailbox{},
                                              const RelMeta *pre = nullptr) {
   const RelMeta m = pre ? *pre : release_meta(a, item);
   const uint32_t nchunks = m.nchunks, nsucc = m.nsucc, off = m.off;
@@ -374,10 +373,9 @@ __device__ __forceinline__ bool release_unit(const EpochArgs &a, uint32_t item, 
     const unsigned c = atom_add_acq_rel(&a.chunk_done[item], 1u);
     if (c + 1 != nchunks) {
       atomicAdd(&a.ctr->done, 1ull);
-      return false;
+      return;
     }
   }
-  bool cont0 = false;
   for (uint32_t i = 0; i < nsucc; ++i) {
     const uint32_t s = i == 0 ? m.s0 : __ldg(&a.succ[off + i]);
     const uint32_t skind = i == 0 ? m.s0kind : __ldg(&a.items[s].kind);
@@ -388,10 +386,7 @@ __device__ __forceinline__ bool release_unit(const EpochArgs &a, uint32_t item, 
                            : atom_add_acq_rel(reinterpret_cast<unsigned *>(&a.pending[s]), 0xFFFFFFFFu) == 1u;
     if (ready) {
       const uint32_t nc = i == 0 ? m.s0nc : __ldg(&a.items[s].nchunks);
-      if (nc == 1 && mailbox_put(mb, (unsigned long long)s << 32)) {   // run it here
-        cont0 |= (i == 0);
-        continue;
-      }
+      if (nc == 1 && mailbox_put(mb, (unsigned long long)s << 32)) continue;   // run it here
       const unsigned long long pos = atomicAdd(&a.ctr->tail, (unsigned long long)nc);
       fence_acq_rel_gpu();   // one release fence covers the nc relaxed publications
 #pragma unroll 1
@@ -399,7 +394,6 @@ __device__ __forceinline__ bool release_unit(const EpochArgs &a, uint32_t item, 
     }
   }
   atomicAdd(&a.ctr->done, 1ull);
-  return cont0;
 }
 
 // ---- mbarrier (compute warps -> scheduler warp: "unit done") -------------
@@ -726,11 +720,6 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
   __shared__ __align__(16) float s_fac[kSlots][kMaxFactors];
   __shared__ unsigned s_popped, s_released, s_mb_state;
   __shared__ unsigned long long s_mb_unit;
-  // the predicted continuation (first successor of the unit being released),
-  // staged by the release warp while that unit is still computing
-  __shared__ DItem s_nitem;
-  __shared__ __align__(16) float s_nfac[kMaxFactors];
-  __shared__ unsigned s_nstage;            // 0 free, else staged item + 1
   __shared__ unsigned long long s_ticket[kSlots], s_g0[kSlots];
   __shared__ long long s_popc[kSlots], s_c1[kSlots];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -739,7 +728,6 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
     s_popped = 0;
     s_released = 0;
     s_mb_state = 0;
-    s_nstage = 0;
   }
   __syncthreads();
 
@@ -813,19 +801,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
         }
       }
       unit = __shfl_sync(0xffffffffu, unit, 0);
-      const bool prestaged =
-          unit != kStop && *reinterpret_cast<volatile unsigned *>(&s_nstage) == (uint32_t)(unit >> 32) + 1u;
-      if (prestaged) {   // copy the release warp's staging (shared -> shared)
-        __threadfence_block();
-        if (lane < 3) reinterpret_cast<uint4 *>(&s_item[b])[lane] = reinterpret_cast<const uint4 *>(&s_nitem)[lane];
-        const uint32_t k = (s_nitem.kind & K_MASK) == K_SCAL ? s_nitem.k : 0u;
-        for (uint32_t j = lane; j < k; j += 32) s_fac[b][j] = s_nfac[j];
-        __syncwarp();
-        __threadfence_block();
-        if (lane == 0) *reinterpret_cast<volatile unsigned *>(&s_nstage) = 0u;
-      } else {
-        stage_unit(a, unit, &s_item[b], s_fac[b], lane);
-      }
+      stage_unit(a, unit, &s_item[b], s_fac[b], lane);
       if (lane == 0) s_unit[b] = unit;
       __syncwarp();
       if (lane == 0) st_release_cta_u32(&s_popped, u + 1);
@@ -839,20 +815,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
       if (s_unit[u % kSlots] == kStop) break;
       // unit u's release metadata, loaded while it is being computed
       RelMeta pre{};
-      unsigned cand = 0xFFFFFFFFu;
-      if (lane == 0) {
-        pre = release_meta(a, (uint32_t)(s_unit[u % kSlots] >> 32));
-        if (pre.nsucc && (pre.s0kind & K_SINGLE_PRED) && pre.s0nc == 1 &&
-            *reinterpret_cast<volatile unsigned *>(&s_nstage) == 0u)
-          cand = pre.s0;
-      }
-      cand = __shfl_sync(0xffffffffu, cand, 0);
-      if (cand != 0xFFFFFFFFu) {   // stage the likely continuation now (overlaps the compute)
-        stage_unit(a, (unsigned long long)cand << 32, &s_nitem, s_nfac, lane);
-        __syncwarp();
-        __threadfence_block();
-        if (lane == 0) *reinterpret_cast<volatile unsigned *>(&s_nstage) = cand + 1u;
-      }
+      if (lane == 0) pre = release_meta(a, (uint32_t)(s_unit[u % kSlots] >> 32));
       mbar_wait(&s_empty[u % kSlots], (u / kSlots) & 1u);
       // batch the following units that are already done
       unsigned m = 1;
@@ -871,12 +834,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
         const int b = (int)(v % kSlots);
         const unsigned long long unit = s_unit[b];
         const long long c1 = a.trace ? clock64() : 0;
-        const bool cont0 =
-            release_unit(a, (uint32_t)(unit >> 32), Mailbox{&s_mb_unit, &s_mb_state}, lane == 0 ? &pre : nullptr);
-        if (lane == 0 && cand != 0xFFFFFFFFu && !cont0) {   // staged in vain: free the staging
-          __threadfence_block();
-          atomicCAS(&s_nstage, cand + 1u, 0u);
-        }
+        release_unit(a, (uint32_t)(unit >> 32), Mailbox{&s_mb_unit, &s_mb_state}, lane == 0 ? &pre : nullptr);
         if (a.trace) {
           const unsigned long long t = s_ticket[b];
           a.trace[4 * t + 0] = s_g0[b];
