@@ -61,6 +61,11 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned *p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -761,8 +766,11 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
             have_ticket = true;
           }
           if (ticket < a.total_units) {
-            const unsigned long long v = ld_acquire_u64(&a.queue[ticket]);
+            // relaxed poll (an acquire load would hold back the mailbox
+            // checks behind its round trip); acquire once it is published
+            const unsigned long long v = ld_relaxed_u64(&a.queue[ticket]);
             if (v != Q_EMPTY) {
+              fence_acq_rel_gpu();
               unit = v;
               have_ticket = false;
               if ((unit >> 32) >= a.nitems) {
