@@ -767,10 +767,10 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
           }
           if (ticket < a.total_units) {
             // relaxed poll (an acquire load would hold back the mailbox
-            // checks behind its round trip); acquire once it is published
-            const unsigned long long v = ld_relaxed_u64(&a.queue[ticket]);
+            // checks behind its round trip); re-read with acquire once published
+            unsigned long long v = ld_relaxed_u64(&a.queue[ticket]);
             if (v != Q_EMPTY) {
-              fence_acq_rel_gpu();
+              v = ld_acquire_u64(&a.queue[ticket]);   // slots are written once: same value, now acquired
               unit = v;
               have_ticket = false;
               if ((unit >> 32) >= a.nitems) {
