@@ -212,6 +212,8 @@ def main():
     ap.add_argument("--chunk-bytes", type=int, default=0, help="fixed work-unit size (0 = adaptive)")
     ap.add_argument("--host-threads", type=int, default=0)
     ap.add_argument("--rounds", type=int, default=0, help="pipelined rounds per SCAL run (0 = library default)")
+    ap.add_argument("--emulate-ranks", type=int, default=0,
+                    help="diagnostic: run only rank 0's shard of an N-rank job (its line is not a bench result)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -252,7 +254,9 @@ def main():
     cfg = dict(C5, sweeps=args.sweeps)
     T, S = cfg["ntiles"], cfg["sweeps"]
     tile = cfg["nx"] // T
-    t_lo, t_hi = rank * T // world, (rank + 1) * T // world
+    # --emulate-ranks N (diagnostic, N=1 only): time rank 0's share of an N-rank run
+    shard_world = args.emulate_ranks if (args.emulate_ranks and world == 1) else world
+    t_lo, t_hi = rank * T // shard_world, (rank + 1) * T // shard_world
     my_tiles = t_hi - t_lo
     elems = my_tiles * tile
     factors = W.sweep_factors(np.random.default_rng(W.SEED_BASE + 4), S)
@@ -381,6 +385,12 @@ def main():
                     roof["traffic"] = tr["dram_bytes_per_launch"]
         except OSError:
             pass
+        if args.emulate_ranks and world == 1:
+            # rank 0's shard of an N-rank run: report its own time only (not a bench line)
+            print(json.dumps({"diagnostic": "emulated rank 0 of N", "N": args.emulate_ranks, "ms_per_step": ms,
+                              "host_build_ms_per_step": host_ms_max, "device_ms_per_step": span_ms_max,
+                              "elements": elems, "tasks_per_step": ntasks}), flush=True)
+            return 0
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",

@@ -50,7 +50,7 @@ constexpr uint32_t kDefaultPipelineMin = 131072;
 constexpr int kEpochRing = 12;                      // epoch buffers in flight (>= rounds + 2)
 constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;   // 20 s
 constexpr size_t kParallelPack = 4096;              // items above which the pack runs on the pool
-constexpr uint64_t kReleaseWarpBelow = 16384;       // work units smaller than this use the "rw" kernel
+constexpr uint64_t kReleaseWarpBelow = 65536;       // units with less work (elements x chain length) use "rw"
 constexpr uint64_t kUploadChunk = 64ull << 20;      // registrations >= this upload in chunks on a copy stream
 constexpr size_t kStageBelow = 1u << 20;            // epoch blobs up to this size are pulled by the set-up kernel
 constexpr uint64_t kDagChunkElems = 16384;          // work-unit cap (64 KiB) for epochs with dependencies
@@ -163,7 +163,6 @@ struct bt_runtime {
   int nrounds = 1;        // bucket rounds (max over round policies)
   int rounds_default = 1; // rounds of a partition of device-resident data
   EpochBuf ep[kEpochRing];
-  int ep_cur = 0;
   uint64_t ep_seq = 0;
   cudaStream_t rstream[2] = {nullptr, nullptr};   // round streams (pipelined SCAL runs)
   cudaEvent_t ev_fork = nullptr, ev_round[2] = {nullptr, nullptr};
@@ -405,8 +404,18 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   }
   if (!stream) stream = rt->stream;
   const double t0 = now_ms();
-  EpochBuf &e = rt->ep[rt->ep_cur];
-  rt->ep_cur = (rt->ep_cur + 1) % kEpochRing;
+  // buffer: the lowest-numbered one that is idle or finished (so a program
+  // touches -- and allocates -- only as many buffers as it keeps in flight),
+  // else the oldest in flight (retire waits for it)
+  EpochBuf *pick = nullptr, *oldest = nullptr;
+  for (EpochBuf &c : rt->ep) {
+    if (!c.inflight || cudaEventQuery(c.done) != cudaErrorNotReady) {
+      pick = &c;
+      break;
+    }
+    if (!oldest || c.seq < oldest->seq) oldest = &c;
+  }
+  EpochBuf &e = pick ? *pick : *oldest;
   if (int r = retire(rt, e)) return r;
 
   const size_t N = B.items.size();
@@ -416,8 +425,11 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
 
   // work-unit size from the epoch's total elements (sampled for huge epochs)
   const size_t stride = std::max<size_t>(1, N / 4096);
-  uint64_t sampled = 0, cnt = 0;
-  for (size_t i = 0; i < N; i += stride, ++cnt) sampled += B.items[i].n;
+  uint64_t sampled = 0, cnt = 0, sampled_work = 0;
+  for (size_t i = 0; i < N; i += stride, ++cnt) {
+    sampled += B.items[i].n;
+    sampled_work += B.items[i].n * std::max<uint32_t>(1, B.items[i].kind == K_SCAL ? B.items[i].k : 1);
+  }
   uint64_t CE = chunk_elems_for(rt, sampled / cnt * N);
   // a DAG's ready width can be far below the item count (C3: ~16 ready 4 MiB
   // tasks): smaller units keep all SMs busy (measured: 64 KiB units 14.6 ms
@@ -617,8 +629,10 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   // small work units are scheduling-bound: use the kernel with a dedicated
   // release warp; large ones are body-bound: keep all 8 warps computing
   static const char *kv = getenv("BT_KERNEL");   // "rw" / "sw": experiments only
-  const uint64_t avg_unit = (sampled / cnt * N) / std::max<uint64_t>(1, U);   // elements per work unit
-  const bool rw = kv ? (kv[0] == 'r') : avg_unit < kReleaseWarpBelow;
+  // work per unit = elements x chained multiplies: a 4 KiB unit of a 64-long
+  // chain is compute-bound (sw), a 4 KiB single scaling is scheduling-bound (rw)
+  const uint64_t avg_work = (sampled_work / cnt * N) / std::max<uint64_t>(1, U);
+  const bool rw = kv ? (kv[0] == 'r') : avg_work < kReleaseWarpBelow;
   CUDA_TRY(rt, launch_epoch(a, grid, stream, rw));
   CUDA_TRY(rt, cudaEventRecord(e.end, stream));
   // write-back of host-homed ranges written for the first time since registration
@@ -741,7 +755,7 @@ int bt_init(const bt_config *cfg_in, bt_runtime **out) {
   rt->npool = threads;
   rt->rounds_default = cfg.pipeline_rounds;
   rt->nrounds = std::max(cfg.pipeline_rounds, cfg.pipeline_rounds > 1 ? kRoundsUploading : 1);
-  rt->lanes.resize((size_t)threads * rt->nrounds);                  // [lane * R + round] when not pipelined
+  rt->lanes.resize((size_t)threads * rt->nrounds);                  // [(round - first round of the launch) * P + lane]
   rt->buckets.resize((size_t)threads * threads * rt->nrounds);      // [chunk][round * P + lane]
   rt->bucket_tasks.resize(rt->buckets.size());
 
@@ -1238,17 +1252,44 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
   // lane l owns slot blocks k with k % P == l (in every round); dense local
   // index over the lane's blocks: (k / P) * 64 + (s & 63)
   const uint32_t nlocal = (uint32_t)((((nslots + 63) >> 6) + P - 1) / P) * 64;
-  const int rounds = pipelined ? R : 1;
   std::vector<size_t> round_size(R, 0);
+  size_t local = 0;
   for (int c = 0; c < P; ++c)
     for (int r = 0; r < R; ++r)
       for (int l = 0; l < P; ++l) round_size[r] += rt->buckets[(size_t)c * G + (size_t)r * P + l].size();
-  for (int rr = 0; rr < rounds; ++rr) {
-    if (pipelined && round_size[rr] == 0) continue;   // rounds of another round policy
+  for (int r = 0; r < R; ++r) local += round_size[r];
+  // launches: adjacent rounds are merged so that each launch carries at least
+  // pipeline_min / 2 local tasks (a short run -- e.g. one rank's shard -- is
+  // launch-overhead bound with many small launches); [bound[j], bound[j+1])
+  // are the rounds of launch j.  Empty rounds belong to another round policy.
+  std::vector<int> bound{0};
+  if (pipelined) {
+    const size_t per = std::max<size_t>(1, rt->cfg.pipeline_min / 2);
+    int nonempty = 0;
+    for (int r = 0; r < R; ++r) nonempty += round_size[r] != 0;
+    const size_t want = std::max<size_t>(1, std::min<size_t>((size_t)nonempty, local / per));
+    size_t cum = 0;
+    size_t j = 0;
+    for (int r = 0; r < R; ++r) {
+      const size_t jr = local ? std::min(want - 1, cum * want / local) : 0;   // launch of round r
+      if (jr != j && round_size[r]) {
+        bound.push_back(r);
+        j = jr;
+      }
+      cum += round_size[r];
+    }
+  }
+  bound.push_back(R);
+  const int launches = (int)bound.size() - 1;
+  for (int rr = 0; rr < launches; ++rr) {
+    const int rlo = bound[rr], rhi = bound[rr + 1];
+    size_t sz = 0;
+    for (int r = rlo; r < rhi; ++r) sz += round_size[r];
+    if (pipelined && sz == 0) continue;
     const double ta = now_ms();
     rt->par([&](int l) {
-      // non-pipelined: this lane builds its groups of every round in one go
-      for (int r = pipelined ? rr : 0; r < (pipelined ? rr + 1 : R); ++r) {
+      // this lane builds its groups of every round of the launch in one go
+      for (int r = rlo; r < rhi; ++r) {
         const uint32_t g = (uint32_t)(r * P + l);
         std::vector<const LaneEntry *> ptrs(P);
         std::vector<const uint32_t *> tptr(P);
@@ -1258,7 +1299,7 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
           tptr[c] = record ? rt->bucket_tasks[(size_t)c * G + g].data() : nullptr;
           cnts[c] = rt->buckets[(size_t)c * G + g].size();
         }
-        Lane &L = rt->lanes[(size_t)l * (pipelined ? 1 : R) + (pipelined ? 0 : r)];
+        Lane &L = rt->lanes[(size_t)(r - rlo) * P + l];
         B.lane_runs(
             L, ptrs.data(), tptr.data(), cnts.data(), P, deps, nlocal,
             [up = (uint32_t)P](uint32_t s) { return ((s >> 6) / up) * 64 + (s & 63); },
@@ -1269,7 +1310,7 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
       }
     });
     const double tb = now_ms();
-    B.merge(rt->lanes, pipelined ? P : P * R, deps, [&](const std::function<void(int)> &f) { rt->pool->run(f); }, P);
+    B.merge(rt->lanes, P * (rhi - rlo), deps, [&](const std::function<void(int)> &f) { rt->pool->run(f); }, P);
     const double tc = now_ms();
     if (pipelined) {
       B.ntasks = tbase + n;   // the round's epoch accounts the run (its items carry the tasks)
@@ -1282,7 +1323,7 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
     t_flush += now_ms() - tc;
   }
   if (pipelined) {
-    for (int i = 0; i < std::min(R, 2); ++i) CUDA_TRY(rt, cudaStreamWaitEvent(rt->stream, rt->ev_round[i], 0));
+    for (int i = 0; i < std::min(launches, 2); ++i) CUDA_TRY(rt, cudaStreamWaitEvent(rt->stream, rt->ev_round[i], 0));
   } else {
     B.ntasks = tbase + n;
   }
