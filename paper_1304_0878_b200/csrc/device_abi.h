@@ -20,10 +20,12 @@ struct alignas(16) DItem {
   uint64_t n;         // elements of each operand
   uint32_t kind;      // K_* | K_SINGLE_PRED
   uint32_t k;         // SCAL: number of chained factors (>= 1); else 1
-  uint32_t arg;       // SCAL: offset of the k factors in EpochArgs::factors;
+  uint32_t arg;       // SCAL: k == 1: float bits of the factor; k > 1: offset of
+                      // the k factors in EpochArgs::factors;
                       // AXPY: float bits of a
   uint32_t nchunks;   // work units of this item = ceil(n / chunk_elems)
-  uint32_t succ_off;  // successors: succ[succ_off .. succ_off + nsucc)
+  uint32_t succ_off;  // successors: succ[succ_off .. succ_off + nsucc); with
+                      // nsucc == 1 the successor's item id itself
   uint32_t nsucc;
 };
 static_assert(sizeof(DItem) == 48, "DItem layout");

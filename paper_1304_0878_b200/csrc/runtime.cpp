@@ -466,7 +466,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
         a.ahi = std::max(a.ahi, it.y + bytes);
       }
       uint32_t reuse = 0;
-      if (it.kind == K_SCAL) {
+      if (it.kind == K_SCAL && it.k > 1) {   // k == 1: the factor travels inline (DItem::arg)
         if (prev && prev->k == it.k && memcmp(B.factors(*prev), B.factors(it), 4ull * it.k) == 0) reuse = 1;
         else a.fac += it.k;
         prev = &it;
@@ -537,7 +537,9 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
       d.n = it.n;
       d.kind = it.kind | (it.npred == 1 ? K_SINGLE_PRED : 0u);
       d.k = it.k;
-      if (it.kind == K_SCAL) {
+      if (it.kind == K_SCAL && it.k == 1) {
+        memcpy(&d.arg, B.factors(it), 4);
+      } else if (it.kind == K_SCAL) {
         if (!rt->cursor[i]) {
           memcpy(fac + fo, B.factors(it), 4ull * it.k);
           prev_fo = (uint32_t)fo;
@@ -561,7 +563,9 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   if (big) rt->par(passB);
   else passB(0);
   // CSR scatter (successor order within a list: edge creation order when
-  // sequential; any order is valid)
+  // sequential; any order is valid).  An item with a single successor holds
+  // the successor's id itself in DItem::succ_off (one dependent load less on
+  // the device's release path: chains).
   if (big) {
     uint32_t *cur = rt->succ_off.data();
     rt->par([&](int p) {
@@ -569,12 +573,21 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
       range_of(E, P, p, lo, hi);
       for (size_t j = lo; j < hi; ++j) {
         const uint64_t ed = B.edges[j];
-        const uint32_t pos = __atomic_fetch_add(&cur[ed >> 32], 1u, __ATOMIC_RELAXED);
+        const uint32_t src = (uint32_t)(ed >> 32);
+        if (di[src].nsucc == 1) {
+          di[src].succ_off = (uint32_t)ed;
+          continue;
+        }
+        const uint32_t pos = __atomic_fetch_add(&cur[src], 1u, __ATOMIC_RELAXED);
         succ[pos] = (uint32_t)ed;
       }
     });
   } else {
-    for (uint64_t ed : B.edges) succ[rt->succ_off[ed >> 32]++] = (uint32_t)ed;
+    for (uint64_t ed : B.edges) {
+      const uint32_t src = (uint32_t)(ed >> 32);
+      if (di[src].nsucc == 1) di[src].succ_off = (uint32_t)ed;
+      else succ[rt->succ_off[src]++] = (uint32_t)ed;
+    }
   }
 
   char *d = e.dblob;
@@ -1171,7 +1184,9 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
   const uint64_t tbase = B.ntasks;
   const bool record = B.record_tasks;
   double tp0 = now_ms();
+  std::vector<double> tstart(P), tend(P), tloop(P);
   rt->par([&](int c) {
+    if (dbg) tstart[c] = now_ms();
     size_t lo, hi;
     range_of(n, P, c, lo, hi);
     // this chunk's buckets, moved to the stack while filling (no false sharing
@@ -1198,6 +1213,7 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
       }
     } restore{mine, mine_t, rt, c, G};
     uint64_t rem = 0;
+    if (dbg) tloop[c] = now_ms();
     for (size_t j = lo; j < hi; ++j) {
       const bt_handle h = h0[i0 + j];
       const uint32_t s = (uint32_t)(h & 0xFFFFFFFFull) - 1u;   // handle index 0 wraps to UINT32_MAX
@@ -1228,7 +1244,20 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
       if (record) mine_t[sh.grp].push_back((uint32_t)(tbase + j));
     }
     remote[c] = rem;
+    if (dbg) tend[c] = now_ms();
   });
+  if (dbg) {
+    double s0 = 1e30, s1 = 0, l1 = 0, e1 = 0, lmax = 0;
+    for (int c = 0; c < P; ++c) {
+      s0 = std::min(s0, tstart[c]);
+      s1 = std::max(s1, tstart[c]);
+      l1 = std::max(l1, tloop[c]);
+      e1 = std::max(e1, tend[c]);
+      lmax = std::max(lmax, tend[c] - tloop[c]);
+    }
+    fprintf(stderr, "phase1: first start +%.3f, last start +%.3f, last loop start +%.3f, last end +%.3f, max loop %.3f ms\n",
+            s0 - tp0, s1 - tp0, l1 - tp0, e1 - tp0, lmax);
+  }
   for (int c = 0; c < P; ++c)
     if (bad[c]) {
       if (dbg) fprintf(stderr, "scal_run_parallel: chunk %d rejected, sequential replay\n", c);
@@ -1249,6 +1278,7 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
   DepState *deps = rt->deps.data();
   const double tp1 = now_ms();
   double t_p2 = 0, t_merge = 0, t_flush = 0;
+  std::vector<double> t_launch;
   // lane l owns slot blocks k with k % P == l (in every round); dense local
   // index over the lane's blocks: (k / P) * 64 + (s & 63)
   const uint32_t nlocal = (uint32_t)((((nslots + 63) >> 6) + P - 1) / P) * 64;
@@ -1317,6 +1347,7 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
       cudaStream_t st = rt->rstream[rr & 1];
       if (int e = flush_epoch(rt, st)) return e;
       CUDA_TRY(rt, cudaEventRecord(rt->ev_round[rr & 1], st));
+      if (dbg) t_launch.push_back(now_ms() - tp0);
     }
     t_p2 += tb - ta;
     t_merge += tc - tb;
@@ -1331,6 +1362,8 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
     fprintf(stderr,
             "scal_run_parallel n=%zu P=%d R=%d phase1 %.3f ms phase2 %.3f ms merge %.3f ms flush %.3f ms\n", n, P, R,
             tp1 - tp0, t_p2, t_merge, t_flush);
+  if (dbg)
+    for (size_t j = 0; j < t_launch.size(); ++j) fprintf(stderr, "  launch %zu issued at %.3f ms\n", j, t_launch[j]);
   return 0;
 }
 
@@ -1375,12 +1408,12 @@ int bt_insert_task_batch(bt_runtime *rt, size_t ntasks, const int32_t *codelets,
   int rc = 0;
   const size_t pmin = rt->cfg.parallel_min;
   // common case first: the whole batch is one long valid SCAL run
-  if (ntasks >= pmin && rt->pool->size() > 1 && scal_run_parallel(rt, codelets, scalars, h0, 0, ntasks) == 0) {
+  if (ntasks >= pmin && scal_run_parallel(rt, codelets, scalars, h0, 0, ntasks) == 0) {
     i = ntasks;
     if (rt->cfg.epoch_tasks && rt->builder.ntasks >= rt->cfg.epoch_tasks && !rt->host_only) rc = flush_epoch(rt);
   }
   while (i < ntasks && rc == 0) {
-    if (codelets[i] == BT_CL_SCAL && rt->pool->size() > 1) {
+    if (codelets[i] == BT_CL_SCAL) {
       size_t j = i;
       while (j < ntasks && codelets[j] == BT_CL_SCAL) ++j;
       if (j - i >= pmin && j - i < ntasks && scal_run_parallel(rt, codelets, scalars, h0, i, j) == 0) {

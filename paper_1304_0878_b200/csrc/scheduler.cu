@@ -123,6 +123,9 @@ __device__ __forceinline__ void st8(float *p, const float (&r)[8]) {
 template <int NV>
 __device__ __forceinline__ void chain_apply(float (&v)[NV][8], const float *sf, uint32_t k) {
   uint32_t j = 0;
+#ifndef BT_TRACE_DETAIL
+#define BT_TRACE_DETAIL 0
+#endif
 #ifndef BT_FACTOR_UNROLL16
 #define BT_FACTOR_UNROLL16 1
 #endif
@@ -336,14 +339,26 @@ __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_re
 // handed to this CTA's own pop warp instead of the global queue, so a chain
 // of dependent tasks stays on one SM (its tile stays in L2) and skips the
 // queue round trip.  state: 0 empty, 2 being written, 1 full.
+// The first successor's descriptor can travel with it (staged: the release
+// warp loaded it while the predecessor was computing), so the pop warp starts
+// the continuation without a global load.
 struct Mailbox {
   unsigned long long *unit;
   unsigned *state;
+  uint4 *item;        // 3 x 16 bytes: the staged DItem
+  unsigned *staged;   // 1: *item holds the unit's descriptor
 };
 
-__device__ __forceinline__ bool mailbox_put(const Mailbox &mb, unsigned long long unit) {
+__device__ __forceinline__ bool mailbox_put(const Mailbox &mb, unsigned long long unit, bool stage = false,
+                                            uint4 i0 = uint4{}, uint4 i1 = uint4{}, uint4 i2 = uint4{}) {
   if (!mb.unit || atomicCAS(mb.state, 0u, 2u) != 0u) return false;
   *reinterpret_cast<volatile unsigned long long *>(mb.unit) = unit;
+  if (stage) {
+    mb.item[0] = i0;
+    mb.item[1] = i1;
+    mb.item[2] = i2;
+  }
+  *reinterpret_cast<volatile unsigned *>(mb.staged) = stage ? 1u : 0u;
   __threadfence_block();
   *reinterpret_cast<volatile unsigned *>(mb.state) = 1u;
   return true;
@@ -354,18 +369,36 @@ __device__ __forceinline__ bool mailbox_put(const Mailbox &mb, unsigned long lon
 struct RelMeta {
   uint32_t nchunks, nsucc, off;
   uint32_t s0, s0kind, s0nc;   // first successor (valid if nsucc > 0)
+  uint4 i0, i1, i2;            // its descriptor (DItem as 3 x 16 bytes)
+  bool s0stage;                // a continuation candidate that needs no factor list
 };
-__device__ __forceinline__ RelMeta release_meta(const EpochArgs &a, uint32_t item) {
+// self: the item's descriptor already staged in shared memory, or null.
+__device__ __forceinline__ RelMeta release_meta(const EpochArgs &a, uint32_t item, const DItem *self = nullptr) {
   RelMeta m;
-  const DItem &it = a.items[item];
-  m.nchunks = __ldg(&it.nchunks);
-  m.nsucc = __ldg(&it.nsucc);
-  m.off = __ldg(&it.succ_off);
+  if (self) {
+    m.nchunks = self->nchunks;
+    m.nsucc = self->nsucc;
+    m.off = self->succ_off;
+  } else {
+    const DItem &it = a.items[item];
+    m.nchunks = __ldg(&it.nchunks);
+    m.nsucc = __ldg(&it.nsucc);
+    m.off = __ldg(&it.succ_off);
+  }
   m.s0 = m.s0kind = m.s0nc = 0;
+  m.s0stage = false;
+  m.i0 = m.i1 = m.i2 = uint4{};
   if (m.nsucc) {
-    m.s0 = __ldg(&a.succ[m.off]);
-    m.s0kind = __ldg(&a.items[m.s0].kind);
-    m.s0nc = __ldg(&a.items[m.s0].nchunks);
+    m.s0 = m.nsucc == 1 ? m.off : __ldg(&a.succ[m.off]);   // a single successor is stored inline
+    const uint4 *src = reinterpret_cast<const uint4 *>(a.items + m.s0);
+    m.i0 = __ldg(src);
+    m.i1 = __ldg(src + 1);   // n (x, y), kind (z), k (w)
+    m.i2 = __ldg(src + 2);   // arg (x), nchunks (y), succ_off (z), nsucc (w)
+    static_assert(offsetof(DItem, kind) == 24 && offsetof(DItem, k) == 28 && offsetof(DItem, nchunks) == 36,
+                  "DItem layout");
+    m.s0kind = m.i1.z;
+    m.s0nc = m.i2.y;
+    m.s0stage = (m.s0kind & K_SINGLE_PRED) && m.s0nc == 1 && ((m.s0kind & K_MASK) != K_SCAL || m.i1.w == 1);
   }
   return m;
 }
@@ -391,7 +424,8 @@ __device__ __forceinline__ void release_unit(const EpochArgs &a, uint32_t item, 
                            : atom_add_acq_rel(reinterpret_cast<unsigned *>(&a.pending[s]), 0xFFFFFFFFu) == 1u;
     if (ready) {
       const uint32_t nc = i == 0 ? m.s0nc : __ldg(&a.items[s].nchunks);
-      if (nc == 1 && mailbox_put(mb, (unsigned long long)s << 32)) continue;   // run it here
+      if (nc == 1 && mailbox_put(mb, (unsigned long long)s << 32, i == 0 && m.s0stage, m.i0, m.i1, m.i2))
+        continue;   // run it here
       const unsigned long long pos = atomicAdd(&a.ctr->tail, (unsigned long long)nc);
       fence_acq_rel_gpu();   // one release fence covers the nc relaxed publications
 #pragma unroll 1
@@ -596,7 +630,8 @@ template <int C, int S>
 __device__ __forceinline__ void compute_loop(const EpochArgs &a, const unsigned long long *s_unit,
                                              const DItem *s_item, float (*s_fac)[kMaxFactors], uint64_t *s_empty,
                                              int lane,
-                                             float *s_bulk = nullptr, uint64_t *s_bulk_bar = nullptr) {
+                                             float *s_bulk = nullptr, uint64_t *s_bulk_bar = nullptr,
+                                             long long *s_cst = nullptr, long long *s_cen = nullptr) {
   const int tid = threadIdx.x - (kBlock - C);
 #if BT_BULK
   const int cw = tid >> 5;
@@ -607,6 +642,9 @@ __device__ __forceinline__ void compute_loop(const EpochArgs &a, const unsigned 
     bar_sync(kBarFull + b, 32 + C);   // FULL[b]: the pop warp + the compute warps
     const unsigned long long unit = s_unit[b];
     if (unit == kStop) break;
+#if BT_TRACE_DETAIL
+    if (s_cst && tid == 0 && a.trace) s_cst[b] = clock64();
+#endif
     const uint32_t chunk = (uint32_t)unit;
     const DItem it = s_item[b];                  // staged by the pop warp
     const uint64_t lo = (uint64_t)chunk * a.chunk_elems;
@@ -644,6 +682,9 @@ __device__ __forceinline__ void compute_loop(const EpochArgs &a, const unsigned 
     // this warp's stores precede the arrive (mbarrier.arrive releases at CTA
     // scope; __syncwarp orders the other lanes' stores before lane 0's arrive)
     __syncwarp();
+#if BT_TRACE_DETAIL
+    if (s_cen && tid == 0 && a.trace) s_cen[b] = clock64();
+#endif
     if (lane == 0) mbar_arrive(&s_empty[b]);
   }
 }
@@ -683,8 +724,12 @@ __device__ __forceinline__ void stage_unit(const EpochArgs &a, unsigned long lon
   const DItem *it = a.items + (uint32_t)(unit >> 32);
   if (lane < 3) reinterpret_cast<uint4 *>(item_dst)[lane] = __ldg(reinterpret_cast<const uint4 *>(it) + lane);
   if ((__ldg(&it->kind) & K_MASK) == K_SCAL) {
-    const uint32_t k = __ldg(&it->k), off = __ldg(&it->arg);
-    for (uint32_t j = lane; j < k; j += 32) fac_dst[j] = __ldg(a.factors + off + j);
+    const uint32_t k = __ldg(&it->k), arg = __ldg(&it->arg);
+    if (k == 1) {   // a single factor travels inline in arg: no dependent load
+      if (lane == 0) fac_dst[0] = __uint_as_float(arg);
+    } else {
+      for (uint32_t j = lane; j < k; j += 32) fac_dst[j] = __ldg(a.factors + arg + j);
+    }
   }
 }
 
@@ -723,16 +768,21 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
   __shared__ DItem s_item[kSlots];
   __shared__ __align__(8) uint64_t s_empty[kSlots];
   __shared__ __align__(16) float s_fac[kSlots][kMaxFactors];
-  __shared__ unsigned s_popped, s_released, s_mb_state;
+  __shared__ unsigned s_popped, s_released, s_mb_state, s_mb_staged;
   __shared__ unsigned long long s_mb_unit;
+  __shared__ uint4 s_mb_item[3];
   __shared__ unsigned long long s_ticket[kSlots], s_g0[kSlots];
   __shared__ long long s_popc[kSlots], s_c1[kSlots];
+#if BT_TRACE_DETAIL
+  __shared__ long long s_cst[kSlots], s_cen[kSlots];
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int b = 0; b < kSlots; ++b) mbar_init(&s_empty[b], kCompute / 32);
     s_popped = 0;
     s_released = 0;
     s_mb_state = 0;
+    s_mb_staged = 0;
   }
   __syncthreads();
 
@@ -745,6 +795,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
       if (u >= kSlots)   // the slot's previous unit must be released
         while (ld_acquire_cta_u32(&s_released) + kSlots <= u) __nanosleep(32);
       unsigned long long unit = kStop;
+      unsigned staged = 0;
       if (lane == 0) {
         const uint64_t g0 = a.trace ? globaltimer() : 0;
         const long long c0 = a.trace ? clock64() : 0;
@@ -754,9 +805,20 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
         // of the epoch done.
         const uint64_t start = globaltimer();
         for (unsigned spin = 0;; ++spin) {
+          // the mailbox first, with no global load outstanding (the block
+          // fence below would wait for it: measured +0.35 us per chain link)
           if (*reinterpret_cast<volatile unsigned *>(&s_mb_state) == 1u) {
             __threadfence_block();
             unit = *reinterpret_cast<volatile unsigned long long *>(&s_mb_unit);
+            staged = *reinterpret_cast<volatile unsigned *>(&s_mb_staged);
+            if (staged) {   // copy the descriptor out before the mailbox is reused
+              const volatile uint4 *src = s_mb_item;
+              uint4 *dst = reinterpret_cast<uint4 *>(&s_item[b]);
+              for (int q = 0; q < 3; ++q) {
+                const uint4 w = {src[q].x, src[q].y, src[q].z, src[q].w};
+                dst[q] = w;
+              }
+            }
             __threadfence_block();
             *reinterpret_cast<volatile unsigned *>(&s_mb_state) = 0u;
             break;
@@ -765,7 +827,8 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
             ticket = atomicAdd(&a.ctr->head, 1ull);
             have_ticket = true;
           }
-          if (ticket < a.total_units) {
+          const bool poll = ticket < a.total_units;
+          if (poll) {
             // relaxed poll (an acquire load would hold back the mailbox
             // checks behind its round trip); re-read with acquire once published
             unsigned long long v = ld_relaxed_u64(&a.queue[ticket]);
@@ -779,13 +842,16 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
               }
               break;
             }
-          } else if (ld_acquire_cta_u32(&s_released) == u &&
-                     *reinterpret_cast<volatile unsigned *>(&s_mb_state) == 0u) {
+          }
+          // (the queue load above also paces this loop: a tight shared-memory
+          // spin slows the CTA's barriers -- measured: chain 2.0 vs 1.4 us)
+          const bool inflight = ld_acquire_cta_u32(&s_released) != u;   // a continuation may come
+          if (!poll && !inflight && *reinterpret_cast<volatile unsigned *>(&s_mb_state) == 0u) {
             unit = kStop;      // all our units released, no continuation pending
             break;
           }
-          if ((spin & 15) == 15) {
-            if (atomicAdd(&a.ctr->done, 0ull) == a.total_units) {
+          if ((spin & 63) == 63) {
+            if (ld_relaxed_u64(&a.ctr->done) == a.total_units) {
               unit = kStop;
               break;
             }
@@ -799,7 +865,9 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
               break;
             }
           }
-          __nanosleep(spin < 64 ? 32 : 256);
+          // back off only when nothing of ours is in flight (no continuation
+          // can arrive; a sleeping pop warp adds its sleep to every chain link)
+          if (!inflight) __nanosleep(spin < 64 ? 32 : 256);
         }
         if (a.trace) {
           s_ticket[b] = unit == kStop ? 0 : atomicAdd(&a.ctr->trace_next, 1ull);
@@ -809,7 +877,12 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
         }
       }
       unit = __shfl_sync(0xffffffffu, unit, 0);
-      stage_unit(a, unit, &s_item[b], s_fac[b], lane);
+      staged = __shfl_sync(0xffffffffu, staged, 0);
+      if (!staged) {
+        stage_unit(a, unit, &s_item[b], s_fac[b], lane);
+      } else if (lane == 0 && (s_item[b].kind & K_MASK) == K_SCAL) {
+        s_fac[b][0] = __uint_as_float(s_item[b].arg);   // staged SCAL continuations have k == 1
+      }
       if (lane == 0) s_unit[b] = unit;
       __syncwarp();
       if (lane == 0) st_release_cta_u32(&s_popped, u + 1);
@@ -819,11 +892,14 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
   } else if (warp == 1) {
     // ================= release warp =================
     for (unsigned u = 0;;) {
-      while (ld_acquire_cta_u32(&s_popped) <= u) __nanosleep(32);
+      // the pop warp publishes within a few hundred cycles once it has a
+      // unit: spin (a sleeping release warp delays the critical path of chains)
+      for (unsigned spin = 0; ld_acquire_cta_u32(&s_popped) <= u; ++spin)
+        if (spin >= 4096) __nanosleep(64);
       if (s_unit[u % kSlots] == kStop) break;
       // unit u's release metadata, loaded while it is being computed
       RelMeta pre{};
-      if (lane == 0) pre = release_meta(a, (uint32_t)(s_unit[u % kSlots] >> 32));
+      if (lane == 0) pre = release_meta(a, (uint32_t)(s_unit[u % kSlots] >> 32), &s_item[u % kSlots]);
       mbar_wait(&s_empty[u % kSlots], (u / kSlots) & 1u);
       // batch the following units that are already done
       unsigned m = 1;
@@ -842,13 +918,21 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
         const int b = (int)(v % kSlots);
         const unsigned long long unit = s_unit[b];
         const long long c1 = a.trace ? clock64() : 0;
-        release_unit(a, (uint32_t)(unit >> 32), Mailbox{&s_mb_unit, &s_mb_state}, lane == 0 ? &pre : nullptr);
+        release_unit(a, (uint32_t)(unit >> 32), Mailbox{&s_mb_unit, &s_mb_state, s_mb_item, &s_mb_staged},
+                     lane == 0 ? &pre : nullptr);
         if (a.trace) {
           const unsigned long long t = s_ticket[b];
           a.trace[4 * t + 0] = s_g0[b];
+#if BT_TRACE_DETAIL
+          // detail: [1] handoff pop -> compute start, [2] compute, [3] compute end -> release start
+          a.trace[4 * t + 1] = (unsigned long long)(s_cst[b] - s_c1[b]);
+          a.trace[4 * t + 2] = (unsigned long long)(s_cen[b] - s_cst[b]);
+          a.trace[4 * t + 3] = (unsigned long long)(c1 - s_cen[b]);
+#else
           a.trace[4 * t + 1] = (unsigned long long)s_popc[b];
           a.trace[4 * t + 2] = (unsigned long long)(c1 - s_c1[b]);
           a.trace[4 * t + 3] = (unsigned long long)(clock64() - c1);
+#endif
           a.trace_item[t] = (uint32_t)(unit >> 32);
         }
       }
@@ -857,7 +941,11 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
       if (lane == 0) st_release_cta_u32(&s_released, u);
     }
   } else {
+#if BT_TRACE_DETAIL
+    compute_loop<kCompute, kSlots>(a, s_unit, s_item, s_fac, s_empty, lane, nullptr, nullptr, s_cst, s_cen);
+#else
     compute_loop<kCompute, kSlots>(a, s_unit, s_item, s_fac, s_empty, lane);
+#endif
   }
   report_exit(a);
 }

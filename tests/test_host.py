@@ -118,7 +118,7 @@ def check_dag(program, snap):
 
 
 @pytest.mark.parametrize("fusion", [True, False])
-@pytest.mark.parametrize("threads,pmin", [(1, 0), (4, 1), (3, 2)])
+@pytest.mark.parametrize("threads,pmin", [(1, 0), (1, 1), (4, 1), (3, 2)])
 def test_builder_matches_conflict_relation_random(B, fusion, threads, pmin):
     """Sequential builder (1 thread) and the parallel SCAL-run lanes (forced on
     every run of >= pmin SCALs) both enforce exactly the conflict relation."""

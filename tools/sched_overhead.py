@@ -88,8 +88,8 @@ def main():
     run_case("C4 unfused (1M tasks, 4 KiB tiles, 64 sweeps)", 15625, 1024, 64, B.BT_FLAG_NO_FUSION)
     run_case("C4 unfused, timestamps", 15625, 1024, 64, B.BT_FLAG_NO_FUSION, reps=2, trace=True)
     run_case("C4 fused", 15625, 1024, 64, 0)
-    run_case("chain of 10,000 on one 4 KiB tile (dependency latency)", 1, 1024, 10000, B.BT_FLAG_NO_FUSION, reps=3,
-             trace=True)
+    run_case("chain of 10,000 on one 4 KiB tile (dependency latency)", 1, 1024, 10000, B.BT_FLAG_NO_FUSION, reps=3)
+    run_case("chain of 10,000, timestamps", 1, 1024, 10000, B.BT_FLAG_NO_FUSION, reps=3, trace=True)
     run_case("C4b: 1M independent 4 KiB tiles x 1 task (pop rate)", 1 << 20, 1024, 1, 0)
     run_case("C4b, timestamps", 1 << 20, 1024, 1, 0, reps=2, trace=True)
 
