@@ -347,6 +347,7 @@ struct Mailbox {
   unsigned *state;
   uint4 *item;        // 3 x 16 bytes: the staged DItem
   unsigned *staged;   // 1: *item holds the unit's descriptor
+  uint64_t *bar;      // mbarrier (count 1): one phase per put, wakes a pop warp in try_wait
 };
 
 __device__ __forceinline__ bool mailbox_put(const Mailbox &mb, unsigned long long unit, bool stage = false,
@@ -361,6 +362,10 @@ __device__ __forceinline__ bool mailbox_put(const Mailbox &mb, unsigned long lon
   *reinterpret_cast<volatile unsigned *>(mb.staged) = stage ? 1u : 0u;
   __threadfence_block();
   *reinterpret_cast<volatile unsigned *>(mb.state) = 1u;
+  if (mb.bar)
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(mb.bar))
+                 : "memory");
   return true;
 }
 
@@ -468,6 +473,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
         : "r"(addr), "r"(parity)
         : "memory");
   }
+}
+
+// Suspend until the phase with this parity completes or about hint_ns pass.
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t *bar, unsigned parity, unsigned hint_ns) {
+  unsigned ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(parity), "r"(hint_ns)
+      : "memory");
+  return ok != 0;
 }
 
 // Scheduler-warp state (lane 0): the unit held in each slot and whether it
@@ -768,10 +784,11 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
   __shared__ DItem s_item[kSlots];
   __shared__ __align__(8) uint64_t s_empty[kSlots];
   __shared__ __align__(16) float s_fac[kSlots][kMaxFactors];
-  __shared__ unsigned s_popped, s_released, s_mb_state, s_mb_staged;
+  __shared__ unsigned s_popped, s_released, s_mb_state, s_mb_staged, s_mb_expect;
+  __shared__ __align__(8) uint64_t s_mb_bar;
   __shared__ unsigned long long s_mb_unit;
   __shared__ uint4 s_mb_item[3];
-  __shared__ unsigned long long s_ticket[kSlots], s_g0[kSlots];
+  __shared__ unsigned long long s_g0[kSlots];
   __shared__ long long s_popc[kSlots], s_c1[kSlots];
 #if BT_TRACE_DETAIL
   __shared__ long long s_cst[kSlots], s_cen[kSlots];
@@ -783,6 +800,8 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
     s_released = 0;
     s_mb_state = 0;
     s_mb_staged = 0;
+    s_mb_expect = 0;
+    mbar_init(&s_mb_bar, 1);
   }
   __syncthreads();
 
@@ -790,6 +809,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
     // ================= pop warp =================
     unsigned long long ticket = 0;
     bool have_ticket = false;
+    unsigned mb_taken = 0;   // mailbox entries taken (= phases of s_mb_bar consumed)
     for (unsigned u = 0;; ++u) {
       const int b = (int)(u % kSlots);
       if (u >= kSlots)   // the slot's previous unit must be released
@@ -821,6 +841,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
             }
             __threadfence_block();
             *reinterpret_cast<volatile unsigned *>(&s_mb_state) = 0u;
+            ++mb_taken;
             break;
           }
           if (!have_ticket) {
@@ -865,12 +886,15 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
               break;
             }
           }
-          // back off only when nothing of ours is in flight (no continuation
-          // can arrive; a sleeping pop warp adds its sleep to every chain link)
-          if (!inflight) __nanosleep(spin < 64 ? 32 : 256);
+          // a continuation is on its way (the release warp said so) and the
+          // queue had nothing: sleep on the mailbox barrier, woken by the put;
+          // with nothing of ours in flight back off; otherwise keep polling
+          if (inflight && *reinterpret_cast<volatile unsigned *>(&s_mb_expect))
+            mbar_try_wait_hint(&s_mb_bar, mb_taken & 1u, 1000u);
+          else if (!inflight)
+            __nanosleep(spin < 64 ? 32 : 256);
         }
         if (a.trace) {
-          s_ticket[b] = unit == kStop ? 0 : atomicAdd(&a.ctr->trace_next, 1ull);
           s_g0[b] = g0;
           s_c1[b] = clock64();
           s_popc[b] = s_c1[b] - c0;
@@ -899,7 +923,12 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
       if (s_unit[u % kSlots] == kStop) break;
       // unit u's release metadata, loaded while it is being computed
       RelMeta pre{};
-      if (lane == 0) pre = release_meta(a, (uint32_t)(s_unit[u % kSlots] >> 32), &s_item[u % kSlots]);
+      if (lane == 0) {
+        pre = release_meta(a, (uint32_t)(s_unit[u % kSlots] >> 32), &s_item[u % kSlots]);
+        // this unit's release will hand a continuation to the pop warp
+        const bool cont = pre.nchunks == 1 && pre.nsucc > 0 && (pre.s0kind & K_SINGLE_PRED) && pre.s0nc == 1;
+        *reinterpret_cast<volatile unsigned *>(&s_mb_expect) = cont ? 1u : 0u;
+      }
       mbar_wait(&s_empty[u % kSlots], (u / kSlots) & 1u);
       // batch the following units that are already done
       unsigned m = 1;
@@ -918,10 +947,12 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
         const int b = (int)(v % kSlots);
         const unsigned long long unit = s_unit[b];
         const long long c1 = a.trace ? clock64() : 0;
-        release_unit(a, (uint32_t)(unit >> 32), Mailbox{&s_mb_unit, &s_mb_state, s_mb_item, &s_mb_staged},
+        release_unit(a, (uint32_t)(unit >> 32), Mailbox{&s_mb_unit, &s_mb_state, s_mb_item, &s_mb_staged, &s_mb_bar},
                      lane == 0 ? &pre : nullptr);
         if (a.trace) {
-          const unsigned long long t = s_ticket[b];
+          // the record index is taken here, after the release (a global
+          // atomic on the pop path would lengthen every dependency link)
+          const unsigned long long t = atomicAdd(&a.ctr->trace_next, 1ull);
           a.trace[4 * t + 0] = s_g0[b];
 #if BT_TRACE_DETAIL
           // detail: [1] handoff pop -> compute start, [2] compute, [3] compute end -> release start
@@ -938,7 +969,10 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
       }
       __syncwarp();
       u += m;
-      if (lane == 0) st_release_cta_u32(&s_released, u);
+      if (lane == 0) {
+        *reinterpret_cast<volatile unsigned *>(&s_mb_expect) = 0u;
+        st_release_cta_u32(&s_released, u);
+      }
     }
   } else {
 #if BT_TRACE_DETAIL
