@@ -55,6 +55,7 @@ constexpr int kMaxFactors = 1024;              // upper bound of bt_config.max_f
 constexpr unsigned long long kStop = ~0ull - 1;
 // named barrier ids (0 is __syncthreads): FULL[slot] = 1 + slot
 constexpr int kBarFull = 1;
+constexpr int kBarCompute = 5;   // the rw kernel's compute warps only (in-slot continuation)
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
   unsigned long long v;
@@ -705,6 +706,101 @@ __device__ __forceinline__ void compute_loop(const EpochArgs &a, const unsigned 
   }
 }
 
+#ifndef BT_INSLOT
+#define BT_INSLOT 1
+#endif
+
+// Compute warps of the "rw" kernel.  As the generic loop, plus in-slot
+// continuation: when a finished unit's only successor has it as its only
+// predecessor and is a single unit needing no factor list, the compute warps
+// run that successor next in the same slot, without a release, a queue or a
+// mailbox round trip (its readiness follows from this unit's completion, and
+// a barrier of the compute warps orders this unit's stores before the
+// successor's loads).  Such chains -- C4's per-tile task chains, 1-wide
+// dependency chains -- then cost one compute-warp barrier per link; the slot
+// is released once, at the chain's last unit (s_final), and the skipped
+// releases are counted into ctr->done.  Off when tracing (one record per unit).
+template <int C, int S>
+__device__ __forceinline__ void compute_loop_rw(const EpochArgs &a, const unsigned long long *s_unit,
+                                                const DItem *s_item, float (*s_fac)[kMaxFactors], uint64_t *s_empty,
+                                                DItem (*s_nitem)[2], float (*s_nfac)[2], unsigned (*s_go)[2],
+                                                unsigned long long *s_final, int lane, long long *s_cst = nullptr,
+                                                long long *s_cen = nullptr) {
+  const int tid = threadIdx.x - (kBlock - C);
+  for (unsigned u = 0;; ++u) {
+    const int b = (int)(u % S);
+    bar_sync(kBarFull + b, 32 + C);   // FULL[b]: the pop warp + the compute warps
+    unsigned long long unit = s_unit[b];
+    if (unit == kStop) break;
+#if BT_TRACE_DETAIL
+    if (s_cst && tid == 0 && a.trace) s_cst[b] = clock64();
+#endif
+    DItem it = s_item[b];                        // staged by the pop warp
+    const float *fac = s_fac[b];
+    unsigned par = 0, extra = 0;
+    for (;;) {
+      // may this unit continue in the slot?  (uniform: every thread sees it)
+      const bool maybe = BT_INSLOT && !a.trace && it.nchunks == 1 && it.nsucc == 1;
+      if (maybe && tid == 0) {   // the successor's descriptor, copied to shared memory under the body
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(&s_nitem[b][par]);
+        const DItem *src = a.items + it.succ_off;
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * q), "l"(reinterpret_cast<const char *>(src) + 16 * q)
+                       : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
+      const uint32_t chunk = (uint32_t)unit;
+      const uint64_t lo = (uint64_t)chunk * a.chunk_elems;
+      const uint64_t hi = min(it.n, lo + a.chunk_elems);
+      switch (it.kind & K_MASK) {
+        case K_SCAL:   // small units (the rw kernel's domain): 2 x 8 elements per thread and step
+          scal_range<2, C>(reinterpret_cast<float *>(it.x) + lo, hi - lo, fac, it.k, tid);
+          break;
+        case K_AXPY:
+          axpy_range<C>(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, hi - lo,
+                        __uint_as_float(it.arg), tid);
+          break;
+        case K_COPY:
+          copy_range<C>(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, hi - lo,
+                        tid);
+          break;
+        default:
+          if (tid == 0) raise_error(a, ERR_BAD_KIND);
+          break;
+      }
+      if (!maybe) break;
+      if (tid == 0) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        const DItem &n = s_nitem[b][par];
+        const unsigned go = (n.kind & K_SINGLE_PRED) && n.nchunks == 1 && ((n.kind & K_MASK) != K_SCAL || n.k == 1)
+                                ? 1u : 0u;
+        if (go) s_nfac[b][par] = __uint_as_float(n.arg);   // a single factor travels in arg
+        s_go[b][par] = go;
+      }
+      // all compute warps: this unit's stores are done (and visible in the CTA)
+      // and the decision is published; buffers alternate so a slow warp can
+      // still read this step's while thread 0 fills the next
+      bar_sync_n<kBarCompute>(C);
+      if (!s_go[b][par]) break;
+      unit = (unsigned long long)it.succ_off << 32;   // nsucc == 1: succ_off is the successor's id
+      it = s_nitem[b][par];
+      fac = &s_nfac[b][par];
+      par ^= 1u;
+      ++extra;
+    }
+    if (tid == 0) {
+      s_final[b] = unit;                                   // the unit the release warp releases
+      if (extra) atomicAdd(&a.ctr->done, (unsigned long long)extra);   // the chain's skipped releases
+    }
+    __syncwarp();
+#if BT_TRACE_DETAIL
+    if (s_cen && tid == 0 && a.trace) s_cen[b] = clock64();
+#endif
+    if (lane == 0) mbar_arrive(&s_empty[b]);
+  }
+}
+
 // Pop the unit at a fresh ticket (lane 0), spinning until it is published.
 __device__ __forceinline__ unsigned long long pop_ticket(const EpochArgs &a, unsigned long long &t) {
   t = atomicAdd(&a.ctr->head, 1ull);
@@ -784,6 +880,10 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
   __shared__ DItem s_item[kSlots];
   __shared__ __align__(8) uint64_t s_empty[kSlots];
   __shared__ __align__(16) float s_fac[kSlots][kMaxFactors];
+  __shared__ DItem s_nitem[kSlots][2];              // in-slot continuation (compute warps)
+  __shared__ float s_nfac[kSlots][2];
+  __shared__ unsigned s_go[kSlots][2];
+  __shared__ unsigned long long s_final[kSlots];    // last unit run in the slot
   __shared__ unsigned s_popped, s_released, s_mb_state, s_mb_staged, s_mb_expect;
   __shared__ __align__(8) uint64_t s_mb_bar;
   __shared__ unsigned long long s_mb_unit;
@@ -925,9 +1025,11 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
       RelMeta pre{};
       if (lane == 0) {
         pre = release_meta(a, (uint32_t)(s_unit[u % kSlots] >> 32), &s_item[u % kSlots]);
-        // this unit's release will hand a continuation to the pop warp
+        // this unit's release will hand a continuation to the pop warp (one
+        // the compute warps run in the slot does not come through the mailbox)
         const bool cont = pre.nchunks == 1 && pre.nsucc > 0 && (pre.s0kind & K_SINGLE_PRED) && pre.s0nc == 1;
-        *reinterpret_cast<volatile unsigned *>(&s_mb_expect) = cont ? 1u : 0u;
+        const bool inslot = BT_INSLOT && !a.trace && pre.nchunks == 1 && pre.nsucc == 1 && pre.s0stage;
+        *reinterpret_cast<volatile unsigned *>(&s_mb_expect) = cont && !inslot ? 1u : 0u;
       }
       mbar_wait(&s_empty[u % kSlots], (u / kSlots) & 1u);
       // batch the following units that are already done
@@ -945,10 +1047,10 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
       if (lane < (int)m) {
         const unsigned v = u + lane;
         const int b = (int)(v % kSlots);
-        const unsigned long long unit = s_unit[b];
+        const unsigned long long unit = s_final[b];   // the popped unit, or the end of an in-slot chain
         const long long c1 = a.trace ? clock64() : 0;
         release_unit(a, (uint32_t)(unit >> 32), Mailbox{&s_mb_unit, &s_mb_state, s_mb_item, &s_mb_staged, &s_mb_bar},
-                     lane == 0 ? &pre : nullptr);
+                     lane == 0 && unit == s_unit[b] ? &pre : nullptr);
         if (a.trace) {
           // the record index is taken here, after the release (a global
           // atomic on the pop path would lengthen every dependency link)
@@ -976,9 +1078,10 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
     }
   } else {
 #if BT_TRACE_DETAIL
-    compute_loop<kCompute, kSlots>(a, s_unit, s_item, s_fac, s_empty, lane, nullptr, nullptr, s_cst, s_cen);
+    compute_loop_rw<kCompute, kSlots>(a, s_unit, s_item, s_fac, s_empty, s_nitem, s_nfac, s_go, s_final, lane, s_cst,
+                                      s_cen);
 #else
-    compute_loop<kCompute, kSlots>(a, s_unit, s_item, s_fac, s_empty, lane);
+    compute_loop_rw<kCompute, kSlots>(a, s_unit, s_item, s_fac, s_empty, s_nitem, s_nfac, s_go, s_final, lane);
 #endif
   }
   report_exit(a);
