@@ -79,7 +79,13 @@ enum {
   BT_FLAG_NO_FUSION  = 1u << 0, /* never fuse consecutive SCAL(RW) tasks of one (sub)handle */
   BT_FLAG_HOST_ONLY  = 1u << 1, /* no GPU: analyse only (bt_dag_snapshot); nothing executes */
   BT_FLAG_TIMESTAMPS = 1u << 2, /* record %globaltimer per work unit (bt_trace) */
-  BT_FLAG_SYNC_EPOCH = 1u << 3  /* debugging: synchronise after every epoch launch */
+  BT_FLAG_SYNC_EPOCH = 1u << 3, /* debugging: synchronise after every epoch launch */
+  /* testing: force one scheduler variant for every epoch instead of the
+   * per-epoch choice (DESIGN.md section "Persistent scheduler kernels"); at
+   * most one of the three may be set (-EINVAL otherwise) */
+  BT_FLAG_KERNEL_SW  = 1u << 8,  /* CTA-wide units, one scheduler warp */
+  BT_FLAG_KERNEL_RW  = 1u << 9,  /* CTA-wide units, pop + release warps, in-slot chains */
+  BT_FLAG_KERNEL_WQ  = 1u << 10  /* one warp per unit */
 };
 
 typedef struct bt_config {

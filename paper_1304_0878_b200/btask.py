@@ -22,6 +22,7 @@ BT_ABI_VERSION = 1
 BT_R, BT_W, BT_RW = 1, 2, 3
 BT_CL_SCAL, BT_CL_AXPY, BT_CL_COPY = 1, 2, 3
 BT_FLAG_NO_FUSION, BT_FLAG_HOST_ONLY, BT_FLAG_TIMESTAMPS, BT_FLAG_SYNC_EPOCH = 1, 2, 4, 8
+BT_FLAG_KERNEL_SW, BT_FLAG_KERNEL_RW, BT_FLAG_KERNEL_WQ = 1 << 8, 1 << 9, 1 << 10
 
 bt_handle = ctypes.c_uint64
 

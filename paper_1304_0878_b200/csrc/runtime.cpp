@@ -28,8 +28,9 @@
 #include "pool.hpp"
 
 namespace bt {
-cudaError_t launch_epoch(const EpochArgs &args, int grid, cudaStream_t stream, bool release_warp);
+cudaError_t launch_epoch(const EpochArgs &args, int grid, cudaStream_t stream, int kernel);
 cudaError_t scheduler_occupancy(int *blocks_per_sm, int *block);
+cudaError_t scheduler_occupancy_wq(int *blocks_per_sm, int *block);
 cudaError_t launch_stage(void *dst, const void *src_mapped, size_t bytes, unsigned long long *q_empty, size_t nq,
                          uint32_t *zero, size_t nz, cudaStream_t stream);
 int max_factors();
@@ -51,6 +52,7 @@ constexpr int kEpochRing = 12;                      // epoch buffers in flight (
 constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;   // 20 s
 constexpr size_t kParallelPack = 4096;              // items above which the pack runs on the pool
 constexpr uint64_t kReleaseWarpBelow = 65536;       // units with less work (elements x chain length) use "rw"
+constexpr uint64_t kWarpUnitMax = 4096;             // units of at most this many elements use "wq"
 constexpr uint64_t kUploadChunk = 64ull << 20;      // registrations >= this upload in chunks on a copy stream
 constexpr size_t kStageBelow = 1u << 20;            // epoch blobs up to this size are pulled by the set-up kernel
 constexpr uint64_t kDagChunkElems = 16384;          // work-unit cap (64 KiB) for epochs with dependencies
@@ -143,6 +145,7 @@ struct bt_runtime {
   int sms = 0;
   int grid_max = 0;
   int block = 0;
+  int grid_wq = 0, block_wq = 0;   // the warp-worker kernel
   int poisoned = 0;
   std::string last_error;
 
@@ -645,8 +648,21 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   // work per unit = elements x chained multiplies: a 4 KiB unit of a 64-long
   // chain is compute-bound (sw), a 4 KiB single scaling is scheduling-bound (rw)
   const uint64_t avg_work = (sampled_work / cnt * N) / std::max<uint64_t>(1, U);
-  const bool rw = kv ? (kv[0] == 'r') : avg_work < kReleaseWarpBelow;
-  CUDA_TRY(rt, launch_epoch(a, grid, stream, rw));
+  // units of at most 16 KiB: one warp per unit ("wq", many units in flight)
+  const uint64_t avg_elems = (sampled / cnt * N) / std::max<uint64_t>(1, U);
+  // ... when the epoch is wide: a narrow one (few initially ready units, e.g.
+  // a 1-wide dependency chain) is latency-bound, and the CTA-wide "rw" kernel
+  // runs chains in its slots with the shortest dependency latency
+  const bool wide = U0 * 4 >= (uint64_t)rt->grid_wq * 8;
+  int kernel = avg_elems <= kWarpUnitMax && rt->grid_wq > 0 && wide ? 2 : avg_work < kReleaseWarpBelow ? 1 : 0;
+  if (kv) kernel = kv[0] == 'w' ? 2 : kv[0] == 'r' ? 1 : 0;
+  if (rt->cfg.flags & BT_FLAG_KERNEL_SW) kernel = 0;
+  if (rt->cfg.flags & BT_FLAG_KERNEL_RW) kernel = 1;
+  if ((rt->cfg.flags & BT_FLAG_KERNEL_WQ) && rt->grid_wq > 0) kernel = 2;
+  const int kgrid = kernel == 2 ? (int)std::min<uint64_t>((uint64_t)rt->grid_wq, (U + 7) / 8) : grid;
+  rt->stats.grid = (uint32_t)kgrid;
+  rt->stats.block = kernel == 2 ? (uint32_t)rt->block_wq : (uint32_t)rt->block;
+  CUDA_TRY(rt, launch_epoch(a, kgrid, stream, kernel));
   CUDA_TRY(rt, cudaEventRecord(e.end, stream));
   // write-back of host-homed ranges written for the first time since registration
   bool wb_waited = false;
@@ -683,7 +699,6 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   rt->stats.epochs += 1;
   rt->stats.upload_bytes += upload;
   rt->stats.fused_tasks += B.fused;
-  rt->stats.grid = (uint32_t)grid;
   B.next_epoch();
   rt->stats.host_build_ms += now_ms() - t0;
   if (rt->cfg.flags & BT_FLAG_SYNC_EPOCH) return retire(rt, e);
@@ -748,6 +763,7 @@ int bt_init(const bt_config *cfg_in, bt_runtime **out) {
   if (cfg.parallel_min == 0) cfg.parallel_min = kDefaultParallelMin;
   if (cfg.pipeline_rounds == 0) cfg.pipeline_rounds = kDefaultRounds;
   if (cfg.pipeline_rounds < 1 || cfg.pipeline_rounds > kEpochRing - 2) return -EINVAL;
+  if (__builtin_popcount(cfg.flags & (BT_FLAG_KERNEL_SW | BT_FLAG_KERNEL_RW | BT_FLAG_KERNEL_WQ)) > 1) return -EINVAL;
   if (cfg.pipeline_min == 0) cfg.pipeline_min = kDefaultPipelineMin;
 
   bt_runtime *rt = new (std::nothrow) bt_runtime();
@@ -804,6 +820,14 @@ int bt_init(const bt_config *cfg_in, bt_runtime **out) {
     rt->grid_max = occ * rt->sms;
     rt->block = block;
     rt->stats.block = (uint32_t)block;
+    int occ_wq = 0, block_wq = 0;
+    if (scheduler_occupancy_wq(&occ_wq, &block_wq) != cudaSuccess || occ_wq < 1) {
+      cudaGetLastError();
+      occ_wq = 0;
+    }
+    if (cfg.ctas_per_sm > 0) occ_wq = std::min(occ_wq, cfg.ctas_per_sm);
+    rt->grid_wq = occ_wq * rt->sms;
+    rt->block_wq = block_wq;
     if (cfg.stream) {
       rt->stream = (cudaStream_t)cfg.stream;
     } else {

@@ -1217,11 +1217,213 @@ cudaError_t launch_stage(void *dst, const void *src_mapped, size_t bytes, unsign
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// "wq": every warp is an independent worker (pop, body, release), for epochs of
+// small units (<= 16 KiB): a CTA-wide unit of 4 KiB leaves most threads idle
+// and keeps one unit's bytes in flight per CTA; eight warps per CTA each with
+// its own unit keep eight (Little's law: the HBM / L2 latency is hidden by
+// units in flight, not by threads per unit).  A warp whose release makes a
+// single-unit successor ready runs it next itself (no queue round trip); the
+// queue ticket for the next pop is taken while the body runs.
+#ifndef BT_WQ_MIN_CTAS
+#define BT_WQ_MIN_CTAS 4
+#endif
+#ifndef BT_WQ_U
+#define BT_WQ_U 2   // 8-float vectors per lane in flight per step
+#endif
+constexpr int kBlockWQ = 256, kWarpsWQ = kBlockWQ / 32;
+#ifndef BT_TICKET_BLOCK
+#define BT_TICKET_BLOCK 4
+#endif
+constexpr unsigned kTicketBlock = BT_TICKET_BLOCK;   // queue positions per RMW on ctr->head
+constexpr unsigned kDoneBatch = 16;                  // completions per RMW on ctr->done
+
+// Release of one finished unit by its warp's lane 0; returns a ready
+// single-unit successor for this warp to run next, or kStop.
+// s0kind / s0nc: the single successor's kind and nchunks when prefetched
+// (nsucc == 1), else ignored.  The unit's completion is counted by the caller.
+__device__ __forceinline__ unsigned long long release_wq(const EpochArgs &a, uint32_t item, const DItem &it,
+                                                         uint32_t s0kind, uint32_t s0nc, bool pre) {
+  if (it.nchunks > 1) {
+    const unsigned c = atom_add_acq_rel(&a.chunk_done[item], 1u);
+    if (c + 1 != it.nchunks) return kStop;
+  }
+  unsigned long long cont = kStop;
+  for (uint32_t i = 0; i < it.nsucc; ++i) {
+    const uint32_t s = it.nsucc == 1 ? it.succ_off : __ldg(&a.succ[it.succ_off + i]);   // single successor inline
+    const uint32_t skind = pre ? s0kind : __ldg(&a.items[s].kind);
+    // a single-predecessor successor is ready now; with more predecessors
+    // the acq_rel RMW both releases ours and acquires theirs
+    const bool ready = (skind & K_SINGLE_PRED)
+                           ? true
+                           : atom_add_acq_rel(reinterpret_cast<unsigned *>(&a.pending[s]), 0xFFFFFFFFu) == 1u;
+    if (!ready) continue;
+    const uint32_t nc = pre ? s0nc : __ldg(&a.items[s].nchunks);
+    if (cont == kStop && nc == 1) {   // run it here next
+      cont = (unsigned long long)s << 32;
+      continue;
+    }
+    const unsigned long long pos = atomicAdd(&a.ctr->tail, (unsigned long long)nc);
+    fence_acq_rel_gpu();   // one release fence covers the nc relaxed publications
+#pragma unroll 1
+    for (uint32_t c = 0; c < nc; ++c) st_relaxed_u64(&a.queue[pos + c], ((unsigned long long)s << 32) | c);
+  }
+  return cont;
+}
+
+__global__ void __launch_bounds__(kBlockWQ, BT_WQ_MIN_CTAS) scheduler_kernel_wq(EpochArgs a) {
+  __shared__ DItem s_wi[kWarpsWQ];
+  __shared__ __align__(16) float s_wf[kWarpsWQ][kMaxFactors];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  DItem *my = &s_wi[w];
+  float *fac = s_wf[w];
+  unsigned long long ticket = 0;      // lane 0: the queue position this warp pops next
+  unsigned tickets = 0;               // lane 0: positions left in its block [ticket, ticket + tickets)
+  unsigned ndone = 0;                 // lane 0: units completed, not yet added to ctr->done
+  bool grow = false, chained = true;  // lane 0: last popped unit continued / not (ticket block size;
+                                      // the first pop takes one position: chains may follow)
+  unsigned long long cont = kStop;    // uniform: a local continuation
+  bool cont_staged = false;           // uniform: its descriptor is already in *my
+  const uint64_t start = globaltimer();
+  for (;;) {
+    uint64_t g0 = 0;
+    long long c0 = 0, c1 = 0, c2 = 0;
+    if (a.trace) {
+      g0 = globaltimer();
+      c0 = clock64();
+    }
+    unsigned long long unit = cont;
+    if (unit == kStop && lane == 0) {
+      grow = !chained;
+      chained = false;
+      for (unsigned spin = 0;; ++spin) {
+        if (!tickets) {
+          // queue positions are taken kTicketBlock at a time (one RMW on head
+          // per block) after a unit that did not continue; one at a time after
+          // one that started a chain (a held block would serialise chains)
+          const unsigned nb = grow ? kTicketBlock : 1u;
+          ticket = atomicAdd(&a.ctr->head, (unsigned long long)nb);
+          tickets = nb;
+        }
+        if (ticket >= a.total_units) break;   // no queue work left for this warp
+        unsigned long long v = ld_relaxed_u64(&a.queue[ticket]);
+        if (v != Q_EMPTY) {
+          v = ld_acquire_u64(&a.queue[ticket]);   // slots are written once: same value, now acquired
+          ++ticket;
+          --tickets;
+          if ((v >> 32) >= a.nitems) {
+            raise_error(a, ERR_BAD_UNIT);
+            break;
+          }
+          unit = v;
+          break;
+        }
+        if (ndone) {   // about to wait: account our finished units first (termination reads the sum)
+          atomicAdd(&a.ctr->done, (unsigned long long)ndone);
+          ndone = 0;
+        }
+        if ((spin & 15) == 15) {
+          // every unit done (the rest ran as continuations): no publication will come
+          if (ld_relaxed_u64(&a.ctr->done) == a.total_units) break;
+          if (ld_relaxed_u32(&a.ctr->abort)) break;
+          if (globaltimer() - start > a.watchdog_ns) {
+            raise_error(a, ERR_WATCHDOG);
+            break;
+          }
+        }
+        __nanosleep(spin < 32 ? 64 : 256);
+      }
+      if (unit == kStop && ndone) {
+        atomicAdd(&a.ctr->done, (unsigned long long)ndone);
+        ndone = 0;
+      }
+    }
+    unit = __shfl_sync(0xffffffffu, unit, 0);
+    if (unit == kStop) break;
+    cont = kStop;
+    // stage the descriptor (lanes 0-2, 16 bytes each; a continuation's was
+    // prefetched) and the factor list
+    const uint32_t item = (uint32_t)(unit >> 32);
+    if (!cont_staged && lane < 3)
+      reinterpret_cast<uint4 *>(my)[lane] = __ldg(reinterpret_cast<const uint4 *>(a.items + item) + lane);
+    __syncwarp();
+    const DItem it = *my;
+    // prefetch the single successor's descriptor under the body (lanes 0-2)
+    const bool pre = it.nsucc == 1 && it.nchunks == 1;
+    uint4 nd = {};
+    if (pre && lane < 3) nd = __ldg(reinterpret_cast<const uint4 *>(a.items + it.succ_off) + lane);
+    if ((it.kind & K_MASK) == K_SCAL) {
+      if (it.k == 1) {
+        if (lane == 0) fac[0] = __uint_as_float(it.arg);   // a single factor travels inline
+      } else {
+        for (uint32_t j = lane; j < it.k; j += 32) fac[j] = __ldg(a.factors + it.arg + j);
+      }
+      __syncwarp();
+    }
+    if (a.trace) c1 = clock64();
+    const uint32_t chunk = (uint32_t)unit;
+    const uint64_t lo = (uint64_t)chunk * a.chunk_elems;
+    const uint64_t hi = min(it.n, lo + a.chunk_elems);
+    switch (it.kind & K_MASK) {
+      case K_SCAL:
+        scal_range<BT_WQ_U, 32>(reinterpret_cast<float *>(it.x) + lo, hi - lo, fac, it.k, lane);
+        break;
+      case K_AXPY:
+        axpy_range<32>(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, hi - lo,
+                       __uint_as_float(it.arg), lane);
+        break;
+      case K_COPY:
+        copy_range<32>(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, hi - lo,
+                       lane);
+        break;
+      default:
+        if (lane == 0) raise_error(a, ERR_BAD_KIND);
+        break;
+    }
+    // the warp's stores precede lane 0's release (__syncwarp orders memory
+    // among the warp's lanes; lane 0's acq_rel operations are cumulative)
+    __syncwarp();
+    if (a.trace) c2 = clock64();
+    const uint32_t s0kind = __shfl_sync(0xffffffffu, nd.z, 1);   // word 1: n (x, y), kind (z), k (w)
+    const uint32_t s0nc = __shfl_sync(0xffffffffu, nd.y, 2);     // word 2: arg (x), nchunks (y)
+    if (lane == 0) {
+      cont = release_wq(a, item, it, s0kind, s0nc, pre);
+      chained |= cont != kStop;
+      if (++ndone == kDoneBatch) {
+        atomicAdd(&a.ctr->done, (unsigned long long)ndone);
+        ndone = 0;
+      }
+    }
+    cont = __shfl_sync(0xffffffffu, cont, 0);
+    // the continuation is the prefetched successor: its descriptor is ready
+    cont_staged = pre && cont != kStop;
+    if (a.trace && lane == 0) {
+      const unsigned long long t = atomicAdd(&a.ctr->trace_next, 1ull);
+      a.trace[4 * t + 0] = g0;
+      a.trace[4 * t + 1] = (unsigned long long)(c1 - c0);
+      a.trace[4 * t + 2] = (unsigned long long)(c2 - c1);
+      a.trace[4 * t + 3] = (unsigned long long)(clock64() - c2);
+      a.trace_item[t] = item;
+    }
+    // the next unit's descriptor overwrites this one's: every lane has read it
+    __syncwarp();
+    if (cont_staged && lane < 3) reinterpret_cast<uint4 *>(my)[lane] = nd;
+  }
+  report_exit(a);
+}
+
 // Host-side launcher (called from runtime.cpp).
-cudaError_t launch_epoch(const EpochArgs &args, int grid, cudaStream_t stream, bool release_warp) {
-  if (release_warp) scheduler_kernel_rw<<<grid, kBlock, 0, stream>>>(args);
+// kernel: 0 = sw, 1 = rw, 2 = wq (grid in CTAs of that kernel's block size).
+cudaError_t launch_epoch(const EpochArgs &args, int grid, cudaStream_t stream, int kernel) {
+  if (kernel == 2) scheduler_kernel_wq<<<grid, kBlockWQ, 0, stream>>>(args);
+  else if (kernel == 1) scheduler_kernel_rw<<<grid, kBlock, 0, stream>>>(args);
   else scheduler_kernel_sw<<<grid, kBlock, 0, stream>>>(args);
   return cudaGetLastError();
+}
+
+cudaError_t scheduler_occupancy_wq(int *blocks_per_sm, int *block) {
+  *block = kBlockWQ;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, scheduler_kernel_wq, kBlockWQ, 0);
 }
 
 cudaError_t scheduler_occupancy(int *blocks_per_sm, int *block) {

@@ -72,12 +72,38 @@ def test_subnormal_inputs_not_flushed(B):
         assert {f"{int(v):08X}" for v in out[0].view(np.uint32)} == {outbits}
 
 
+KERNELS = {"auto": 0, "sw": 1 << 8, "rw": 1 << 9, "wq": 1 << 10}   # BT_FLAG_KERNEL_*
+
+
+@pytest.mark.parametrize("kernel", ["sw", "rw", "wq"])
+@pytest.mark.parametrize("fusion", [True, False])
+@pytest.mark.parametrize("chunk_bytes", [0, 96, 4096])
+def test_random_programs_per_kernel(B, kernel, fusion, chunk_bytes):
+    """Each scheduler variant, forced for every epoch, is bit-exact on random
+    SCAL/AXPY/COPY programs (DAGs with ragged tiles, multi-chunk items, chains)."""
+    flags = (0 if fusion else B.BT_FLAG_NO_FUSION) | KERNELS[kernel]
+    for seed in range(1000, 1040):
+        p = W.random_small_program(seed, max_tasks=10)
+        compare_program(p, flags=flags, chunk_bytes=chunk_bytes)
+
+
+@pytest.mark.parametrize("kernel", ["sw", "rw", "wq"])
+def test_chains_per_kernel(B, kernel):
+    """Unfused dependency chains (in-slot / in-warp continuations) and wide
+    independent units, per scheduler variant, against the oracle."""
+    for order in ("sweep", "tile"):
+        p = W.c4_fine(ntiles=300, tile_nx=1024, sweeps=12, order=order)
+        compare_program(p, flags=B.BT_FLAG_NO_FUSION | KERNELS[kernel])
+    p = W.c4_fine(ntiles=1, tile_nx=1000, sweeps=300)   # one 1-wide chain, ragged vector tail
+    compare_program(p, flags=B.BT_FLAG_NO_FUSION | KERNELS[kernel])
+
+
 @pytest.mark.parametrize("fusion", [True, False])
 @pytest.mark.parametrize("chunk_bytes", [0, 32, 96, 65536])
 def test_random_programs(B, fusion, chunk_bytes):
     """>= 200 random programs, byte-identical to submission order.
-    Work units below 64 KiB run on the release-warp kernel ("rw"), larger ones
-    (chunk_bytes=65536) on the single-scheduler-warp kernel ("sw")."""
+    The kernel is the runtime's per-epoch choice (test_random_programs_per_kernel
+    forces each variant)."""
     flags = 0 if fusion else B.BT_FLAG_NO_FUSION
     for seed in range(70):
         p = W.random_small_program(seed, max_tasks=10)

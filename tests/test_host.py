@@ -60,6 +60,18 @@ def test_init_without_gpu_is_enodev_unless_host_only(B):
     assert B.bt_shutdown(h) == 0
 
 
+def test_init_rejects_two_forced_kernels(B):
+    """BT_FLAG_KERNEL_* (testing): at most one scheduler variant may be forced."""
+    cfg = B.bt_config()
+    B.bt_config_init(ctypes.byref(cfg))
+    h = ctypes.c_void_p()
+    cfg.flags = B.BT_FLAG_HOST_ONLY | B.BT_FLAG_KERNEL_SW | B.BT_FLAG_KERNEL_WQ
+    assert B.bt_init(ctypes.byref(cfg), ctypes.byref(h)) == -errno.EINVAL
+    cfg.flags = B.BT_FLAG_HOST_ONLY | B.BT_FLAG_KERNEL_WQ
+    assert B.bt_init(ctypes.byref(cfg), ctypes.byref(h)) == 0
+    assert B.bt_shutdown(h) == 0
+
+
 def host_rt(B, **kw):
     return B.Runtime(flags=B.BT_FLAG_HOST_ONLY | kw.pop("flags", 0), **kw)
 
