@@ -83,15 +83,28 @@ def run_case(name, ntiles, tile, sweeps, flags, reps=5, trace=False):
     return out
 
 
+CASES = [
+    ("C4 unfused (1M tasks, 4 KiB tiles, 64 sweeps)", 15625, 1024, 64, B.BT_FLAG_NO_FUSION, 5, False),
+    ("C4 unfused, timestamps", 15625, 1024, 64, B.BT_FLAG_NO_FUSION, 2, True),
+    ("C4 fused", 15625, 1024, 64, 0, 5, False),
+    ("chain of 10,000 on one 4 KiB tile (dependency latency)", 1, 1024, 10000, B.BT_FLAG_NO_FUSION, 3, False),
+    ("chain of 10,000, timestamps", 1, 1024, 10000, B.BT_FLAG_NO_FUSION, 3, True),
+    ("C4b: 1M independent 4 KiB tiles x 1 task (pop rate)", 1 << 20, 1024, 1, 0, 5, False),
+    ("C4b, timestamps", 1 << 20, 1024, 1, 0, 2, True),
+]
+
+
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", default="", help="run only cases whose name starts with this (e.g. for ncu)")
+    ap.add_argument("--reps", type=int, default=0, help="override the repetitions")
+    args = ap.parse_args()
     torch.cuda.set_device(0)
-    run_case("C4 unfused (1M tasks, 4 KiB tiles, 64 sweeps)", 15625, 1024, 64, B.BT_FLAG_NO_FUSION)
-    run_case("C4 unfused, timestamps", 15625, 1024, 64, B.BT_FLAG_NO_FUSION, reps=2, trace=True)
-    run_case("C4 fused", 15625, 1024, 64, 0)
-    run_case("chain of 10,000 on one 4 KiB tile (dependency latency)", 1, 1024, 10000, B.BT_FLAG_NO_FUSION, reps=3)
-    run_case("chain of 10,000, timestamps", 1, 1024, 10000, B.BT_FLAG_NO_FUSION, reps=3, trace=True)
-    run_case("C4b: 1M independent 4 KiB tiles x 1 task (pop rate)", 1 << 20, 1024, 1, 0)
-    run_case("C4b, timestamps", 1 << 20, 1024, 1, 0, reps=2, trace=True)
+    for name, ntiles, tile, sweeps, flags, reps, trace in CASES:
+        if args.case and not name.startswith(args.case):
+            continue
+        run_case(name, ntiles, tile, sweeps, flags, reps=args.reps or reps, trace=trace)
 
 
 if __name__ == "__main__":
