@@ -402,7 +402,7 @@ def main():
             "config": {"workload": workload_name(cfg), "tasks_per_step": ntasks * world, "builder_threads": threads,
                        "fusion": fused, "parallelism": f"owner-computes tiles over {world} rank(s)",
                        "l2": "4 GiB working set > 126 MB L2 (no flush needed)"},
-            "gpu_launches": int(st["epochs"]),
+            "gpu_launches": int(st["kernel_launches"]),
             "clocks": clocks,
             "roofline": roof,
         }

@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define BT_ABI_VERSION 1
+#define BT_ABI_VERSION 2   /* 2: bt_stats.kernel_launches, BT_FLAG_KERNEL_* */
 
 typedef struct bt_runtime bt_runtime;
 typedef uint64_t bt_handle;
@@ -242,8 +242,9 @@ typedef struct bt_stats {
   double device_ms;           /* summed persistent-kernel time of completed epochs */
   double device_span_ms;      /* summed device time from the first launch after a wait to the end
                                  of that wait's work (overlapping launches counted once) */
-  uint32_t grid;              /* persistent CTAs per launch */
-  uint32_t block;             /* threads per CTA */
+  uint32_t grid;              /* persistent CTAs of the last launch */
+  uint32_t block;             /* threads per CTA of the last launch */
+  uint64_t kernel_launches;   /* this library's kernel launches (per epoch: set-up + scheduler) */
 } bt_stats;
 int bt_stats_get(bt_runtime *rt, bt_stats *out);
 int bt_stats_reset(bt_runtime *rt);

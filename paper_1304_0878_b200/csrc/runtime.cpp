@@ -608,6 +608,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   for (auto &kv2 : rt->caches) uploads_pending |= !kv2.second.uploads.empty();
   const bool sm_copy = uploads_pending || upload <= kStageBelow;
   if (!sm_copy) CUDA_TRY(rt, cudaMemcpyAsync(d, h, upload, cudaMemcpyHostToDevice, stream));
+  rt->stats.kernel_launches += 2;   // the set-up kernel below and the scheduler kernel
   CUDA_TRY(rt, launch_stage(d, sm_copy ? e.hblob_dev : nullptr, upload,
                             reinterpret_cast<unsigned long long *>(d + o_queue) + U0, U - U0,
                             reinterpret_cast<uint32_t *>(d + o_cdone), N, stream));

@@ -259,10 +259,12 @@ def test_empty_wait_and_tiny(B):
     assert x[0] == np.float32(1.5) * np.float32(3.14)
 
 
-def test_trace_timestamps(B):
+@pytest.mark.parametrize("kernel", ["auto", "sw", "rw", "wq"])
+def test_trace_timestamps(B, kernel):
+    """One trace record per unit (continuations are off while tracing)."""
     p = W.c4_fine(ntiles=500, sweeps=8)
     from paper_1304_0878_b200.programs import Session
-    with B.Runtime(flags=B.BT_FLAG_TIMESTAMPS | B.BT_FLAG_NO_FUSION) as rt:
+    with B.Runtime(flags=B.BT_FLAG_TIMESTAMPS | B.BT_FLAG_NO_FUSION | KERNELS[kernel]) as rt:
         s = Session(rt, p)
         s.submit()
         rt.wait()
