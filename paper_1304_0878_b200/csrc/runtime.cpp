@@ -53,6 +53,7 @@ constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;   // 20 s
 constexpr size_t kParallelPack = 4096;              // items above which the pack runs on the pool
 constexpr uint64_t kReleaseWarpBelow = 65536;       // units with less work (elements x chain length) use "rw"
 constexpr uint64_t kWarpUnitMax = 4096;             // units of at most this many elements use "wq"
+constexpr uint64_t kPrefetchBelowK = 32;            // "sw" epochs with shorter average chains prefetch
 constexpr uint64_t kUploadChunk = 64ull << 20;      // registrations >= this upload in chunks on a copy stream
 constexpr size_t kStageBelow = 1u << 20;            // epoch blobs up to this size are pulled by the set-up kernel
 constexpr uint64_t kDagChunkElems = 16384;          // work-unit cap (64 KiB) for epochs with dependencies
@@ -656,8 +657,11 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   // runs chains in its slots with the shortest dependency latency
   const bool wide = U0 * 4 >= (uint64_t)rt->grid_wq * 8;
   int kernel = avg_elems <= kWarpUnitMax && rt->grid_wq > 0 && wide ? 2 : avg_work < kReleaseWarpBelow ? 1 : 0;
+  // sw: epochs of short chains (average k below the FP32/HBM ridge) are
+  // HBM-bound and use the instance whose bodies prefetch the next step's data
+  if (kernel == 0 && avg_work < kPrefetchBelowK * avg_elems) kernel = 3;
   if (kv) kernel = kv[0] == 'w' ? 2 : kv[0] == 'r' ? 1 : 0;
-  if (rt->cfg.flags & BT_FLAG_KERNEL_SW) kernel = 0;
+  if (rt->cfg.flags & BT_FLAG_KERNEL_SW) kernel = avg_work < kPrefetchBelowK * avg_elems ? 3 : 0;
   if (rt->cfg.flags & BT_FLAG_KERNEL_RW) kernel = 1;
   if ((rt->cfg.flags & BT_FLAG_KERNEL_WQ) && rt->grid_wq > 0) kernel = 2;
   const int kgrid = kernel == 2 ? (int)std::min<uint64_t>((uint64_t)rt->grid_wq, (U + 7) / 8) : grid;

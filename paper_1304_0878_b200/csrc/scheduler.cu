@@ -233,6 +233,56 @@ __device__ void scal_range(float *x, uint64_t n, const float *sf, uint32_t k, in
   for (uint64_t t = head + 8 * nv + tid; t < n; t += C) __stcg(x + t, chain_scalar(__ldcg(x + t), sf, k));
 }
 
+// Software-pipelined variant: the next step's U vectors are loaded before the
+// current step's multiplies, so a warp never waits for a load at a step start
+// (two register sets, A and B, alternate; U = 2 keeps them within the budget).
+template <int U, int C>
+__device__ void scal_range_pf(float *x, uint64_t n, const float *sf, uint32_t k, int tid) {
+  const uint64_t head = head_elems(x, n);
+  for (uint64_t i = tid; i < head; i += C) __stcg(x + i, chain_scalar(__ldcg(x + i), sf, k));
+  float *xv = x + head;
+  const uint64_t nv = (n - head) >> 3;
+  uint64_t i = tid;
+  if (i + (U - 1) * C < nv) {
+    float a[U][8], b[U][8];
+#pragma unroll
+    for (int q = 0; q < U; ++q) ld8(xv + 8 * (i + q * C), a[q]);
+    for (;;) {
+      // A holds step i; prefetch step i + U*C into B
+      uint64_t j = i + U * C;
+      bool more = j + (U - 1) * C < nv;
+      if (more) {
+#pragma unroll
+        for (int q = 0; q < U; ++q) ld8(xv + 8 * (j + q * C), b[q]);
+      }
+      chain_apply<U>(a, sf, k);
+#pragma unroll
+      for (int q = 0; q < U; ++q) st8(xv + 8 * (i + q * C), a[q]);
+      i = j;
+      if (!more) break;
+      // B holds step i; prefetch into A
+      j = i + U * C;
+      more = j + (U - 1) * C < nv;
+      if (more) {
+#pragma unroll
+        for (int q = 0; q < U; ++q) ld8(xv + 8 * (j + q * C), a[q]);
+      }
+      chain_apply<U>(b, sf, k);
+#pragma unroll
+      for (int q = 0; q < U; ++q) st8(xv + 8 * (i + q * C), b[q]);
+      i = j;
+      if (!more) break;
+    }
+  }
+  for (; i < nv; i += C) {
+    float v[1][8];
+    ld8(xv + 8 * i, v[0]);
+    chain_apply<1>(v, sf, k);
+    st8(xv + 8 * i, v[0]);
+  }
+  for (uint64_t t = head + 8 * nv + tid; t < n; t += C) __stcg(x + t, chain_scalar(__ldcg(x + t), sf, k));
+}
+
 // AXPY: y[i] = fl(fl(a*x[i]) + y[i]) (two roundings, no FFMA).
 __device__ __forceinline__ float axpy1(float a, float x, float y) { return __fadd_rn(__fmul_rn(a, x), y); }
 
@@ -643,7 +693,7 @@ __device__ void scal_bulk(float *x, uint64_t nv, const float *sf, uint32_t k, in
 }
 #endif
 
-template <int C, int S>
+template <int C, int S, bool PF = false>
 __device__ __forceinline__ void compute_loop(const EpochArgs &a, const unsigned long long *s_unit,
                                              const DItem *s_item, float (*s_fac)[kMaxFactors], uint64_t *s_empty,
                                              int lane,
@@ -682,7 +732,14 @@ __device__ __forceinline__ void compute_loop(const EpochArgs &a, const unsigned 
           break;
         }
 #endif
-        scal_range<4, C>(reinterpret_cast<float *>(it.x) + lo, hi - lo, s_fac[b], it.k, tid);
+        // short chains are HBM-bound: keep the next step's loads in flight
+        // (C5-16 kernel 6.41 vs 6.33 TB/s); long ones are FP32-bound: the
+        // wider step without prefetch is faster (C5 2.07 vs 2.08 ms).  One
+        // body per kernel instance (both inlined would spill).
+        if (PF)
+          scal_range_pf<2, C>(reinterpret_cast<float *>(it.x) + lo, hi - lo, s_fac[b], it.k, tid);
+        else
+          scal_range<4, C>(reinterpret_cast<float *>(it.x) + lo, hi - lo, s_fac[b], it.k, tid);
         break;
       case K_AXPY:
         axpy_range<C>(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, hi - lo,
@@ -1088,6 +1145,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
 }
 
 // "sw": one scheduler warp pops and releases, 8 compute warps, 2 slots.
+template <bool PF>
 __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sw(EpochArgs a) {
   constexpr int kCompute = kComputeSW;
   __shared__ unsigned long long s_unit[2];
@@ -1179,9 +1237,9 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sw(Epoch
     }
   } else {
 #if BT_BULK
-    compute_loop<kCompute, kSlotsSW>(a, s_unit, s_item, s_fac, s_empty, lane, &s_bulk[0][0][0], &s_bulk_bar[0][0]);
+    compute_loop<kCompute, kSlotsSW, PF>(a, s_unit, s_item, s_fac, s_empty, lane, &s_bulk[0][0][0], &s_bulk_bar[0][0]);
 #else
-    compute_loop<kCompute, kSlotsSW>(a, s_unit, s_item, s_fac, s_empty, lane);
+    compute_loop<kCompute, kSlotsSW, PF>(a, s_unit, s_item, s_fac, s_empty, lane);
 #endif
   }
   report_exit(a);
@@ -1413,11 +1471,13 @@ __global__ void __launch_bounds__(kBlockWQ, BT_WQ_MIN_CTAS) scheduler_kernel_wq(
 }
 
 // Host-side launcher (called from runtime.cpp).
-// kernel: 0 = sw, 1 = rw, 2 = wq (grid in CTAs of that kernel's block size).
+// kernel: 0 = sw, 1 = rw, 2 = wq, 3 = sw with prefetching SCAL bodies (short
+// chains); grid in CTAs of that kernel's block size.
 cudaError_t launch_epoch(const EpochArgs &args, int grid, cudaStream_t stream, int kernel) {
   if (kernel == 2) scheduler_kernel_wq<<<grid, kBlockWQ, 0, stream>>>(args);
   else if (kernel == 1) scheduler_kernel_rw<<<grid, kBlock, 0, stream>>>(args);
-  else scheduler_kernel_sw<<<grid, kBlock, 0, stream>>>(args);
+  else if (kernel == 3) scheduler_kernel_sw<true><<<grid, kBlock, 0, stream>>>(args);
+  else scheduler_kernel_sw<false><<<grid, kBlock, 0, stream>>>(args);
   return cudaGetLastError();
 }
 
@@ -1430,7 +1490,10 @@ cudaError_t scheduler_occupancy(int *blocks_per_sm, int *block) {
   *block = kBlock;
   int a = 0, b = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, scheduler_kernel_rw, kBlock, 0);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, scheduler_kernel_sw, kBlock, 0);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, scheduler_kernel_sw<false>, kBlock, 0);
+  int c = 0;
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, scheduler_kernel_sw<true>, kBlock, 0);
+  if (c < b) b = c;
   *blocks_per_sm = a < b ? a : b;
   return e;
 }
