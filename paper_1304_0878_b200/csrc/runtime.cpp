@@ -481,6 +481,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   };
   if (big) rt->par(passA);
   else passA(0);
+  const double tA = now_ms();
   std::vector<RangeAcc> base(P);
   RangeAcc tot;
   for (int p = 0; p < P; ++p) {
@@ -566,6 +567,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   };
   if (big) rt->par(passB);
   else passB(0);
+  const double tB = now_ms();
   // CSR scatter (successor order within a list: edge creation order when
   // sequential; any order is valid).  An item with a single successor holds
   // the successor's id itself in DItem::succ_off (one dependent load less on
@@ -595,6 +597,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   }
 
   char *d = e.dblob;
+  const double tC = now_ms();
   if (!rt->span_open) {
     CUDA_TRY(rt, cudaEventRecord(rt->span_start, stream));
     rt->span_open = true;
@@ -706,6 +709,10 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   rt->stats.fused_tasks += B.fused;
   B.next_epoch();
   rt->stats.host_build_ms += now_ms() - t0;
+  static const bool dbg = getenv("BT_DEBUG_TIMING") != nullptr;
+  if (dbg)
+    fprintf(stderr, "flush_epoch N=%zu E=%zu U=%llu upload=%zu B: passA %.3f passB %.3f csr %.3f launch %.3f ms\n", N, E,
+            (unsigned long long)U, upload, tA - t0, tB - tA, tC - tB, now_ms() - tC);
   if (rt->cfg.flags & BT_FLAG_SYNC_EPOCH) return retire(rt, e);
   return 0;
 }
