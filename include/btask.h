@@ -165,6 +165,29 @@ int bt_data_set_rank(bt_runtime *rt, bt_handle h, int rank);
  * floor(t * nranks / nparts).  -EINVAL if h is not partitioned. */
 int bt_data_distribute_block(bt_runtime *rt, bt_handle h);
 
+/* Cross-rank reads between the ranks of one node (StarPU-MPI, P:1041-1061:
+ * data a task only reads is transferred to the rank that runs it).
+ * Collective: every rank of the job (one process each, ranks 0..nranks-1 of
+ * bt_config) calls it once with the same `name`, a POSIX shared-memory name
+ * unique to the job ("/bt-<job id>"); it returns when all ranks have joined.
+ * Call it before registering data: device replicas of host-homed data are
+ * then allocated shareably (cudaMalloc; device-homed data must be cudaMalloc'ed
+ * memory, e.g. a torch tensor).
+ * Afterwards an AXPY/COPY whose read operand x lives on rank a and whose
+ * written operand y lives on rank b != a no longer fails with -EXDEV: every
+ * rank submits it (same order on all ranks); rank a and rank b meet there --
+ * b copies x's current value (ordered after a's earlier writers of x) from
+ * a's device memory (CUDA IPC; a peer copy over NVLink between GPUs) into b's
+ * own replica of x, a's later writers of x wait for that copy, and the task
+ * runs on b; other ranks skip it.  Every rank must register x (with local
+ * storage) and partition it alike.  A non-owner's replica of x holds the last
+ * value it received; only owners' data is defined after the program.
+ * Returns 0, -EINVAL (nranks < 2, bad name, ranks disagree), -ENODEV
+ * (host-only runtime), -EBUSY (already initialised), -ETIMEDOUT (a rank did
+ * not join within 60 s), -EIO.  A rendezvous that times out (60 s) returns
+ * -EIO from the insert and poisons the runtime. */
+int bt_comm_init(bt_runtime *rt, const char *name);
+
 /* starpu_insert_task, asynchronous.
  *   codelet    BT_CL_*
  *   cl_args    packed scalar arguments, little-endian, declaration order, no
@@ -177,7 +200,7 @@ int bt_data_distribute_block(bt_runtime *rt, bt_handle h);
  * -ENOENT unknown/stale handle ("attempt to use unregistered pointer"),
  * -EINVAL (bad codelet/modes/nbuffers/cl_args_size, operand length mismatch),
  * -EBUSY (partitioned parent, or acquired handle), -EXDEV (the task reads
- * data homed on another rank: cross-rank tasks are not supported),
+ * data homed on another rank and bt_comm_init was not called),
  * -ENOMEM, -EIO. */
 int bt_insert_task(bt_runtime *rt, int codelet, const void *cl_args, size_t cl_args_size,
                    const bt_handle *handles, const int *modes, unsigned nbuffers);

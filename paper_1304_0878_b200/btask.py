@@ -74,6 +74,7 @@ _SIGS = {
     "bt_data_unpartition": (_c.c_int, [_c.c_void_p, bt_handle]),
     "bt_data_set_rank": (_c.c_int, [_c.c_void_p, bt_handle, _c.c_int]),
     "bt_data_distribute_block": (_c.c_int, [_c.c_void_p, bt_handle]),
+    "bt_comm_init": (_c.c_int, [_c.c_void_p, _c.c_char_p]),
     "bt_insert_task": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_void_p, _c.c_size_t, _P(bt_handle), _P(_c.c_int),
                                    _c.c_uint]),
     "bt_insert_task_batch": (_c.c_int, [_c.c_void_p, _c.c_size_t, _P(_c.c_int32), _P(_c.c_float), _P(bt_handle),
@@ -189,6 +190,10 @@ class Runtime:
 
     def distribute_block(self, h: int):
         self._check(bt_data_distribute_block(self.rt, h), "bt_data_distribute_block")
+
+    def comm_init(self, name: str):
+        """bt_comm_init: collective over the job's ranks (cross-rank reads)."""
+        self._check(bt_comm_init(self.rt, name.encode()), "bt_comm_init")
 
     def acquire(self, h: int, mode: int = BT_R):
         self._check(bt_data_acquire(self.rt, h, mode), "bt_data_acquire")

@@ -13,8 +13,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libbtask.so")
-SOURCES = ["scheduler.cu", "runtime.cpp", "builder.cpp"]
-HEADERS = ["device_abi.h", "builder.hpp", "pool.hpp"]
+SOURCES = ["scheduler.cu", "runtime.cpp", "builder.cpp", "comm.cpp"]
+HEADERS = ["device_abi.h", "builder.hpp", "pool.hpp", "comm.hpp"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

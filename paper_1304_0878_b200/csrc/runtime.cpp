@@ -24,6 +24,7 @@
 
 #include "../../include/btask.h"
 #include "builder.hpp"
+#include "comm.hpp"
 #include "device_abi.h"
 #include "pool.hpp"
 
@@ -95,6 +96,8 @@ struct Slot {
   int home_node = 0;
   int acquired = 0;           // 0, BT_R or BT_RW (on the acquired handle itself)
   bool owns_dev = false;      // root only: runtime-allocated replica
+  bool ipc_alloc = false;     // root only: replica from cudaMalloc (shareable with other ranks)
+  uint64_t reg_key = 0;       // root only: registration ordinal (equal on all ranks)
 };
 
 struct EpochBuf {
@@ -187,6 +190,8 @@ struct bt_runtime {
   }
   void put_event(cudaEvent_t e) { ev_free.push_back(e); }
   bt_stats stats{};
+  std::unique_ptr<Comm> comm;   // cross-rank reads (bt_comm_init)
+  uint64_t reg_seq = 0;         // registrations so far (Slot::reg_key)
 
   // host-only snapshot storage
   std::vector<uint8_t> snap_kind;
@@ -910,6 +915,7 @@ int bt_shutdown(bt_runtime *rt) {
     if (rt->d2h) cudaStreamDestroy(rt->d2h);
     if (rt->span_start) cudaEventDestroy(rt->span_start);
     if (rt->span_end) cudaEventDestroy(rt->span_end);
+    rt->comm.reset();
     if (rt->own_stream) cudaStreamDestroy(rt->stream);
   }
   delete rt;
@@ -950,7 +956,9 @@ int bt_vector_data_register(bt_runtime *rt, bt_handle *out, int home_node, void 
     if (home_node == 1) {
       dptr = static_cast<float *>(ptr);
     } else {
-      cudaError_t e = cudaMallocAsync((void **)&dptr, nx * 4, rt->stream);
+      // with cross-rank reads enabled the replica must be shareable (CUDA IPC
+      // cannot export stream-ordered pool allocations)
+      cudaError_t e = rt->comm ? cudaMalloc((void **)&dptr, nx * 4) : cudaMallocAsync((void **)&dptr, nx * 4, rt->stream);
       if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(rt, -ENOMEM, "cannot allocate the device replica (%zu bytes)", nx * 4);
@@ -959,7 +967,8 @@ int bt_vector_data_register(bt_runtime *rt, bt_handle *out, int home_node, void 
       if (nx * 4 < kUploadChunk) {
         e = cudaMemcpyAsync(dptr, ptr, nx * 4, cudaMemcpyHostToDevice, rt->stream);
         if (e != cudaSuccess) {
-          cudaFreeAsync(dptr, rt->stream);
+          if (rt->comm) cudaFree(dptr);
+          else cudaFreeAsync(dptr, rt->stream);
           return cuda_fail(rt, e, "register upload");
         }
       }
@@ -975,6 +984,8 @@ int bt_vector_data_register(bt_runtime *rt, bt_handle *out, int home_node, void 
   sl.home_node = home_node;
   sh.rank = ptr ? rt->cfg.rank : -1;
   sl.owns_dev = owns;
+  sl.ipc_alloc = owns && rt->comm;
+  sl.reg_key = ++rt->reg_seq;
   if (ptr) {
     rt->ranges[lo] = {hi, s};
     rt->by_ptr[lo] = s;
@@ -1111,6 +1122,20 @@ int bt_data_set_rank(bt_runtime *rt, bt_handle h, int rank) {
   return 0;
 }
 
+int bt_comm_init(bt_runtime *rt, const char *name) {
+  if (int r = check_live(rt)) return r;
+  if (rt->host_only) return fail(rt, -ENODEV, "host-only runtime: nothing executes");
+  if (rt->comm) return fail(rt, -EBUSY, "bt_comm_init already called");
+  if (rt->cfg.nranks < 2) return fail(rt, -EINVAL, "cross-rank reads need nranks >= 2");
+  cudaSetDevice(rt->device);
+  Comm *c = nullptr;
+  std::string err;
+  if (int r = Comm::create(name, rt->cfg.rank, rt->cfg.nranks, rt->device, &c, &err))
+    return fail(rt, r, "bt_comm_init: %s", err.c_str());
+  rt->comm.reset(c);
+  return 0;
+}
+
 int bt_data_distribute_block(bt_runtime *rt, bt_handle h) {
   if (int r = check_live(rt)) return r;
   uint32_t s = resolve(rt, h);
@@ -1141,6 +1166,41 @@ inline int64_t operand(bt_runtime *rt, int codelet, bt_handle h) {
   return s;
 }
 
+// Order `stream` after the chunked uploads covering device bytes [lo, hi).
+int wait_uploads(bt_runtime *rt, cudaStream_t stream, uint64_t lo, uint64_t hi) {
+  for (auto &kv : rt->caches) {
+    RootCache &c = kv.second;
+    if (c.uploads.empty() || hi <= c.dlo || lo >= c.dhi) continue;
+    for (const UploadChunk &u : c.uploads)
+      if (u.lo < hi && lo < u.hi) CUDA_TRY(rt, cudaStreamWaitEvent(stream, u.ev, 0));
+  }
+  return 0;
+}
+
+// One side of a cross-rank read of slot x (comm.hpp): the owner publishes
+// it for `peer` (send), the reader copies it into its own replica (recv).
+// Everything submitted earlier is flushed first, so the copy is ordered after
+// the owner's earlier writers and the reader's earlier readers of the replica.
+int cross_rank_read(bt_runtime *rt, uint32_t x, int peer, bool send) {
+  if (int r = flush_epoch(rt)) return r;
+  const Slot &xs = rt->slots[x];
+  const uint32_t root = xs.root;
+  float *const dptr = rt->hot[x].dptr;
+  const uint64_t bytes = rt->hot[x].nx * 4;
+  const uint64_t lo = reinterpret_cast<uint64_t>(dptr);
+  if (int r = wait_uploads(rt, rt->stream, lo, lo + bytes)) return r;   // initial data in the replica
+  std::string err;
+  const int r = send ? rt->comm->send(rt->stream, peer, rt->slots[root].reg_key, rt->hot[root].dptr,
+                                      rt->hot[root].nx * 4, &err)
+                     : rt->comm->recv(rt->stream, peer, rt->slots[root].reg_key, (xs.offset - rt->slots[root].offset) * 4,
+                                      dptr, bytes, &err);
+  if (r) {
+    rt->poisoned = -EIO;   // the ranks' streams are no longer in a known order
+    return fail(rt, r, "cross-rank read: %s", err.c_str());
+  }
+  return 0;
+}
+
 int submit(bt_runtime *rt, int codelet, float scalar, bt_handle h0, bt_handle h1) {
   int64_t s0 = operand(rt, codelet, h0);
   if (s0 < 0) return (int)s0;
@@ -1164,7 +1224,15 @@ int submit(bt_runtime *rt, int codelet, float scalar, bt_handle h0, bt_handle h1
     if (x.nx != y.nx) return insert_fail(rt, codelet, -EINVAL, "operand lengths differ");
     if (x.rank != y.rank) {
       if (x.rank < 0 || y.rank < 0) return insert_fail(rt, codelet, -EINVAL, "data has no home rank");
-      return insert_fail(rt, codelet, -EXDEV, "operands live on different ranks");
+      if (!rt->comm)
+        return insert_fail(rt, codelet, -EXDEV, "operands live on different ranks (see bt_comm_init)");
+      // cross-rank read (comm.hpp): the task runs on y's owner, which first
+      // copies x from x's owner; both meet here in submission order
+      const int me = rt->cfg.rank;
+      if (me == x.rank || me == y.rank) {
+        if (!x.dptr || (me == y.rank && !y.dptr)) return insert_fail(rt, codelet, -EINVAL, "no local storage");
+        if (int r = cross_rank_read(rt, (uint32_t)s0, me == x.rank ? y.rank : x.rank, me == x.rank)) return r;
+      }
     }
     if (y.rank != rt->cfg.rank) {
       if (y.rank < 0) return insert_fail(rt, codelet, -EINVAL, "data has no home rank");
@@ -1574,7 +1642,12 @@ int bt_data_unregister(bt_runtime *rt, bt_handle h) {
       if (int r = sync_to_host(rt, s, lo, lo + sh.nx * 4)) return r;
     }
     rt->caches.erase(s);
-    if (sl.owns_dev) CUDA_TRY(rt, cudaFreeAsync(sh.dptr, rt->stream));
+    if (sl.owns_dev && sl.ipc_alloc) {
+      CUDA_TRY(rt, cudaStreamSynchronize(rt->stream));
+      CUDA_TRY(rt, cudaFree(sh.dptr));
+    } else if (sl.owns_dev) {
+      CUDA_TRY(rt, cudaFreeAsync(sh.dptr, rt->stream));
+    }
   }
   if (sl.hptr) {
     rt->ranges.erase(reinterpret_cast<uintptr_t>(sl.hptr));

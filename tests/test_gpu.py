@@ -450,3 +450,71 @@ def test_bench_launch_configuration_c5(B):
     got = x[torch.from_numpy(idx).cuda()].cpu().numpy()
     exp = oracle.scal_chain(oracle.scal_chain(x0, f), f)
     assert_bits_equal(got, exp, "bench configuration, two steps")
+
+
+# ---- cross-rank reads (bt_comm_init) ----------------
+
+def _check_owned(program, results, owners):
+    from tests import xrank
+    exp = oracle.run(program)
+    seen = 0
+    for b in range(len(program.buffers)):
+        for t, off, n in xrank.leaf_ranges(program, b):
+            assert (b, t) in results, f"leaf {(b, t)} owned by nobody"
+            assert_bits_equal(results[(b, t)], exp[b][off:off + n], f"{program.name} buffer {b} tile {t}")
+            seen += 1
+    assert seen == len(results)
+
+
+@pytest.mark.parametrize("batch", [True, False])
+def test_cross_rank_reads_random_programs(B, batch):
+    """Two ranks (processes) with random owners per leaf run random SCAL/AXPY/COPY
+    programs; an AXPY/COPY reading another rank's data copies it over (CUDA IPC)
+    at its submission point.  Every leaf's owner ends with the oracle's bits."""
+    from tests import xrank
+    for seed in range(4):
+        p = W.random_small_program(3000 + seed, max_tasks=12, max_elems=4096)
+        results, stats, owners = xrank.run(p, nranks=2, seed=seed, batch=batch)
+        _check_owned(p, results, owners)
+
+
+def test_cross_rank_write_after_read(B):
+    """WAR across ranks: X (rank 0) is read by rank 1 (COPY X->Y), then
+    overwritten by rank 0 right away; rank 1 must still see the old X.  Also
+    RAW the other way (AXPY Y->Z on rank 0 reads Y from rank 1).  4 MiB
+    buffers, 24 rounds, three ranks."""
+    from tests import xrank
+    n = 1 << 20
+    rng = np.random.default_rng(W.SEED_BASE + 90)
+    bufs = [W.unit_interval_floats(rng, n) for _ in range(4)]
+    rows = []
+    for i in range(24):
+        f = float(np.float32(0.9 + 0.2 * rng.random()))
+        rows += [(W.SCAL, f, 0, -1, -1, -1),          # X *= f        (rank 0)
+                 (W.COPY, 0.0, 0, -1, 1, -1),         # Y = X          (rank 1 reads X)
+                 (W.SCAL, 1.0 / f, 0, -1, -1, -1),    # X *= 1/f      (rank 0, after rank 1's copy)
+                 (W.AXPY, 0.5, 1, -1, 2, -1),         # Z += 0.5 Y     (rank 2 reads Y)
+                 (W.SCAL, 0.75, 1, -1, -1, -1),       # Y *= 0.75      (rank 1)
+                 (W.COPY, 0.0, 2, -1, 3, -1)]         # W = Z          (rank 0 reads Z)
+    p = W.Program(bufs, [0, 0, 0, 0], W._tasks(len(rows)), name="cross-rank WAR/RAW")
+    for i, r in enumerate(rows):
+        p.tasks[i] = r
+    results, stats, owners = xrank.run(p, nranks=3, owners=[0, 1, 2, 0])
+    _check_owned(p, results, owners)
+
+
+def test_cross_rank_read_after_long_write(B):
+    """RAW across ranks: rank 0 runs a long unfused chain on X (64 MiB x 48
+    dependent scalings) and rank 1 copies X right after it was submitted: the
+    copy must wait for the chain's last scaling on rank 0's stream."""
+    from tests import xrank
+    n = 1 << 24
+    rng = np.random.default_rng(W.SEED_BASE + 91)
+    bufs = [W.unit_interval_floats(rng, n), np.zeros(n, np.float32)]
+    rows = [(W.SCAL, float(np.float32(0.9 + 0.2 * rng.random())), 0, -1, -1, -1) for _ in range(48)]
+    rows.append((W.COPY, 0.0, 0, -1, 1, -1))
+    p = W.Program(bufs, [0, 0], W._tasks(len(rows)), name="cross-rank RAW after a long chain")
+    for i, r in enumerate(rows):
+        p.tasks[i] = r
+    results, stats, owners = xrank.run(p, nranks=2, owners=[0, 1], batch=False, flags=B.BT_FLAG_NO_FUSION)
+    _check_owned(p, results, owners)
