@@ -72,6 +72,19 @@ def test_init_rejects_two_forced_kernels(B):
     assert B.bt_shutdown(h) == 0
 
 
+def test_comm_init_conventions_without_gpu(B):
+    """bt_comm_init (cross-rank reads) needs a GPU runtime with nranks >= 2."""
+    cfg = B.bt_config()
+    B.bt_config_init(ctypes.byref(cfg))
+    h = ctypes.c_void_p()
+    cfg.flags = B.BT_FLAG_HOST_ONLY
+    cfg.nranks, cfg.rank = 2, 1
+    assert B.bt_init(ctypes.byref(cfg), ctypes.byref(h)) == 0
+    assert B.bt_comm_init(h, b"/bt-test-host") == -errno.ENODEV
+    assert "host-only" in B.bt_last_error(h).decode()
+    assert B.bt_shutdown(h) == 0
+
+
 def host_rt(B, **kw):
     return B.Runtime(flags=B.BT_FLAG_HOST_ONLY | kw.pop("flags", 0), **kw)
 
