@@ -42,10 +42,15 @@ def load_peaks():
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
-def workload_name(cfg):
-    return (f"C5: {cfg['nx']} float32 ({cfg['nx'] * 4 / 2**30:.0f} GiB), {cfg['ntiles']} tiles x "
+def workload_name(cfg, world=1, scaling="weak"):
+    base = (f"C5: {cfg['nx']} float32 ({cfg['nx'] * 4 / 2**30:.0f} GiB), {cfg['ntiles']} tiles x "
             f"{cfg['nx'] // cfg['ntiles']}, {cfg['sweeps']} chained vector_scal sweeps (sweep-major), "
             f"owner-computes tiles")
+    if world == 1:
+        return base
+    if scaling == "weak":
+        return base + f"; weak scaling: one such 4 GiB shard per GPU ({world} x 4 GiB in total)"
+    return base + f"; strong scaling: the 4 GiB vector's tiles split over {world} GPUs"
 
 
 class ClockSampler:
@@ -147,9 +152,10 @@ def run_reference(args):
     value = 8.0 * elems / dt / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "tasks_per_s": sample_tiles * cfg["sweeps"] / dt,
-            "config": {"workload": workload_name(cfg), "sample": f"{sample_tiles} of {cfg['ntiles']} tiles, "
+            "config": {"workload": workload_name(cfg, args.gpus, args.scaling),
+                       "sample": f"{sample_tiles} of {cfg['ntiles']} tiles, "
                        f"all {cfg['sweeps']} sweeps, task-major"},
             "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
                              "sample": f"{sample_tiles} tiles x {tile} floats x {cfg['sweeps']} sweeps "
@@ -212,6 +218,9 @@ def main():
     ap.add_argument("--chunk-bytes", type=int, default=0, help="fixed work-unit size (0 = adaptive)")
     ap.add_argument("--host-threads", type=int, default=0)
     ap.add_argument("--rounds", type=int, default=0, help="pipelined rounds per SCAL run (0 = library default)")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="N > 1: weak = a full 4 GiB C5 shard per GPU (default, per-GPU work fixed); "
+                         "strong = one 4 GiB vector split over the GPUs")
     ap.add_argument("--hbm-variant", type=int, default=1,
                     help="also time the HBM-bound 16-sweep variant on the same tiles (secondary key)")
     ap.add_argument("--streamed", type=int, default=1,
@@ -246,10 +255,10 @@ def main():
         else:
             dist.init_process_group(backend)
 
-    def allreduce_max(vals):
+    def allreduce_max(vals, op="max"):
         t = torch.tensor(vals, dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         if dist:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
         return t.tolist()
 
     from paper_1304_0878_b200 import btask as B
@@ -259,8 +268,14 @@ def main():
     T, S = cfg["ntiles"], cfg["sweeps"]
     tile = cfg["nx"] // T
     # --emulate-ranks N (diagnostic, N=1 only): time rank 0's share of an N-rank run
-    shard_world = args.emulate_ranks if (args.emulate_ranks and world == 1) else world
-    t_lo, t_hi = rank * T // shard_world, (rank + 1) * T // shard_world
+    # weak scaling (default, per-GPU work fixed): every rank owns a full C5 shard
+    # of T tiles; strong: the T tiles of one vector are split over the ranks
+    if args.scaling == "weak" and not args.emulate_ranks:
+        shard_world, shard_rank = 1, 0
+    else:
+        shard_world = args.emulate_ranks if (args.emulate_ranks and world == 1) else world
+        shard_rank = rank
+    t_lo, t_hi = shard_rank * T // shard_world, (shard_rank + 1) * T // shard_world
     my_tiles = t_hi - t_lo
     elems = my_tiles * tile
     factors = W.sweep_factors(np.random.default_rng(W.SEED_BASE + 4), S)
@@ -304,6 +319,7 @@ def main():
     span_ms = st["device_span_ms"] / args.steps                  # device time per step (launches overlap)
     host_ms = st["host_build_ms"] / args.steps
     ms, kern_ms_max, host_ms_max, span_ms_max = allreduce_max([ms, kern_ms, host_ms, span_ms])
+    launches_all = int(allreduce_max([float(st["kernel_launches"])], op="sum")[0])   # every rank's kernels
 
     # ---- streamed (diagnostic, not the headline): the same K steps submitted
     # back to back and waited for once (bt_insert_task_batch is asynchronous:
@@ -392,7 +408,7 @@ def main():
 
     if rank == 0:
         peaks, peak_src = load_peaks()
-        total_elems = cfg["nx"] * 1.0
+        total_elems = cfg["nx"] * (world if (args.scaling == "weak" and not args.emulate_ranks) else 1) * 1.0
         compulsory = 8.0 * total_elems                     # read + write each element once per step
         value = compulsory / (ms * 1e-3) / 1e9
         clocks = clk.summary()
@@ -441,16 +457,18 @@ def main():
             return 0
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "frac_of_8TBps": value / NOMINAL_HBM_GBPS, "frac_of_measured_hbm": value / peaks["hbm_gbs"],
+            "frac_of_8TBps": value / (NOMINAL_HBM_GBPS * world),
+            "frac_of_measured_hbm": value / (peaks["hbm_gbs"] * world),
             "tasks_per_s": ntasks * world / (ms * 1e-3),
             "effective_unfused_GBps": 8.0 * total_elems * S / (ms * 1e-3) / 1e9,
             "host_build_ms_per_step": host_ms_max, "device_ms_per_step": span_ms_max,
-            "config": {"workload": workload_name(cfg), "tasks_per_step": ntasks * world, "builder_threads": threads,
+            "config": {"workload": workload_name(cfg, world, args.scaling), "tasks_per_step": ntasks * world,
+                       "builder_threads": threads,
                        "fusion": fused, "parallelism": f"owner-computes tiles over {world} rank(s)",
                        "l2": "4 GiB working set > 126 MB L2 (no flush needed)"},
-            "gpu_launches": int(st["kernel_launches"]),
+            "gpu_launches": launches_all,
             "clocks": clocks,
             "roofline": roof,
         }
