@@ -48,7 +48,10 @@ constexpr uint32_t kUnitsPerCta = 16;               // adaptive chunking: target
 constexpr uint32_t kDefaultMaxFused = 256;
 constexpr uint32_t kDefaultParallelMin = 16384;
 constexpr int kDefaultRounds = 4;
-constexpr int kRoundsUploading = 8;                 // rounds for partitions of data still being uploaded
+#ifndef BT_ROUNDS_UPLOADING
+#define BT_ROUNDS_UPLOADING 8
+#endif
+constexpr int kRoundsUploading = BT_ROUNDS_UPLOADING;   // rounds for partitions of data still being uploaded
 constexpr uint32_t kDefaultPipelineMin = 131072;
 constexpr int kEpochRing = 12;                      // epoch buffers in flight (>= rounds + 2)
 constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;   // 20 s
