@@ -518,3 +518,50 @@ def test_cross_rank_read_after_long_write(B):
         p.tasks[i] = r
     results, stats, owners = xrank.run(p, nranks=2, owners=[0, 1], batch=False, flags=B.BT_FLAG_NO_FUSION)
     _check_owned(p, results, owners)
+
+
+@pytest.mark.parametrize("kernel", ["auto", "sw", "rw", "wq"])
+@pytest.mark.parametrize("max_fused", [1024, 256, 7])
+def test_long_chain_max_fused(B, kernel, max_fused):
+    """1,000 chained SCALs on one ragged 4,099-element vector: fused into items
+    of up to max_fused factors (1,024 = the kernels' shared-memory factor
+    capacity), each with every rounding in submission order."""
+    rng = np.random.default_rng(W.SEED_BASE + 92)
+    x = W.unit_interval_floats(rng, 4099)
+    f = W.sweep_factors(rng, 1000)
+    p = W.sweep_program(x.shape[0], 1, f, x, name="1000-chain")
+    stats = compare_program(p, max_fused=max_fused, flags=KERNELS[kernel])
+    assert stats["items"] == -(-1000 // max_fused)
+
+
+def test_one_element_tiles(B):
+    """Degenerate partitions: 1-element tiles (nparts = nx) and 3-element tiles
+    (every 256-bit vector path falls back to the scalar head/tail), with
+    SCAL/AXPY/COPY across tiles of two buffers."""
+    rng = np.random.default_rng(W.SEED_BASE + 93)
+    for nx, nparts in ((777, 777), (3 * 500 + 2, 500)):
+        bufs = [W.unit_interval_floats(rng, nx), W.unit_interval_floats(rng, nx)]
+        rows = []
+        lens = [len(range(*W_tile(nx, nparts, t))) for t in range(nparts)]
+        for _ in range(3000):
+            kind = int(rng.integers(0, 3))
+            b0, t0 = int(rng.integers(0, 2)), int(rng.integers(0, nparts))
+            if kind == 0:
+                rows.append((W.SCAL, float(np.float32(0.9 + 0.2 * rng.random())), b0, t0, -1, -1))
+                continue
+            same = [t for t in range(nparts) if lens[t] == lens[t0]]
+            t1 = int(rng.choice(same))
+            b1 = 1 - b0
+            if kind == 1:
+                rows.append((W.AXPY, float(np.float32(rng.uniform(-0.5, 0.5))), b0, t0, b1, t1))
+            else:
+                rows.append((W.COPY, 0.0, b0, t0, b1, t1))
+        p = W.Program(bufs, [nparts, nparts], W._tasks(len(rows)), name=f"{nparts} tiles over {nx}")
+        for i, r in enumerate(rows):
+            p.tasks[i] = r
+        compare_program(p)
+
+
+def W_tile(nx, nparts, t):
+    off, n = oracle.model.tile_range(nx, nparts, t)
+    return off, off + n
