@@ -1390,6 +1390,9 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
   // lane l owns slot blocks k with k % P == l (in every round); dense local
   // index over the lane's blocks: (k / P) * 64 + (s & 63)
   const uint32_t nlocal = (uint32_t)((((nslots + 63) >> 6) + P - 1) / P) * 64;
+  // (k / P) * 64 per 64-slot block k, so the per-task local index needs no division
+  std::vector<uint32_t> blk_local((nslots + 63) >> 6);
+  for (size_t k = 0; k < blk_local.size(); ++k) blk_local[k] = (uint32_t)(k / (size_t)P) * 64;
   std::vector<size_t> round_size(R, 0);
   size_t local = 0;
   for (int c = 0; c < P; ++c)
@@ -1440,7 +1443,7 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
         Lane &L = rt->lanes[(size_t)(r - rlo) * P + l];
         B.lane_runs(
             L, ptrs.data(), tptr.data(), cnts.data(), P, deps, nlocal,
-            [up = (uint32_t)P](uint32_t s) { return ((s >> 6) / up) * 64 + (s & 63); },
+            [bl = blk_local.data()](uint32_t s) { return bl[s >> 6] + (s & 63); },
             [up = (uint32_t)P, ul = (uint32_t)l](uint32_t loc) { return ((loc >> 6) * up + ul) * 64 + (loc & 63); },
             [hot](uint32_t s) {
               return std::pair<uint64_t, uint64_t>(reinterpret_cast<uint64_t>(hot[s].dptr), hot[s].nx);
