@@ -56,7 +56,6 @@ constexpr uint32_t kDefaultPipelineMin = 131072;
 constexpr int kEpochRing = 12;                      // epoch buffers in flight (>= rounds + 2)
 constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;   // 20 s
 constexpr size_t kParallelPack = 4096;              // items above which the pack runs on the pool
-constexpr uint64_t kReleaseWarpBelow = 65536;       // units with less work (elements x chain length) use "rw"
 constexpr uint64_t kWarpUnitMax = 4096;             // units of at most this many elements use "wq"
 constexpr uint64_t kPrefetchBelowK = 32;            // "sw" epochs with shorter average chains prefetch
 constexpr uint64_t kUploadChunk = 64ull << 20;      // registrations >= this upload in chunks on a copy stream
@@ -656,11 +655,9 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
       if (u.lo < tot.ahi && tot.alo < u.hi) CUDA_TRY(rt, cudaStreamWaitEvent(stream, u.ev, 0));
   }
   CUDA_TRY(rt, cudaEventRecord(e.start, stream));
-  // small work units are scheduling-bound: use the kernel with a dedicated
-  // release warp; large ones are body-bound: keep all 8 warps computing
-  static const char *kv = getenv("BT_KERNEL");   // "rw" / "sw": experiments only
-  // work per unit = elements x chained multiplies: a 4 KiB unit of a 64-long
-  // chain is compute-bound (sw), a 4 KiB single scaling is scheduling-bound (rw)
+  // scheduler variant ("Persistent scheduler kernels")
+  static const char *kv = getenv("BT_KERNEL");   // "sw" / "rw" / "wq": experiments only
+  // work per unit = elements x chained multiplies
   const uint64_t avg_work = (sampled_work / cnt * N) / std::max<uint64_t>(1, U);
   // units of at most 16 KiB: one warp per unit ("wq", many units in flight)
   const uint64_t avg_elems = (sampled / cnt * N) / std::max<uint64_t>(1, U);
@@ -668,12 +665,14 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   // a 1-wide dependency chain) is latency-bound, and the CTA-wide "rw" kernel
   // runs chains in its slots with the shortest dependency latency
   const bool wide = U0 * 4 >= (uint64_t)rt->grid_wq * 8;
-  int kernel = avg_elems <= kWarpUnitMax && rt->grid_wq > 0 && wide ? 2 : avg_work < kReleaseWarpBelow ? 1 : 0;
-  // sw: epochs of short chains (average k below the FP32/HBM ridge) are
-  // HBM-bound and use the instance whose bodies prefetch the next step's data
-  if (kernel == 0 && avg_work < kPrefetchBelowK * avg_elems) kernel = 3;
-  if (kv) kernel = kv[0] == 'w' ? 2 : kv[0] == 'r' ? 1 : 0;
-  if (rt->cfg.flags & BT_FLAG_KERNEL_SW) kernel = avg_work < kPrefetchBelowK * avg_elems ? 3 : 0;
+  // units above 16 KiB: CTA-wide bodies with one scheduler warp ("sw"; C3
+  // with 64 KiB units: 14.1 ms vs 14.7 ms on "rw", tools/c3_chunks.py); epochs
+  // of short chains (average k below the FP32/HBM ridge) are HBM-bound and
+  // use the instance whose bodies prefetch the next step's data
+  const bool prefetch = avg_work < kPrefetchBelowK * avg_elems;
+  int kernel = avg_elems <= kWarpUnitMax ? (wide && rt->grid_wq > 0 ? 2 : 1) : prefetch ? 3 : 0;
+  if (kv) kernel = kv[0] == 'w' ? 2 : kv[0] == 'r' ? 1 : prefetch ? 3 : 0;
+  if (rt->cfg.flags & BT_FLAG_KERNEL_SW) kernel = prefetch ? 3 : 0;
   if (rt->cfg.flags & BT_FLAG_KERNEL_RW) kernel = 1;
   if ((rt->cfg.flags & BT_FLAG_KERNEL_WQ) && rt->grid_wq > 0) kernel = 2;
   const int kgrid = kernel == 2 ? (int)std::min<uint64_t>((uint64_t)rt->grid_wq, (U + 7) / 8) : grid;

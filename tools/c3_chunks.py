@@ -1,4 +1,5 @@
-"""C3 (random DAG, 64 x 4 MiB buffers) device time vs work-unit size."""
+"""C3 (random DAG, 64 x 4 MiB buffers) device time vs work-unit size and
+scheduler variant:  python tools/c3_chunks.py [auto|sw|rw|wq ...]"""
 import json, os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -9,8 +10,10 @@ from paper_1304_0878_b200.programs import Session
 
 p = W.c3_random_dag()
 tensors = [torch.from_numpy(b).cuda() for b in p.buffers]
-for cb in [0, 16384, 32768, 65536, 131072, 262144]:
-    with B.Runtime(chunk_bytes=cb) as rt:
+KFLAG = {"auto": 0, "sw": B.BT_FLAG_KERNEL_SW, "rw": B.BT_FLAG_KERNEL_RW, "wq": B.BT_FLAG_KERNEL_WQ}
+kernels = sys.argv[1:] or ["auto"]
+for kern, cb in [(k, c) for k in kernels for c in [0, 16384, 32768, 65536, 131072, 262144]]:
+    with B.Runtime(chunk_bytes=cb, flags=KFLAG[kern]) as rt:
         s = Session(rt, p, device_tensors=tensors)
         h0, h1 = s.handle_arrays()
         t = p.tasks
@@ -22,4 +25,4 @@ for cb in [0, 16384, 32768, 65536, 131072, 262144]:
             if r:
                 dev.append(rt.stats()["device_span_ms"])
         s.finish()
-    print(json.dumps({"chunk_bytes": cb, "device_ms": float(np.median(dev))}), flush=True)
+    print(json.dumps({"kernel": kern, "chunk_bytes": cb, "device_ms": float(np.median(dev))}), flush=True)
