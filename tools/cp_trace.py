@@ -1,3 +1,5 @@
+"""Per-link timeline of a 200-long chain of 4 MiB tasks on the sw kernel from
+BT_FLAG_TIMESTAMPS traces (task span, gaps, per-unit pop/body/release)."""
 import sys, json
 sys.path.insert(0, '.')
 import numpy as np, torch
