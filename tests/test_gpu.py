@@ -565,3 +565,20 @@ def test_one_element_tiles(B):
 def W_tile(nx, nparts, t):
     off, n = oracle.model.tile_range(nx, nparts, t)
     return off, off + n
+
+
+def test_two_runtimes_interleaved(B):
+    """Two runtimes in one process on one GPU (own streams, pools, epochs):
+    their programs are submitted interleaved and each matches the oracle."""
+    from paper_1304_0878_b200.programs import Session
+    progs = [W.random_small_program(4100 + i, max_tasks=40, max_elems=3000) for i in range(2)]
+    with B.Runtime(flags=B.BT_FLAG_NO_FUSION) as r0, B.Runtime(host_threads=3) as r1:
+        sess = [Session(r0, progs[0]), Session(r1, progs[1])]
+        for s_ in sess:
+            s_.submit(batch=False)
+        r1.wait()
+        r0.wait()
+        outs = [s_.finish() for s_ in sess]
+    for p, out in zip(progs, outs):
+        for b, (o, e) in enumerate(zip(out, oracle.run(p))):
+            assert_bits_equal(o, e, f"{p.name} buffer {b}")
