@@ -51,7 +51,13 @@ def run(name, p, reps, **kw):
         s = Session(rt, p, device_tensors=tensors)
         h0, h1 = s.handle_arrays()
         only_scal = bool(np.all(p.tasks["codelet"] == W.SCAL))
-        t = p.tasks
+        # contiguous task columns made once (strided structured-array views
+        # would be copied by the binding inside the timed region)
+        t = {k: np.ascontiguousarray(p.tasks[k]) for k in ("codelet", "scalar")}
+        t["codelet"] = t["codelet"].astype(np.int32)
+        t["scalar"] = t["scalar"].astype(np.float32)
+        h0 = np.ascontiguousarray(h0, np.uint64)
+        h1 = np.ascontiguousarray(h1, np.uint64)
         times, dev = [], []
         for r in range(reps + 1):
             rt.stats_reset()
