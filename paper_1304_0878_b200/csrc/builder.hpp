@@ -95,7 +95,16 @@ struct LaneEntry {
   uint32_t fbits;
 };
 
+// A run of consecutive tasks of one SCAL batch whose handles belong to the
+// same builder group (stream positions [start, start + len) of the batch).
+struct RunRec {
+  uint32_t start;
+  uint32_t len;
+};
+
 struct alignas(64) Lane {
+  vec<LaneEntry> gather;              // the lane's entries of one round, gathered from the runs
+  vec<uint32_t> gtask;                // their task indices (record_tasks only)
   vec<uint32_t> cnt;                  // lane_runs scratch: per local slot counters
   vec<uint32_t> tasks;                // lane_runs scratch: task index per sorted factor
   vec<HItem> items;

@@ -157,6 +157,11 @@ struct bt_runtime {
   std::string last_error;
 
   std::vector<SlotHot> hot;
+  // phase-1 key per slot: (gen << 32) | (grp << 1) | ok, ok = a local SCAL
+  // target (live, not partitioned or blocked, has device storage, this rank);
+  // rebuilt by scal_run_parallel when any SlotHot changed (key_dirty)
+  std::vector<uint64_t> key;
+  bool key_dirty = true;
   std::vector<Slot> slots;
   std::vector<DepState> deps;
   std::map<uint32_t, std::vector<uint32_t>> free_ranges;        // count -> starts
@@ -167,8 +172,8 @@ struct bt_runtime {
   Builder builder;
   std::unique_ptr<Pool> pool;
   std::vector<Lane> lanes;
-  std::vector<vec<LaneEntry>> buckets;                  // [chunk][round * P + lane]
-  std::vector<vec<uint32_t>> bucket_tasks;              // task indices (record_tasks only)
+  std::vector<vec<RunRec>> runs;                        // [chunk][round * P + lane]: runs of the stream
+  std::vector<uint64_t> run_tasks;                      // [chunk][round * P + lane]: tasks in those runs
   int npool = 1;
   int nrounds = 1;        // bucket rounds (max over round policies)
   int rounds_default = 1; // rounds of a partition of device-resident data
@@ -267,11 +272,13 @@ uint32_t alloc_slots(bt_runtime *rt, uint32_t count) {
     it->second.pop_back();
   } else {
     s = (uint32_t)rt->hot.size();
+    rt->key_dirty = true;
     rt->hot.resize(s + count);
     rt->slots.resize(s + count);
     rt->deps.resize(s + count);
   }
   for (uint32_t i = 0; i < count; ++i) {
+    rt->key_dirty = true;
     SlotHot &h = rt->hot[s + i];
     const uint32_t gen = h.gen;
     h = SlotHot();
@@ -287,6 +294,7 @@ uint32_t alloc_slots(bt_runtime *rt, uint32_t count) {
 
 void free_slots(bt_runtime *rt, uint32_t s, uint32_t count) {
   for (uint32_t i = 0; i < count; ++i) {
+    rt->key_dirty = true;
     SlotHot &h = rt->hot[s + i];
     h.flags = 0;
     if (++h.gen == 0) h.gen = 1;
@@ -300,6 +308,7 @@ void set_blocked(bt_runtime *rt, uint32_t s, bool on) {
   while (!stack.empty()) {
     const uint32_t x = stack.back();
     stack.pop_back();
+    rt->key_dirty = true;
     if (on) rt->hot[x].flags |= F_BLOCKED;
     else rt->hot[x].flags &= ~F_BLOCKED;
     const Slot &sl = rt->slots[x];
@@ -805,8 +814,8 @@ int bt_init(const bt_config *cfg_in, bt_runtime **out) {
   rt->rounds_default = cfg.pipeline_rounds;
   rt->nrounds = std::max(cfg.pipeline_rounds, cfg.pipeline_rounds > 1 ? kRoundsUploading : 1);
   rt->lanes.resize((size_t)threads * rt->nrounds);                  // [(round - first round of the launch) * P + lane]
-  rt->buckets.resize((size_t)threads * threads * rt->nrounds);      // [chunk][round * P + lane]
-  rt->bucket_tasks.resize(rt->buckets.size());
+  rt->runs.resize((size_t)threads * threads * rt->nrounds);         // [chunk][round * P + lane]
+  rt->run_tasks.assign(rt->runs.size(), 0);
 
   if (!rt->host_only) {
     int ndev = 0;
@@ -978,6 +987,7 @@ int bt_vector_data_register(bt_runtime *rt, bt_handle *out, int home_node, void 
     }
   }
   const uint32_t s = alloc_slots(rt, 1);
+  rt->key_dirty = true;
   SlotHot &sh = rt->hot[s];
   Slot &sl = rt->slots[s];
   sl.root = s;
@@ -1035,6 +1045,7 @@ int bt_data_partition(bt_runtime *rt, bt_handle h, uint32_t nparts) {
   if (acquired_chain(rt, s)) return fail(rt, -EBUSY, "handle is acquired");
   if (nparts == 0 || nparts > rt->hot[s].nx) return fail(rt, -EINVAL, "bad number of parts");
   const uint32_t c0 = alloc_slots(rt, nparts);   // may reallocate the slot arrays
+  rt->key_dirty = true;
   SlotHot &ph = rt->hot[s];
   Slot &p = rt->slots[s];
   const uint64_t base = ph.nx / nparts, extra = ph.nx % nparts;
@@ -1046,6 +1057,7 @@ int bt_data_partition(bt_runtime *rt, bt_handle h, uint32_t nparts) {
     if (it != rt->caches.end() && !it->second.uploads.empty() && rounds > 1) rounds = (uint32_t)rt->nrounds;
   }
   for (uint32_t t = 0; t < nparts; ++t) {
+    rt->key_dirty = true;
     SlotHot &ch = rt->hot[c0 + t];
     Slot &c = rt->slots[c0 + t];
     const uint64_t off = t * base + std::min<uint64_t>(t, extra);
@@ -1105,6 +1117,7 @@ int bt_data_unpartition(bt_runtime *rt, bt_handle h) {
   free_slots(rt, p.first_child, p.nparts);
   p.nparts = 0;
   p.first_child = NONE;
+  rt->key_dirty = true;
   rt->hot[s].flags &= ~F_PARTITIONED;
   return 0;
 }
@@ -1118,6 +1131,7 @@ int bt_data_set_rank(bt_runtime *rt, bt_handle h, int rank) {
   while (!stack.empty()) {
     uint32_t x = stack.back();
     stack.pop_back();
+    rt->key_dirty = true;
     rt->hot[x].rank = rank;
     const Slot &sl = rt->slots[x];
     for (uint32_t t = 0; t < sl.nparts; ++t) stack.push_back(sl.first_child + t);
@@ -1291,35 +1305,63 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
   const uint64_t tbase = B.ntasks;
   const bool record = B.record_tasks;
   double tp0 = now_ms();
+  if (rt->key_dirty || rt->key.size() != nslots) {
+    rt->key.resize(nslots);
+    uint64_t *key = rt->key.data();
+    auto fill = [&](int c) {
+      size_t lo, hi;
+      range_of(nslots, nslots >= 65536 ? P : 1, c, lo, hi);
+      for (size_t x = lo; x < hi; ++x) {
+        const SlotHot &sh = hot[x];
+        const bool ok = (sh.flags & (F_LIVE | F_PARTITIONED | F_BLOCKED)) == F_LIVE && (sh.dptr || host_only) &&
+                        sh.rank == myrank;
+        key[x] = ((uint64_t)sh.gen << 32) | ((uint64_t)(sh.grp & 0x7FFFFFFFu) << 1) | (ok ? 1u : 0u);
+      }
+    };
+    if (nslots >= 65536) rt->par(fill);
+    else fill(0);
+    rt->key_dirty = false;
+  }
+  const uint64_t *kt = rt->key.data();
   std::vector<double> tstart(P), tend(P), tloop(P);
   rt->par([&](int c) {
     if (dbg) tstart[c] = now_ms();
     size_t lo, hi;
     range_of(n, P, c, lo, hi);
-    // this chunk's buckets, moved to the stack while filling (no false sharing
-    // of vector headers between threads)
-    std::vector<vec<LaneEntry>> mine(G);
-    std::vector<vec<uint32_t>> mine_t(record ? G : 0);
+    // this chunk's run lists, moved to the stack while filling (no false
+    // sharing of vector headers between threads); phase 1 writes only run
+    // records (one per change of group along the stream), not the tasks:
+    // the lanes read their tasks' handles and factors from the caller's
+    // arrays in phase 2, so phase 1 (which every launch waits for) reads
+    // codelets + handles once and writes almost nothing
+    std::vector<vec<RunRec>> mine(G);
+    std::vector<uint64_t> cnt(G, 0);
     for (uint32_t g = 0; g < G; ++g) {
-      mine[g].swap(rt->buckets[(size_t)c * G + g]);
+      mine[g].swap(rt->runs[(size_t)c * G + g]);
       mine[g].clear();
-      if (record) {
-        mine_t[g].swap(rt->bucket_tasks[(size_t)c * G + g]);
-        mine_t[g].clear();
-      }
     }
     struct Restore {
-      std::vector<vec<LaneEntry>> &m;
-      std::vector<vec<uint32_t>> &mt;
+      std::vector<vec<RunRec>> &m;
+      std::vector<uint64_t> &cnt;
       bt_runtime *rt;
       int c;
       uint32_t G;
       ~Restore() {
-        for (uint32_t g = 0; g < G; ++g) m[g].swap(rt->buckets[(size_t)c * G + g]);
-        for (uint32_t g = 0; g < (uint32_t)mt.size(); ++g) mt[g].swap(rt->bucket_tasks[(size_t)c * G + g]);
+        for (uint32_t g = 0; g < G; ++g) {
+          m[g].swap(rt->runs[(size_t)c * G + g]);
+          rt->run_tasks[(size_t)c * G + g] = cnt[g];
+        }
       }
-    } restore{mine, mine_t, rt, c, G};
+    } restore{mine, cnt, rt, c, G};
     uint64_t rem = 0;
+    uint32_t cur = NONE;      // group of the open run
+    size_t run0 = lo;         // its first task
+    auto close_run = [&](size_t j) {
+      if (cur == NONE) return;
+      mine[cur].push_back(RunRec{(uint32_t)run0, (uint32_t)(j - run0)});
+      cnt[cur] += j - run0;
+      cur = NONE;
+    };
     if (dbg) tloop[c] = now_ms();
     for (size_t j = lo; j < hi; ++j) {
       const bt_handle h = h0[i0 + j];
@@ -1328,28 +1370,28 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
         bad[c] = 1;
         return;
       }
-      const SlotHot &sh = hot[s];
-      if (__builtin_expect(sh.gen != (uint32_t)(h >> 32) ||
-                               (sh.flags & (F_LIVE | F_PARTITIONED | F_BLOCKED)) != F_LIVE ||
-                               (!sh.dptr && !host_only),
-                           0)) {
-        bad[c] = 1;
-        return;
-      }
-      if (__builtin_expect(sh.rank != myrank, 0)) {
-        if (sh.rank < 0) {
+      const uint64_t k = kt[s];
+      if (__builtin_expect(((k >> 32) != (h >> 32)) | !(k & 1u), 0)) {
+        // not a local SCAL target: a stale handle or a bad state (the run
+        // fails), or another rank's tile (skipped)
+        const SlotHot &sh = hot[s];
+        if (sh.gen != (uint32_t)(h >> 32) || (sh.flags & (F_LIVE | F_PARTITIONED | F_BLOCKED)) != F_LIVE ||
+            (!sh.dptr && !host_only) || sh.rank == myrank || sh.rank < 0) {
           bad[c] = 1;
           return;
         }
+        close_run(j);
         ++rem;
         continue;
       }
-      LaneEntry e;
-      e.slot = s;
-      memcpy(&e.fbits, &scalars[i0 + j], 4);
-      mine[sh.grp].push_back(e);
-      if (record) mine_t[sh.grp].push_back((uint32_t)(tbase + j));
+      const uint32_t g = (uint32_t)k >> 1;
+      if (g != cur) {
+        close_run(j);
+        cur = g;
+        run0 = j;
+      }
     }
+    close_run(hi);
     remote[c] = rem;
     if (dbg) tend[c] = now_ms();
   });
@@ -1396,7 +1438,7 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
   size_t local = 0;
   for (int c = 0; c < P; ++c)
     for (int r = 0; r < R; ++r)
-      for (int l = 0; l < P; ++l) round_size[r] += rt->buckets[(size_t)c * G + (size_t)r * P + l].size();
+      for (int l = 0; l < P; ++l) round_size[r] += rt->run_tasks[(size_t)c * G + (size_t)r * P + l];
   for (int r = 0; r < R; ++r) local += round_size[r];
   // launches: adjacent rounds are merged so that each launch carries at least
   // pipeline_min / 2 local tasks (a short run -- e.g. one rank's shard -- is
@@ -1431,17 +1473,32 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
       // this lane builds its groups of every round of the launch in one go
       for (int r = rlo; r < rhi; ++r) {
         const uint32_t g = (uint32_t)(r * P + l);
-        std::vector<const LaneEntry *> ptrs(P);
-        std::vector<const uint32_t *> tptr(P);
-        std::vector<size_t> cnts(P);
-        for (int c = 0; c < P; ++c) {
-          ptrs[c] = rt->buckets[(size_t)c * G + g].data();
-          tptr[c] = record ? rt->bucket_tasks[(size_t)c * G + g].data() : nullptr;
-          cnts[c] = rt->buckets[(size_t)c * G + g].size();
-        }
         Lane &L = rt->lanes[(size_t)(r - rlo) * P + l];
+        // gather this group's tasks from the batch, in stream order
+        size_t m = 0;
+        for (int c = 0; c < P; ++c) m += rt->run_tasks[(size_t)c * G + g];
+        L.gather.resize(m);
+        if (record) L.gtask.resize(m);
+        LaneEntry *ge = L.gather.data();
+        uint32_t *gt = L.gtask.data();
+        size_t q = 0;
+        for (int c = 0; c < P; ++c)
+          for (const RunRec &run : rt->runs[(size_t)c * G + g]) {
+            const bt_handle *hh = h0 + i0 + run.start;
+            const float *ff = scalars + i0 + run.start;
+            for (uint32_t j = 0; j < run.len; ++j) {
+              ge[q + j].slot = (uint32_t)(hh[j] & 0xFFFFFFFFull) - 1u;
+              memcpy(&ge[q + j].fbits, &ff[j], 4);
+            }
+            if (record)
+              for (uint32_t j = 0; j < run.len; ++j) gt[q + j] = (uint32_t)(tbase + run.start + j);
+            q += run.len;
+          }
+        const LaneEntry *ptrs[1] = {ge};
+        const uint32_t *tptr[1] = {record ? gt : nullptr};
+        const size_t cnts[1] = {m};
         B.lane_runs(
-            L, ptrs.data(), tptr.data(), cnts.data(), P, deps, nlocal,
+            L, ptrs, tptr, cnts, 1, deps, nlocal,
             [bl = blk_local.data()](uint32_t s) { return bl[s >> 6] + (s & 63); },
             [up = (uint32_t)P, ul = (uint32_t)l](uint32_t loc) { return ((loc >> 6) * up + ul) * 64 + (loc & 63); },
             [hot](uint32_t s) {
@@ -1636,6 +1693,7 @@ int bt_data_unregister(bt_runtime *rt, bt_handle h) {
   uint32_t s = resolve(rt, h);
   if (s == NONE) return fail(rt, -ENOENT, "attempt to use unregistered pointer");
   Slot &sl = rt->slots[s];
+  rt->key_dirty = true;
   SlotHot &sh = rt->hot[s];
   if (sl.parent != NONE) return fail(rt, -EBUSY, "cannot unregister a sub-handle");
   if (sl.nparts) return fail(rt, -EBUSY, "unpartition before unregistering");
