@@ -415,31 +415,39 @@ def main():
         # roofline of the dominant kernel (the persistent scheduler kernel; a step is
         # `launches_per_step` launches -- the pipelined rounds -- on two streams):
         # fused chain of S multiplies per element -> FP32-multiply bound when S exceeds the ridge.
-        # achieved = rank 0's algorithmic work per step / its device time per step (first launch
-        # start -> last launch end, CUDA events), i.e. per-launch work / per-launch share.
+        # achieved = algorithmic work per launch / the kernel's average launch duration (CUDA
+        # events recorded around each launch on its own stream); adjacent rounds' launches
+        # overlap by their tails, so the per-launch share of the step's device span
+        # (first launch start -> last launch end) is reported beside it.
         per_launch_elems = elems / launches_per_step
         fmul = per_launch_elems * S
-        kern_ms = span_ms / launches_per_step
+        avg_launch = st["device_ms"] / max(1, st["epochs"])
+        share_ms = span_ms / launches_per_step
         alu_peak = SM_COUNT * FP32_LANES_PER_SM * (peaks.get("sm_max_mhz") or 1965.0) * 1e6 / 1e12
         hbm_bytes = 8.0 * per_launch_elems
         t_alu = fmul / (alu_peak * 1e12)
         t_hbm = hbm_bytes / (peaks["hbm_gbs"] * 1e9)
         fused = not args.no_fusion
         if fused and t_alu > t_hbm:
-            roof = {"bound": "alu", "achieved": fmul / (kern_ms * 1e-3) / 1e12, "peak": alu_peak,
+            work, scale = fmul, 1e12
+            roof = {"bound": "alu", "peak": alu_peak,
                     "unit": "TFMUL/s", "peak_source": f"{SM_COUNT} SMs x {FP32_LANES_PER_SM} FP32 lanes x "
                                                      f"{peaks.get('sm_max_mhz')} MHz (DESIGN.md)"}
         else:
-            b = hbm_bytes if fused else 8.0 * per_launch_elems * S
-            roof = {"bound": "hbm", "achieved": b / (kern_ms * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+            work, scale = (hbm_bytes if fused else 8.0 * per_launch_elems * S), 1e9
+            roof = {"bound": "hbm", "peak": peaks["hbm_gbs"],
                     "unit": "GB/s", "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
+        roof["achieved"] = work / (avg_launch * 1e-3) / scale
         roof["frac"] = roof["achieved"] / roof["peak"]
-        roof["kernel"] = "bt::scheduler_kernel"
-        roof["kernel_ms"] = kern_ms
+        roof["kernel"] = "bt::scheduler_kernel_sw"
+        roof["avg_launch_ms"] = avg_launch
+        roof["work_per_launch"] = work
         roof["launches_per_step"] = launches_per_step
         roof["device_span_ms_per_step"] = span_ms
-        roof["avg_launch_ms"] = st["device_ms"] / max(1, st["epochs"])
-        roof["hbm_GBps_physical_min"] = hbm_bytes / (kern_ms * 1e-3) / 1e9
+        roof["span_share_ms"] = share_ms
+        roof["achieved_span_share"] = work / (share_ms * 1e-3) / scale
+        roof["frac_span_share"] = roof["achieved_span_share"] / roof["peak"]
+        roof["hbm_GBps_physical"] = hbm_bytes / (avg_launch * 1e-3) / 1e9
         roof["traffic"] = None
         try:
             with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:

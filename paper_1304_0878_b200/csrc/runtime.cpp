@@ -734,7 +734,11 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   return 0;
 }
 
+double g_wait_return_ms = 0;   // BT_DEBUG_TIMING: host time the last wait_all returned
+
 int wait_all(bt_runtime *rt) {
+  static const bool dbg = getenv("BT_DEBUG_TIMING") != nullptr;
+  const double w0 = dbg ? now_ms() : 0;
   if (int r = flush_epoch(rt)) return r;
   if (rt->span_open) CUDA_TRY(rt, cudaEventRecord(rt->span_end, rt->stream));
   // retire in launch order (older first)
@@ -745,7 +749,9 @@ int wait_all(bt_runtime *rt) {
     if (!next) break;
     if (int r = retire(rt, *next)) return r;
   }
+  const double w1 = dbg ? now_ms() : 0;
   CUDA_TRY(rt, cudaStreamSynchronize(rt->stream));
+  const double w2 = dbg ? now_ms() : 0;
   for (auto &kv2 : rt->caches) {   // every epoch that needed an upload chunk has run
     for (const UploadChunk &u : kv2.second.uploads) {
       CUDA_TRY(rt, cudaEventSynchronize(u.ev));
@@ -757,6 +763,11 @@ int wait_all(bt_runtime *rt) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, rt->span_start, rt->span_end) == cudaSuccess) rt->stats.device_span_ms += ms;
     rt->span_open = false;
+  }
+  if (dbg) {
+    g_wait_return_ms = now_ms();
+    fprintf(stderr, "wait_all: retire %.3f ms, stream sync %.3f ms, rest %.3f ms\n", w1 - w0, w2 - w1,
+            g_wait_return_ms - w2);
   }
   return 0;
 }
@@ -1305,6 +1316,7 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
   const uint64_t tbase = B.ntasks;
   const bool record = B.record_tasks;
   double tp0 = now_ms();
+  if (dbg && g_wait_return_ms > 0) fprintf(stderr, "scal_run_parallel: %.3f ms after the last wait returned\n", tp0 - g_wait_return_ms);
   if (rt->key_dirty || rt->key.size() != nslots) {
     rt->key.resize(nslots);
     uint64_t *key = rt->key.data();
