@@ -211,6 +211,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-fusion", action="store_true", help="unfused (scheduler-bound) variant")
+    ap.add_argument("--no-stream", action="store_true",
+                    help="one launch per pipelined round instead of one stream launch per step (comparison)")
     ap.add_argument("--sweeps", type=int, default=C5["sweeps"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--skip-cpu", action="store_true")
@@ -281,7 +283,7 @@ def main():
     factors = W.sweep_factors(np.random.default_rng(W.SEED_BASE + 4), S)
 
     stream = torch.cuda.current_stream(dev)
-    flags = B.BT_FLAG_NO_FUSION if args.no_fusion else 0
+    flags = (B.BT_FLAG_NO_FUSION if args.no_fusion else 0) | (B.BT_FLAG_NO_STREAM if args.no_stream else 0)
     # builder threads: share the node's cores among the ranks on it, leaving two per rank
     threads = args.host_threads or max(1, min(16, (os.cpu_count() or 2) // int(
         os.environ.get("LOCAL_WORLD_SIZE", "1")) - 2))
@@ -314,8 +316,9 @@ def main():
         torch.cuda.synchronize(dev)
     ms = ev0.elapsed_time(ev1) / args.steps
     st = rt.stats()
-    launches_per_step = st["epochs"] / args.steps
-    kern_ms = st["device_ms"] / max(1, st["epochs"])            # average launch duration
+    launches_per_step = st["sched_launches"] / args.steps          # scheduler-kernel launches
+    epochs_per_step = st["epochs"] / args.steps                    # rounds (sub-epochs of a stream launch)
+    kern_ms = st["device_ms"] / max(1, st["sched_launches"])       # average launch duration
     span_ms = st["device_span_ms"] / args.steps                  # device time per step (launches overlap)
     host_ms = st["host_build_ms"] / args.steps
     ms, kern_ms_max, host_ms_max, span_ms_max = allreduce_max([ms, kern_ms, host_ms, span_ms])
@@ -362,7 +365,7 @@ def main():
         torch.cuda.synchronize(dev)
         st16 = rt.stats()
         hbm16 = allreduce_max([eh0.elapsed_time(eh1) / k16, st16["device_span_ms"] / k16,
-                               st16["device_ms"] / max(1, st16["epochs"])]) + [k16, st16["epochs"] / k16]
+                               st16["device_ms"] / max(1, st16["sched_launches"])]) + [k16, st16["sched_launches"] / k16]
 
     rt.unpartition(h)
     rt.unregister(h)
@@ -412,8 +415,9 @@ def main():
         compulsory = 8.0 * total_elems                     # read + write each element once per step
         value = compulsory / (ms * 1e-3) / 1e9
         clocks = clk.summary()
-        # roofline of the dominant kernel (the persistent scheduler kernel; a step is
-        # `launches_per_step` launches -- the pipelined rounds -- on two streams):
+        # roofline of the dominant kernel (the persistent scheduler kernel; a step is one
+        # stream launch whose sub-epochs are the pipelined rounds, or with --no-stream one
+        # launch per round on two streams):
         # fused chain of S multiplies per element -> FP32-multiply bound when S exceeds the ridge.
         # achieved = algorithmic work per launch / the kernel's average launch duration (CUDA
         # events recorded around each launch on its own stream); adjacent rounds' launches
@@ -421,7 +425,7 @@ def main():
         # (first launch start -> last launch end) is reported beside it.
         per_launch_elems = elems / launches_per_step
         fmul = per_launch_elems * S
-        avg_launch = st["device_ms"] / max(1, st["epochs"])
+        avg_launch = st["device_ms"] / max(1, st["sched_launches"])
         share_ms = span_ms / launches_per_step
         alu_peak = SM_COUNT * FP32_LANES_PER_SM * (peaks.get("sm_max_mhz") or 1965.0) * 1e6 / 1e12
         hbm_bytes = 8.0 * per_launch_elems
@@ -439,10 +443,12 @@ def main():
                     "unit": "GB/s", "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})"}
         roof["achieved"] = work / (avg_launch * 1e-3) / scale
         roof["frac"] = roof["achieved"] / roof["peak"]
-        roof["kernel"] = "bt::scheduler_kernel_sw"
+        roof["kernel"] = ("bt::scheduler_kernel_sws (stream launch: the step's rounds are sub-epochs of one launch)"
+                          if launches_per_step < epochs_per_step else "bt::scheduler_kernel_sw")
         roof["avg_launch_ms"] = avg_launch
         roof["work_per_launch"] = work
         roof["launches_per_step"] = launches_per_step
+        roof["epochs_per_step"] = epochs_per_step
         roof["device_span_ms_per_step"] = span_ms
         roof["span_share_ms"] = share_ms
         roof["achieved_span_share"] = work / (share_ms * 1e-3) / scale

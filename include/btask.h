@@ -53,7 +53,8 @@
 extern "C" {
 #endif
 
-#define BT_ABI_VERSION 2   /* 2: bt_stats.kernel_launches, BT_FLAG_KERNEL_* */
+#define BT_ABI_VERSION 3   /* 2: bt_stats.kernel_launches, BT_FLAG_KERNEL_*; 3: bt_stats.sched_launches,
+                               BT_FLAG_NO_STREAM */
 
 typedef struct bt_runtime bt_runtime;
 typedef uint64_t bt_handle;
@@ -80,6 +81,8 @@ enum {
   BT_FLAG_HOST_ONLY  = 1u << 1, /* no GPU: analyse only (bt_dag_snapshot); nothing executes */
   BT_FLAG_TIMESTAMPS = 1u << 2, /* record %globaltimer per work unit (bt_trace) */
   BT_FLAG_SYNC_EPOCH = 1u << 3, /* debugging: synchronise after every epoch launch */
+  BT_FLAG_NO_STREAM  = 1u << 4, /* one launch per pipelined round instead of one stream launch per
+                                   run ("Stream launches"); for comparisons */
   /* testing: force one scheduler variant for every epoch instead of the
    * per-epoch choice (DESIGN.md section "Persistent scheduler kernels"); at
    * most one of the three may be set (-EINVAL otherwise) */
@@ -268,6 +271,8 @@ typedef struct bt_stats {
   uint32_t grid;              /* persistent CTAs of the last launch */
   uint32_t block;             /* threads per CTA of the last launch */
   uint64_t kernel_launches;   /* this library's kernel launches (per epoch: set-up + scheduler) */
+  uint64_t sched_launches;    /* of which scheduler-kernel launches (a stream launch runs several epochs);
+                                 device_ms / sched_launches = average launch duration */
 } bt_stats;
 int bt_stats_get(bt_runtime *rt, bt_stats *out);
 int bt_stats_reset(bt_runtime *rt);

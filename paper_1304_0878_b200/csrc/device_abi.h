@@ -64,6 +64,32 @@ struct EpochArgs {
   uint64_t chunk_elems;         // elements per unit (multiple of 8)
   uint64_t watchdog_ns;         // spin limit before declaring ERR_WATCHDOG
   uint32_t nitems;
+  unsigned *stream_abort;       // stream launch: the launch-wide abort flag (StreamCtl::abort), else null
 };
+
+// ---- stream launch (one persistent launch consumes a growing
+// sequence of sub-epochs) ----------------------------------------------------
+// The pipelined rounds of one SCAL run are sub-epochs of ONE launch of the
+// "sw" kernel: the host builds, uploads and publishes sub-epoch r while the
+// kernel already runs sub-epochs < r.  Sub-epochs are independent (disjoint
+// handles; everything they depend on precedes the launch in stream order), so
+// a CTA only needs to know which sub-epoch a queue ticket falls in: tickets
+// are taken from one launch-wide counter and sub-epoch r owns tickets
+// [base_r, base_r + total_units_r) with base_r = sum of the earlier subs'
+// units.  The host publishes sub-epoch r by copying its EpochArgs into
+// subs[r] and then r + 1 into `published` (two stream-ordered copies after
+// the copy of its blob); the kernel reads subs[r] only after observing
+// published > r with ld.acquire.
+constexpr int kMaxSubs = 16;
+struct alignas(64) StreamCtl {
+  unsigned long long ticket;    // next launch-wide ticket
+  unsigned published;           // sub-epochs whose args and blobs are in device memory
+  unsigned abort;               // any sub-epoch's fault stops every CTA
+  unsigned exited;              // CTAs that left the kernel
+  unsigned nsub;                // sub-epochs of this launch (fixed at its start)
+  unsigned pad[10];
+  EpochArgs subs[kMaxSubs];
+};
+static_assert(sizeof(StreamCtl) % 64 == 0, "StreamCtl layout");
 
 }  // namespace bt

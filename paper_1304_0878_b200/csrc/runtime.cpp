@@ -30,6 +30,7 @@
 
 namespace bt {
 cudaError_t launch_epoch(const EpochArgs &args, int grid, cudaStream_t stream, int kernel);
+cudaError_t launch_stream(StreamCtl *ctl, uint64_t watchdog_ns, int grid, cudaStream_t stream, bool prefetch);
 cudaError_t scheduler_occupancy(int *blocks_per_sm, int *block);
 cudaError_t scheduler_occupancy_wq(int *blocks_per_sm, int *block);
 cudaError_t launch_stage(void *dst, const void *src_mapped, size_t bytes, unsigned long long *q_empty, size_t nq,
@@ -114,6 +115,7 @@ struct EpochBuf {
   uint64_t seq = 0;           // launch order
   uint64_t units = 0;
   bool traced = false;
+  bool timed = true;          // start/end bracket a launch (false: a later sub-epoch of a stream launch)
   Counters *hctr = nullptr;     // mapped pinned: written by the kernel's last CTA
   Counters *hctr_dev = nullptr;
   size_t trace_off_h = 0;     // offset of the trace copy in hblob
@@ -180,6 +182,17 @@ struct bt_runtime {
   EpochBuf ep[kEpochRing];
   uint64_t ep_seq = 0;
   cudaStream_t rstream[2] = {nullptr, nullptr};   // round streams (pipelined SCAL runs)
+  // stream launch (device_abi.h StreamCtl): the rounds of one
+  // pipelined SCAL run as sub-epochs of one "sw" launch.  want: the run asks
+  // for it (decided at its first flush); active: sub-epochs next..nsub-1 join
+  // the running launch
+  StreamCtl *sctl = nullptr;
+  struct {
+    bool want = false, active = false;
+    unsigned nsub = 0, next = 0;
+    bool prefetch = false;
+  } sl;
+  cudaEvent_t ev_pub0 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_round[2] = {nullptr, nullptr};
   cudaEvent_t span_start = nullptr, span_end = nullptr;
   bool span_open = false;
@@ -378,7 +391,7 @@ int retire(bt_runtime *rt, EpochBuf &e) {
   e.inflight = false;
   if (err != cudaSuccess) return cuda_fail(rt, err, "epoch completion");
   float ms = 0.f;
-  if (cudaEventElapsedTime(&ms, e.start, e.end) == cudaSuccess) rt->stats.device_ms += ms;
+  if (e.timed && cudaEventElapsedTime(&ms, e.start, e.end) == cudaSuccess) rt->stats.device_ms += ms;
   const Counters *c = e.hctr;
   if (c->error != ERR_NONE) {
     rt->poisoned = -EIO;
@@ -513,8 +526,39 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     tot.ahi = std::max(tot.ahi, acc[p].ahi);
   }
   const uint64_t U = tot.units, U0 = tot.ready, F = tot.fac;
+  const bool traced = (rt->cfg.flags & BT_FLAG_TIMESTAMPS) != 0;
   if (tot.succ != E) return fail(rt, -EIO, "internal: successor count mismatch");
 
+  // scheduler variant (DESIGN.md, "Persistent scheduler kernels")
+  static const char *kv = getenv("BT_KERNEL");   // "sw" / "rw" / "wq": experiments only
+  // work per unit = elements x chained multiplies
+  const uint64_t avg_work = (sampled_work / cnt * N) / std::max<uint64_t>(1, U);
+  // units of at most 16 KiB: one warp per unit ("wq", many units in flight)
+  const uint64_t avg_elems = (sampled / cnt * N) / std::max<uint64_t>(1, U);
+  // ... when the epoch is wide: a narrow one (few initially ready units, e.g.
+  // a 1-wide dependency chain) is latency-bound, and the CTA-wide "rw" kernel
+  // runs chains in its slots with the shortest dependency latency
+  const bool wide = U0 * 4 >= (uint64_t)rt->grid_wq * 8;
+  // units above 16 KiB: CTA-wide bodies with one scheduler warp ("sw"; C3
+  // with 64 KiB units: 14.1 ms vs 14.7 ms on "rw", tools/c3_chunks.py); epochs
+  // of short chains (average k below the FP32/HBM ridge) are HBM-bound and
+  // use the instance whose bodies prefetch the next step's data
+  const bool prefetch = avg_work < kPrefetchBelowK * avg_elems;
+  int kernel = avg_elems <= kWarpUnitMax ? (wide && rt->grid_wq > 0 ? 2 : 1) : prefetch ? 3 : 0;
+  if (kv) kernel = kv[0] == 'w' ? 2 : kv[0] == 'r' ? 1 : prefetch ? 3 : 0;
+  if (rt->cfg.flags & BT_FLAG_KERNEL_SW) kernel = prefetch ? 3 : 0;
+  if (rt->cfg.flags & BT_FLAG_KERNEL_RW) kernel = 1;
+  if ((rt->cfg.flags & BT_FLAG_KERNEL_WQ) && rt->grid_wq > 0) kernel = 2;
+  // stream launch: the run's first sub-epoch decides whether its rounds join
+  // one launch ("sw" kernels only; no tracing, no host-homed write-backs)
+  if (rt->sl.want) {
+    rt->sl.want = false;
+    rt->sl.active = (kernel == 0 || kernel == 3) && !traced && rt->caches.empty() &&
+                    !(rt->cfg.flags & BT_FLAG_SYNC_EPOCH) && rt->sctl && rt->sl.nsub >= 2;
+    rt->sl.next = 0;
+    rt->sl.prefetch = kernel == 3;
+  }
+  const bool sub = rt->sl.active;
   // device layout: ctr | items | pending | succ | factors | queue[U] | chunk_done[N] | trace
   const size_t o_ctr = 0;
   const size_t o_items = 64;
@@ -525,11 +569,16 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   const size_t upload = o_queue + 8 * U0;
   const size_t o_cdone = align_up(o_queue + 8 * U, 16);
   const size_t o_trace = align_up(o_cdone + 4 * N, 16);
-  const bool traced = (rt->cfg.flags & BT_FLAG_TIMESTAMPS) != 0;
   const size_t dneed = o_trace + (traced ? 36 * U : 0);
   const size_t o_readback = align_up(upload, 64);
   const size_t o_trace_h = o_readback + 64;
-  const size_t hneed = align_up(o_trace_h + (traced ? 36 * U : 0), 16);
+  // sub-epoch of a stream launch: the whole blob through chunk_done goes up by
+  // one copy (no set-up kernel), followed by its EpochArgs and the new
+  // `published` count, staged after the blob: [StreamCtl header | args | count]
+  const size_t o_sx_h = align_up(std::max(o_trace_h + (traced ? 36 * U : 0), o_cdone + 4 * N), 64);
+  const size_t o_args_h = o_sx_h + 64;
+  const size_t o_pub_h = align_up(o_args_h + sizeof(EpochArgs), 16);
+  const size_t hneed = sub ? o_pub_h + 16 : align_up(o_trace_h + (traced ? 36 * U : 0), 16);
   if (int r = ensure_host(rt, e, hneed)) return r;
   if (int r = ensure_dev(rt, e, dneed)) return r;
 
@@ -615,6 +664,84 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
 
   char *d = e.dblob;
   const double tC = now_ms();
+  if (!e.hctr) {
+    CUDA_TRY(rt, cudaHostAlloc((void **)&e.hctr, sizeof(Counters), cudaHostAllocMapped | cudaHostAllocPortable));
+    CUDA_TRY(rt, cudaHostGetDevicePointer((void **)&e.hctr_dev, e.hctr, 0));
+  }
+  memset(e.hctr, 0, sizeof(Counters));
+  EpochArgs a{};
+  a.items = reinterpret_cast<const DItem *>(d + o_items);
+  a.pending = reinterpret_cast<int32_t *>(d + o_pend);
+  a.chunk_done = reinterpret_cast<uint32_t *>(d + o_cdone);
+  a.succ = reinterpret_cast<const uint32_t *>(d + o_succ);
+  a.factors = reinterpret_cast<const float *>(d + o_fac);
+  a.queue = reinterpret_cast<unsigned long long *>(d + o_queue);
+  a.ctr = reinterpret_cast<Counters *>(d + o_ctr);
+  a.host_ctr = e.hctr_dev;
+  a.trace = traced ? reinterpret_cast<unsigned long long *>(d + o_trace) : nullptr;
+  a.trace_item = traced ? reinterpret_cast<uint32_t *>(d + o_trace + 32 * U) : nullptr;
+  a.total_units = U;
+  a.chunk_elems = CE;
+  a.watchdog_ns = kWatchdogNs;
+  a.nitems = (uint32_t)N;
+  a.stream_abort = sub ? &rt->sctl->abort : nullptr;
+  auto account = [&]() {
+    e.inflight = true;
+    e.seq = ++rt->ep_seq;
+    e.units = U;
+    e.traced = traced;
+    e.trace_off_h = o_trace_h;
+    rt->stats.items += N;
+    rt->stats.edges += E;
+    rt->stats.units += U;
+    rt->stats.epochs += 1;
+    rt->stats.upload_bytes += upload;
+    rt->stats.fused_tasks += B.fused;
+    B.next_epoch();
+    rt->stats.host_build_ms += now_ms() - t0;
+  };
+  if (sub) {
+    // ---- sub-epoch r of the run's stream launch (device_abi.h StreamCtl) ----
+    const unsigned r = rt->sl.next;
+    cudaStream_t ls = rt->rstream[0];                    // the launch
+    cudaStream_t up = r == 0 ? ls : rt->rstream[1];      // this sub-epoch's copies
+    if (!rt->span_open) {
+      CUDA_TRY(rt, cudaEventRecord(rt->span_start, ls));
+      rt->span_open = true;
+    }
+    // the launch is already running (r > 0): no set-up kernel, so the queue's
+    // unpublished slots read EMPTY and the chunk counters zero in the blob
+    for (uint64_t i = U0; i < U; ++i) q[i] = Q_EMPTY;
+    memset(h + o_cdone, 0, 4 * N);
+    memcpy(h + o_args_h, &a, sizeof a);
+    *reinterpret_cast<uint32_t *>(h + o_pub_h) = r + 1;
+    if (r == 0) {   // launch-wide header: ticket = published = abort = exited = 0, nsub
+      memset(h + o_sx_h, 0, 64);
+      *reinterpret_cast<uint32_t *>(h + o_sx_h + offsetof(StreamCtl, nsub)) = rt->sl.nsub;
+      CUDA_TRY(rt, cudaMemcpyAsync(rt->sctl, h + o_sx_h, 64, cudaMemcpyHostToDevice, up));
+    }
+    CUDA_TRY(rt, cudaMemcpyAsync(d, h, o_cdone + 4 * N, cudaMemcpyHostToDevice, up));
+    CUDA_TRY(rt, cudaMemcpyAsync(&rt->sctl->subs[r], h + o_args_h, sizeof(EpochArgs), cudaMemcpyHostToDevice, up));
+    CUDA_TRY(rt, cudaMemcpyAsync(&rt->sctl->published, h + o_pub_h, 4, cudaMemcpyHostToDevice, up));
+    if (r == 0) {
+      // later sub-epochs' copies follow the header reset
+      CUDA_TRY(rt, cudaEventRecord(rt->ev_pub0, ls));
+      CUDA_TRY(rt, cudaStreamWaitEvent(rt->rstream[1], rt->ev_pub0, 0));
+      CUDA_TRY(rt, cudaEventRecord(e.start, ls));
+      rt->stats.grid = (uint32_t)rt->grid_max;
+      rt->stats.block = (uint32_t)rt->block;
+      rt->stats.kernel_launches += 1;
+      rt->stats.sched_launches += 1;
+      CUDA_TRY(rt, launch_stream(rt->sctl, kWatchdogNs, rt->grid_max, ls, rt->sl.prefetch));
+      CUDA_TRY(rt, cudaEventRecord(e.end, ls));
+    }
+    CUDA_TRY(rt, cudaEventRecord(e.done, ls));   // after the launch: it ends once every sub-epoch ran
+    e.timed = r == 0;
+    if (++rt->sl.next == rt->sl.nsub) rt->sl.active = false;
+    account();
+    return 0;
+  }
+  e.timed = true;
   if (!rt->span_open) {
     CUDA_TRY(rt, cudaEventRecord(rt->span_start, stream));
     rt->span_open = true;
@@ -634,26 +761,6 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
                             reinterpret_cast<unsigned long long *>(d + o_queue) + U0, U - U0,
                             reinterpret_cast<uint32_t *>(d + o_cdone), N, stream));
 
-  EpochArgs a{};
-  a.items = reinterpret_cast<const DItem *>(d + o_items);
-  a.pending = reinterpret_cast<int32_t *>(d + o_pend);
-  a.chunk_done = reinterpret_cast<uint32_t *>(d + o_cdone);
-  a.succ = reinterpret_cast<const uint32_t *>(d + o_succ);
-  a.factors = reinterpret_cast<const float *>(d + o_fac);
-  a.queue = reinterpret_cast<unsigned long long *>(d + o_queue);
-  a.ctr = reinterpret_cast<Counters *>(d + o_ctr);
-  if (!e.hctr) {
-    CUDA_TRY(rt, cudaHostAlloc((void **)&e.hctr, sizeof(Counters), cudaHostAllocMapped | cudaHostAllocPortable));
-    CUDA_TRY(rt, cudaHostGetDevicePointer((void **)&e.hctr_dev, e.hctr, 0));
-  }
-  memset(e.hctr, 0, sizeof(Counters));
-  a.host_ctr = e.hctr_dev;
-  a.trace = traced ? reinterpret_cast<unsigned long long *>(d + o_trace) : nullptr;
-  a.trace_item = traced ? reinterpret_cast<uint32_t *>(d + o_trace + 32 * U) : nullptr;
-  a.total_units = U;
-  a.chunk_elems = CE;
-  a.watchdog_ns = kWatchdogNs;
-  a.nitems = (uint32_t)N;
   const int grid = (int)std::min<uint64_t>((uint64_t)rt->grid_max, U);
 
   // host-homed data this epoch touches must have arrived (chunked uploads)
@@ -664,28 +771,9 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
       if (u.lo < tot.ahi && tot.alo < u.hi) CUDA_TRY(rt, cudaStreamWaitEvent(stream, u.ev, 0));
   }
   CUDA_TRY(rt, cudaEventRecord(e.start, stream));
-  // scheduler variant (DESIGN.md, "Persistent scheduler kernels")
-  static const char *kv = getenv("BT_KERNEL");   // "sw" / "rw" / "wq": experiments only
-  // work per unit = elements x chained multiplies
-  const uint64_t avg_work = (sampled_work / cnt * N) / std::max<uint64_t>(1, U);
-  // units of at most 16 KiB: one warp per unit ("wq", many units in flight)
-  const uint64_t avg_elems = (sampled / cnt * N) / std::max<uint64_t>(1, U);
-  // ... when the epoch is wide: a narrow one (few initially ready units, e.g.
-  // a 1-wide dependency chain) is latency-bound, and the CTA-wide "rw" kernel
-  // runs chains in its slots with the shortest dependency latency
-  const bool wide = U0 * 4 >= (uint64_t)rt->grid_wq * 8;
-  // units above 16 KiB: CTA-wide bodies with one scheduler warp ("sw"; C3
-  // with 64 KiB units: 14.1 ms vs 14.7 ms on "rw", tools/c3_chunks.py); epochs
-  // of short chains (average k below the FP32/HBM ridge) are HBM-bound and
-  // use the instance whose bodies prefetch the next step's data
-  const bool prefetch = avg_work < kPrefetchBelowK * avg_elems;
-  int kernel = avg_elems <= kWarpUnitMax ? (wide && rt->grid_wq > 0 ? 2 : 1) : prefetch ? 3 : 0;
-  if (kv) kernel = kv[0] == 'w' ? 2 : kv[0] == 'r' ? 1 : prefetch ? 3 : 0;
-  if (rt->cfg.flags & BT_FLAG_KERNEL_SW) kernel = prefetch ? 3 : 0;
-  if (rt->cfg.flags & BT_FLAG_KERNEL_RW) kernel = 1;
-  if ((rt->cfg.flags & BT_FLAG_KERNEL_WQ) && rt->grid_wq > 0) kernel = 2;
   const int kgrid = kernel == 2 ? (int)std::min<uint64_t>((uint64_t)rt->grid_wq, (U + 7) / 8) : grid;
   rt->stats.grid = (uint32_t)kgrid;
+  rt->stats.sched_launches += 1;
   rt->stats.block = kernel == 2 ? (uint32_t)rt->block_wq : (uint32_t)rt->block;
   CUDA_TRY(rt, launch_epoch(a, kgrid, stream, kernel));
   CUDA_TRY(rt, cudaEventRecord(e.end, stream));
@@ -712,20 +800,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   }
   if (traced) CUDA_TRY(rt, cudaMemcpyAsync(h + o_trace_h, d + o_trace, 36 * U, cudaMemcpyDeviceToHost, stream));
   CUDA_TRY(rt, cudaEventRecord(e.done, stream));
-  e.inflight = true;
-  e.seq = ++rt->ep_seq;
-  e.units = U;
-  e.traced = traced;
-  e.trace_off_h = o_trace_h;
-
-  rt->stats.items += N;
-  rt->stats.edges += E;
-  rt->stats.units += U;
-  rt->stats.epochs += 1;
-  rt->stats.upload_bytes += upload;
-  rt->stats.fused_tasks += B.fused;
-  B.next_epoch();
-  rt->stats.host_build_ms += now_ms() - t0;
+  account();
   static const bool dbg = getenv("BT_DEBUG_TIMING") != nullptr;
   if (dbg)
     fprintf(stderr, "flush_epoch N=%zu E=%zu U=%llu upload=%zu B: passA %.3f passB %.3f csr %.3f launch %.3f ms\n", N, E,
@@ -900,6 +975,12 @@ int bt_init(const bt_config *cfg_in, bt_runtime **out) {
         delete rt;
         return -ENOMEM;
       }
+    if (!(cfg.flags & BT_FLAG_NO_STREAM) &&
+        (cudaMalloc((void **)&rt->sctl, sizeof(StreamCtl)) != cudaSuccess ||
+         cudaEventCreateWithFlags(&rt->ev_pub0, cudaEventDisableTiming) != cudaSuccess)) {
+      cudaGetLastError();
+      rt->sctl = nullptr;   // pipelined runs then launch once per round
+    }
     // keep freed replicas in the pool (register/unregister loops reuse them)
     cudaMemPool_t mp;
     if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
@@ -933,6 +1014,8 @@ int bt_shutdown(bt_runtime *rt) {
       if (rt->ev_round[i]) cudaEventDestroy(rt->ev_round[i]);
     }
     if (rt->ev_fork) cudaEventDestroy(rt->ev_fork);
+    if (rt->ev_pub0) cudaEventDestroy(rt->ev_pub0);
+    if (rt->sctl) cudaFree(rt->sctl);
     for (cudaEvent_t ev : rt->ev_free) cudaEventDestroy(ev);
     if (rt->h2d) cudaStreamDestroy(rt->h2d);
     if (rt->d2h) cudaStreamDestroy(rt->d2h);
@@ -1475,6 +1558,23 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
   }
   bound.push_back(R);
   const int launches = (int)bound.size() - 1;
+  // the rounds' epochs join one stream launch (if the first one's kernel
+  // choice allows it: flush_epoch); sl is reset however this run ends
+  struct SlReset {
+    bt_runtime *rt;
+    ~SlReset() { rt->sl.want = rt->sl.active = false; }
+  } sl_reset{rt};
+  if (pipelined && rt->sctl) {
+    unsigned nsub = 0;
+    for (int rr = 0; rr < launches; ++rr) {
+      size_t sz = 0;
+      for (int r = bound[rr]; r < bound[rr + 1]; ++r) sz += round_size[r];
+      nsub += sz != 0;
+    }
+    rt->sl.want = nsub >= 2 && nsub <= (unsigned)kMaxSubs;
+    rt->sl.active = false;
+    rt->sl.nsub = nsub;
+  }
   for (int rr = 0; rr < launches; ++rr) {
     const int rlo = bound[rr], rhi = bound[rr + 1];
     size_t sz = 0;

@@ -340,6 +340,7 @@ __device__ void copy_range(const float *x, float *y, uint64_t n, int tid) {
 __device__ __forceinline__ void raise_error(const EpochArgs &a, unsigned code) {
   atomicCAS(&a.ctr->error, 0u, code);
   atomicExch(&a.ctr->abort, 1u);
+  if (a.stream_abort) atomicExch(a.stream_abort, 1u);
 }
 
 // Pop the unit at ticket t (spinning until published), or kStop.
@@ -693,8 +694,11 @@ __device__ void scal_bulk(float *x, uint64_t nv, const float *sf, uint32_t k, in
 }
 #endif
 
-template <int C, int S, bool PF = false>
-__device__ __forceinline__ void compute_loop(const EpochArgs &a, const unsigned long long *s_unit,
+// STREAM: a stream launch; slot b's unit belongs to the sub-epoch whose
+// arguments the scheduler warp staged in s_args[b] (else every unit uses a0).
+template <int C, int S, bool PF = false, bool STREAM = false>
+__device__ __forceinline__ void compute_loop(const EpochArgs &a0, const EpochArgs *s_args,
+                                             const unsigned long long *s_unit,
                                              const DItem *s_item, float (*s_fac)[kMaxFactors], uint64_t *s_empty,
                                              int lane,
                                              float *s_bulk = nullptr, uint64_t *s_bulk_bar = nullptr,
@@ -709,6 +713,7 @@ __device__ __forceinline__ void compute_loop(const EpochArgs &a, const unsigned 
     bar_sync(kBarFull + b, 32 + C);   // FULL[b]: the pop warp + the compute warps
     const unsigned long long unit = s_unit[b];
     if (unit == kStop) break;
+    const EpochArgs &a = STREAM ? s_args[b] : a0;
 #if BT_TRACE_DETAIL
     if (s_cst && tid == 0 && a.trace) s_cst[b] = clock64();
 #endif
@@ -1237,12 +1242,176 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sw(Epoch
     }
   } else {
 #if BT_BULK
-    compute_loop<kCompute, kSlotsSW, PF>(a, s_unit, s_item, s_fac, s_empty, lane, &s_bulk[0][0][0], &s_bulk_bar[0][0]);
+    compute_loop<kCompute, kSlotsSW, PF>(a, nullptr, s_unit, s_item, s_fac, s_empty, lane, &s_bulk[0][0][0], &s_bulk_bar[0][0]);
 #else
-    compute_loop<kCompute, kSlotsSW, PF>(a, s_unit, s_item, s_fac, s_empty, lane);
+    compute_loop<kCompute, kSlotsSW, PF>(a, nullptr, s_unit, s_item, s_fac, s_empty, lane);
 #endif
   }
   report_exit(a);
+}
+
+// "sw" as a stream launch (StreamCtl, device_abi.h): the
+// pipelined rounds of one SCAL run are sub-epochs of this single launch, built
+// and published by the host while the kernel already runs the earlier ones.
+// Identical to "sw" except that the scheduler warp maps each launch-wide ticket
+// to (sub-epoch, position in its queue) and stages that sub-epoch's arguments
+// in shared memory next to the unit (s_args[slot]), where the compute warps
+// and the release path read them.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <bool PF>
+__global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sws(StreamCtl *ctl, uint64_t watchdog_ns) {
+  constexpr int kCompute = kComputeSW;
+  __shared__ unsigned long long s_unit[2];
+  __shared__ DItem s_item[2];
+  __shared__ __align__(8) uint64_t s_empty[2];
+  __shared__ __align__(16) float s_fac[2][kMaxFactors];
+  __shared__ __align__(16) EpochArgs s_args[2];
+  static_assert(sizeof(EpochArgs) % 8 == 0, "EpochArgs layout");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_empty[0], kCompute / 32);
+    mbar_init(&s_empty[1], kCompute / 32);
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    SlotState st[2];
+    for (int b = 0; b < 2; ++b) {
+      st[b].unit = kStop;
+      st[b].parity = 0;
+      st[b].unreleased = false;
+    }
+    int slot_sub[2] = {-1, -1};   // warp-uniform: the sub-epoch whose arguments s_args[b] holds
+    // lane 0: the sub-epoch this CTA's tickets have reached (tickets only grow)
+    const unsigned nsub = __ldcg(&ctl->nsub);
+    unsigned cur = 0, pub = 0;
+    unsigned long long base = 0, cur_units = ~0ull;   // ~0: not loaded yet
+    unsigned long long *cur_queue = nullptr;
+    uint32_t cur_nitems = 0;
+    for (unsigned u = 0;; ++u) {
+      const int b = u & 1;
+      unsigned long long unit = kStop;
+      unsigned sub = 0;
+      if (lane == 0) {
+        drain_slot(s_args[b], st[b], &s_empty[b]);   // slot b's previous unit (u-2), with its sub-epoch's args
+        const unsigned long long t = atomicAdd(&ctl->ticket, 1ull);
+        bool stop = false;
+        uint64_t start = 0;
+        // the sub-epoch holding ticket t (waiting for its publication)
+        for (unsigned spin = 0;;) {
+          if (cur >= nsub) {
+            stop = true;
+            break;
+          }
+          if (cur >= pub) {
+            pub = ld_acquire_u32(&ctl->published);
+            if (cur >= pub) {
+              if (spin == 0) start = globaltimer();
+              poll_slot(s_args[b ^ 1], st[b ^ 1], &s_empty[b ^ 1]);
+              __nanosleep(spin < 64 ? 64 : 512);
+              if ((++spin & 63) == 0) {
+                if (ld_relaxed_u32(&ctl->abort) || globaltimer() - start > watchdog_ns) {
+                  atomicExch(&ctl->abort, 1u);   // the host sees the unfinished sub-epochs
+                  stop = true;
+                  break;
+                }
+              }
+              continue;
+            }
+          }
+          if (cur_units == ~0ull) {   // read past ld.acquire(published), L2 only
+            cur_units = __ldcg(&ctl->subs[cur].total_units);
+            cur_queue = reinterpret_cast<unsigned long long *>(
+                __ldcg(reinterpret_cast<const unsigned long long *>(&ctl->subs[cur].queue)));
+            cur_nitems = __ldcg(&ctl->subs[cur].nitems);
+          }
+          if (t < base + cur_units) break;
+          base += cur_units;
+          ++cur;
+          cur_units = ~0ull;
+        }
+        if (!stop) {
+          const unsigned long long lt = t - base;
+          unit = ld_acquire_u64(&cur_queue[lt]);
+          if (unit == Q_EMPTY) {
+            const uint64_t t0 = globaltimer();
+            for (unsigned spin = 0;; ++spin) {
+              poll_slot(s_args[b ^ 1], st[b ^ 1], &s_empty[b ^ 1]);
+              __nanosleep(spin < 64 ? 32 : 256);
+              unit = ld_acquire_u64(&cur_queue[lt]);
+              if (unit != Q_EMPTY) break;
+              if ((spin & 63) == 63) {
+                if (ld_relaxed_u32(&ctl->abort)) {
+                  unit = kStop;
+                  break;
+                }
+                if (globaltimer() - t0 > watchdog_ns) {
+                  raise_error(ctl->subs[cur], ERR_WATCHDOG);
+                  unit = kStop;
+                  break;
+                }
+              }
+            }
+          }
+          if (unit != kStop && (unit >> 32) >= cur_nitems) {
+            raise_error(ctl->subs[cur], ERR_BAD_UNIT);
+            unit = kStop;
+          }
+        }
+        sub = cur;
+        st[b].unit = unit;
+        st[b].unreleased = unit != kStop;
+      }
+      unit = __shfl_sync(0xffffffffu, unit, 0);
+      sub = __shfl_sync(0xffffffffu, sub, 0);
+      if (unit != kStop && (int)sub != slot_sub[b]) {
+        // stage the sub-epoch's arguments for slot b (its previous unit is
+        // released); L2-only loads: subs[] is written during the launch
+        const unsigned long long *src = reinterpret_cast<const unsigned long long *>(&ctl->subs[sub]);
+        unsigned long long *dst = reinterpret_cast<unsigned long long *>(&s_args[b]);
+        for (int i = lane; i < (int)(sizeof(EpochArgs) / 8); i += 32) dst[i] = __ldcg(src + i);
+        __syncwarp();
+        slot_sub[b] = (int)sub;
+      }
+      stage_unit(s_args[b], unit, &s_item[b], s_fac[b], lane);
+      if (lane == 0) s_unit[b] = unit;
+      __syncwarp();
+      bar_arrive(kBarFull + b, 32 + kCompute);
+      if (unit == kStop) {
+        if (lane == 0) drain_slot(s_args[b ^ 1], st[b ^ 1], &s_empty[b ^ 1]);   // unit u-1 still in flight
+        break;
+      }
+    }
+  } else {
+    compute_loop<kCompute, kSlotsSW, PF, true>(s_args[0], s_args, s_unit, s_item, s_fac, s_empty, lane);
+  }
+  // the last CTA to leave copies every published sub-epoch's counters to its
+  // mapped host copy (the host retires the sub-epochs one by one)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&ctl->exited, 1u) == gridDim.x - 1) {
+      __threadfence();
+      const unsigned n = min(__ldcg(&ctl->nsub), ld_acquire_u32(&ctl->published));
+      for (unsigned r = 0; r < n; ++r) {
+        Counters *c = reinterpret_cast<Counters *>(
+            __ldcg(reinterpret_cast<const unsigned long long *>(&ctl->subs[r].ctr)));
+        volatile Counters *h = reinterpret_cast<volatile Counters *>(
+            __ldcg(reinterpret_cast<const unsigned long long *>(&ctl->subs[r].host_ctr)));
+        h->head = atomicAdd(&c->head, 0ull);
+        h->tail = atomicAdd(&c->tail, 0ull);
+        h->done = atomicAdd(&c->done, 0ull);
+        h->error = atomicAdd(&c->error, 0u);
+        h->exited = gridDim.x;
+      }
+      __threadfence_system();
+    }
+  }
 }
 
 // Epoch set-up in one launch: copy the epoch blob from mapped pinned host
@@ -1470,6 +1639,14 @@ __global__ void __launch_bounds__(kBlockWQ, BT_WQ_MIN_CTAS) scheduler_kernel_wq(
   report_exit(a);
 }
 
+// Stream launch (runtime.cpp, flush_epoch): the "sw" kernel over the
+// sub-epochs the host publishes in *ctl.
+cudaError_t launch_stream(StreamCtl *ctl, uint64_t watchdog_ns, int grid, cudaStream_t stream, bool prefetch) {
+  if (prefetch) scheduler_kernel_sws<true><<<grid, kBlock, 0, stream>>>(ctl, watchdog_ns);
+  else scheduler_kernel_sws<false><<<grid, kBlock, 0, stream>>>(ctl, watchdog_ns);
+  return cudaGetLastError();
+}
+
 // Host-side launcher (called from runtime.cpp).
 // kernel: 0 = sw, 1 = rw, 2 = wq, 3 = sw with prefetching SCAL bodies (short
 // chains); grid in CTAs of that kernel's block size.
@@ -1493,6 +1670,10 @@ cudaError_t scheduler_occupancy(int *blocks_per_sm, int *block) {
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, scheduler_kernel_sw<false>, kBlock, 0);
   int c = 0;
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, scheduler_kernel_sw<true>, kBlock, 0);
+  if (c < b) b = c;
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, scheduler_kernel_sws<false>, kBlock, 0);
+  if (c < b) b = c;
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, scheduler_kernel_sws<true>, kBlock, 0);
   if (c < b) b = c;
   *blocks_per_sm = a < b ? a : b;
   return e;

@@ -309,6 +309,76 @@ def test_c5_shape_pipelined_default(B):
     assert stats["epochs"] >= 4
 
 
+# ---- stream launches: the rounds of a pipelined run as
+# sub-epochs of one persistent launch, published while it runs ----
+
+def run_device(B, program, repeats=1, **kw):
+    """Device-homed buffers (torch tensors); the program submitted `repeats`
+    times back to back with one wait at the end."""
+    import torch
+    from paper_1304_0878_b200.programs import Session
+    tensors = [torch.from_numpy(b.copy()).cuda() for b in program.buffers]
+    with B.Runtime(**kw) as rt:
+        s = Session(rt, program, device_tensors=tensors)
+        for _ in range(repeats):
+            s.submit()
+        rt.wait()
+        st = rt.stats()
+        s.finish()
+    torch.cuda.synchronize()
+    return [t.cpu().numpy() for t in tensors], st
+
+
+def repeated(program, k):
+    return W.Program(program.buffers, program.nparts, np.concatenate([program.tasks] * k), name=program.name)
+
+
+@pytest.mark.parametrize("rounds,threads", [(2, 2), (4, 3), (6, 5), (10, 4)])
+@pytest.mark.parametrize("fusion", [True, False])
+def test_stream_launch(B, rounds, threads, fusion):
+    """32 KiB tiles ("sw" units), sweep-major SCAL runs: every run's rounds join
+    one launch (fewer scheduler launches than epochs); unfused, each sub-epoch
+    is a DAG of chains released on the device.  Three runs in flight back to
+    back, then one wait; bit-exact against the oracle."""
+    p = W.c5_sharded(nx=600 * 8192, ntiles=600, sweeps=12)
+    flags = 0 if fusion else B.BT_FLAG_NO_FUSION
+    out, st = run_device(B, p, repeats=3, flags=flags, pipeline_rounds=rounds, pipeline_min=500,
+                         parallel_min=500, host_threads=threads)
+    assert_bits_equal(out[0], oracle.run(repeated(p, 3))[0], f"stream launch r={rounds}")
+    assert st["epochs"] >= 2 * 3 and st["sched_launches"] == 3, st
+    out2, st2 = run_device(B, p, repeats=1, flags=flags | B.BT_FLAG_NO_STREAM, pipeline_rounds=rounds,
+                           pipeline_min=500, parallel_min=500, host_threads=threads)
+    assert_bits_equal(out2[0], oracle.run(p)[0], f"per-round launches r={rounds}")
+    assert st2["sched_launches"] == st2["epochs"], st2
+
+
+def test_stream_launch_mixed_program(B):
+    """Pipelined SCAL runs (stream launches) between AXPY/COPY tasks on the same
+    device-homed tiles: the dependencies across launches and the ordinary
+    epochs in between hold."""
+    rng = np.random.default_rng(4242)
+    nbuf, nparts, n = 2, 200, 200 * 8192
+    bufs = [W.unit_interval_floats(rng, n) for _ in range(nbuf)]
+    rows = []
+    for blk in range(4):
+        f = W.sweep_factors(rng, 6)
+        for s_ in range(6):
+            for t in range(nparts):
+                rows.append((W.SCAL, f[s_], blk % nbuf, t, -1, -1))
+        for _ in range(int(rng.integers(1, 30))):
+            t = int(rng.integers(0, nparts))
+            rows.append((W.AXPY if rng.random() < .5 else W.COPY, np.float32(0.25), 1 - blk % nbuf, t, blk % nbuf, t))
+    tasks = W._tasks(len(rows))
+    for i, r in enumerate(rows):
+        tasks[i] = r
+    p = W.Program(bufs, [nparts] * nbuf, tasks, name="stream launches between AXPY/COPY")
+    out, st = run_device(B, p, pipeline_rounds=4, pipeline_min=500, parallel_min=500, host_threads=3)
+    exp = oracle.run(p)
+    for b in range(nbuf):
+        assert_bits_equal(out[b], exp[b], f"mixed buffer {b}")
+    assert st["sched_launches"] < st["epochs"], st
+
+
 # ---- host <-> device coherence: chunked upload, eager write-back, dirty path ----
 
 def _sweeps(B, rt, subs, factors):
