@@ -116,6 +116,7 @@ struct EpochBuf {
   uint64_t units = 0;
   bool traced = false;
   bool timed = true;          // start/end bracket a launch (false: a later sub-epoch of a stream launch)
+  bool held = false;          // a deferred stream launch's sub-epoch, not launched yet: never picked
   Counters *hctr = nullptr;     // mapped pinned: written by the kernel's last CTA
   Counters *hctr_dev = nullptr;
   size_t trace_off_h = 0;     // offset of the trace copy in hblob
@@ -191,6 +192,7 @@ struct bt_runtime {
     bool want = false, active = false;
     unsigned nsub = 0, next = 0;
     bool prefetch = false;
+    EpochBuf *bufs[kMaxSubs] = {};    // the sub-epochs' buffers (bufs[0]'s start/end time the launch)
   } sl;
   cudaEvent_t ev_pub0 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_round[2] = {nullptr, nullptr};
@@ -443,6 +445,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   // else the oldest in flight (retire waits for it)
   EpochBuf *pick = nullptr, *oldest = nullptr;
   for (EpochBuf &c : rt->ep) {
+    if (c.held) continue;
     if (!c.inflight || cudaEventQuery(c.done) != cudaErrorNotReady) {
       pick = &c;
       break;
@@ -723,19 +726,38 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     CUDA_TRY(rt, cudaMemcpyAsync(d, h, o_cdone + 4 * N, cudaMemcpyHostToDevice, up));
     CUDA_TRY(rt, cudaMemcpyAsync(&rt->sctl->subs[r], h + o_args_h, sizeof(EpochArgs), cudaMemcpyHostToDevice, up));
     CUDA_TRY(rt, cudaMemcpyAsync(&rt->sctl->published, h + o_pub_h, 4, cudaMemcpyHostToDevice, up));
-    if (r == 0) {
-      // later sub-epochs' copies follow the header reset
+    // BT_STREAM_DEFER=1: launch after the last sub-epoch is published, for
+    // tools that serialise kernel launches (ncu, compute-sanitizer): the
+    // launch call does not return before the kernel ends there, so a running
+    // kernel would wait for publications the host cannot make
+    static const bool defer = getenv("BT_STREAM_DEFER") != nullptr;
+    if (r == 0) {   // later sub-epochs' copies follow the header reset
       CUDA_TRY(rt, cudaEventRecord(rt->ev_pub0, ls));
       CUDA_TRY(rt, cudaStreamWaitEvent(rt->rstream[1], rt->ev_pub0, 0));
-      CUDA_TRY(rt, cudaEventRecord(e.start, ls));
+    }
+    rt->sl.bufs[r] = &e;
+    if (defer && r + 1 == rt->sl.nsub) {
+      CUDA_TRY(rt, cudaEventRecord(rt->ev_pub0, up));
+      CUDA_TRY(rt, cudaStreamWaitEvent(ls, rt->ev_pub0, 0));
+    }
+    if (defer ? r + 1 == rt->sl.nsub : r == 0) {
+      EpochBuf &e0 = *rt->sl.bufs[0];
+      CUDA_TRY(rt, cudaEventRecord(e0.start, ls));
       rt->stats.grid = (uint32_t)rt->grid_max;
       rt->stats.block = (uint32_t)rt->block;
       rt->stats.kernel_launches += 1;
       rt->stats.sched_launches += 1;
       CUDA_TRY(rt, launch_stream(rt->sctl, kWatchdogNs, rt->grid_max, ls, rt->sl.prefetch));
-      CUDA_TRY(rt, cudaEventRecord(e.end, ls));
+      CUDA_TRY(rt, cudaEventRecord(e0.end, ls));
+      for (unsigned q = 0; q < r; ++q) {   // deferred: the earlier sub-epochs complete with the launch
+        CUDA_TRY(rt, cudaEventRecord(rt->sl.bufs[q]->done, ls));
+        rt->sl.bufs[q]->held = false;
+      }
     }
-    CUDA_TRY(rt, cudaEventRecord(e.done, ls));   // after the launch: it ends once every sub-epoch ran
+    // after the launch (which ends once every sub-epoch ran); deferred and not
+    // yet launched: held (not reusable) until the launch is enqueued
+    e.held = defer && r + 1 < rt->sl.nsub;
+    if (!e.held) CUDA_TRY(rt, cudaEventRecord(e.done, ls));
     e.timed = r == 0;
     if (++rt->sl.next == rt->sl.nsub) rt->sl.active = false;
     account();
@@ -1562,7 +1584,13 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
   // choice allows it: flush_epoch); sl is reset however this run ends
   struct SlReset {
     bt_runtime *rt;
-    ~SlReset() { rt->sl.want = rt->sl.active = false; }
+    ~SlReset() {
+      rt->sl.want = rt->sl.active = false;
+      for (EpochBuf *&b : rt->sl.bufs) {   // a run that failed before its deferred launch
+        if (b) b->held = false;
+        b = nullptr;
+      }
+    }
   } sl_reset{rt};
   if (pipelined && rt->sctl) {
     unsigned nsub = 0;

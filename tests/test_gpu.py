@@ -352,6 +352,29 @@ def test_stream_launch(B, rounds, threads, fusion):
     assert st2["sched_launches"] == st2["epochs"], st2
 
 
+def test_stream_launch_deferred(B, tmp_path):
+    """BT_STREAM_DEFER=1 (for tools that serialise launches): the stream launch
+    is enqueued after its last sub-epoch is published; same results."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, oracle, workloads as W\n"
+        "from tests.test_gpu import run_device, repeated, assert_bits_equal\n"
+        "from paper_1304_0878_b200 import btask as B\n"
+        "p = W.c5_sharded(nx=300 * 8192, ntiles=300, sweeps=8)\n"
+        "for flags in (0, B.BT_FLAG_NO_FUSION):\n"
+        "    out, st = run_device(B, p, repeats=2, flags=flags, pipeline_rounds=4, pipeline_min=200,\n"
+        "                         parallel_min=200, host_threads=3)\n"
+        "    assert_bits_equal(out[0], oracle.run(repeated(p, 2))[0], 'deferred stream launch')\n"
+        "    assert st['sched_launches'] == 2 and st['epochs'] >= 4, st\n"
+        "print('ok')\n")
+    import os
+    env = dict(os.environ, BT_STREAM_DEFER="1")
+    r = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(os.path.dirname(__file__)), env=env,
+                       capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
 def test_stream_launch_mixed_program(B):
     """Pipelined SCAL runs (stream launches) between AXPY/COPY tasks on the same
     device-homed tiles: the dependencies across launches and the ordinary
