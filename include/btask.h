@@ -273,6 +273,7 @@ typedef struct bt_stats {
   uint64_t kernel_launches;   /* this library's kernel launches (per epoch: set-up + scheduler) */
   uint64_t sched_launches;    /* of which scheduler-kernel launches (a stream launch runs several epochs);
                                  device_ms / sched_launches = average launch duration */
+  uint64_t stream_closes;     /* stream launches ended early (a later round needed a larger epoch buffer) */
 } bt_stats;
 int bt_stats_get(bt_runtime *rt, bt_stats *out);
 int bt_stats_reset(bt_runtime *rt);

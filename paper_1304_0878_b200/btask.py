@@ -41,7 +41,7 @@ class bt_stats(ctypes.Structure):
                 ("epochs", ctypes.c_uint64), ("upload_bytes", ctypes.c_uint64), ("host_build_ms", ctypes.c_double),
                 ("device_ms", ctypes.c_double), ("device_span_ms", ctypes.c_double), ("grid", ctypes.c_uint32),
                 ("block", ctypes.c_uint32), ("kernel_launches", ctypes.c_uint64),
-                ("sched_launches", ctypes.c_uint64)]
+                ("sched_launches", ctypes.c_uint64), ("stream_closes", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -148,6 +148,20 @@ struct RootCache {
 
 struct bt_runtime {
   bt_config cfg;
+  // BT_DEBUG_ERRORS: the last scheduling events, dumped with a device fault
+  char evlog[64][96] = {};
+  unsigned evn = 0;
+  void ev(const char *fmt, ...) __attribute__((format(printf, 2, 3))) {
+    static const bool on = getenv("BT_DEBUG_ERRORS") != nullptr;
+    if (!on) return;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(evlog[evn++ % 64], 96, fmt, ap);
+    va_end(ap);
+  }
+  void ev_dump() {
+    for (unsigned i = evn > 64 ? evn - 64 : 0; i < evn; ++i) fprintf(stderr, "  ev %u: %s\n", i, evlog[i % 64]);
+  }
   bool host_only = false;
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -188,10 +202,12 @@ struct bt_runtime {
   // for it (decided at its first flush); active: sub-epochs next..nsub-1 join
   // the running launch
   StreamCtl *sctl = nullptr;
+  char *close_h = nullptr;   // pinned: published values 1..kMaxSubs, then a zero EpochArgs (close_stream)
   struct {
     bool want = false, active = false;
     unsigned nsub = 0, next = 0;
     bool prefetch = false;
+    bool started = false;
     EpochBuf *bufs[kMaxSubs] = {};    // the sub-epochs' buffers (bufs[0]'s start/end time the launch)
   } sl;
   cudaEvent_t ev_pub0 = nullptr;
@@ -246,6 +262,8 @@ int fail(bt_runtime *rt, int err, const char *fmt, ...) {
     vsnprintf(buf, sizeof buf, fmt, ap);
     va_end(ap);
     rt->last_error = buf;
+    static const bool dbg = getenv("BT_DEBUG_ERRORS") != nullptr;
+    if (dbg) fprintf(stderr, "btask error %d: %s\n", err, buf);
   }
   return err;
 }
@@ -401,6 +419,31 @@ int retire(bt_runtime *rt, EpochBuf &e) {
                 c->error == ERR_WATCHDOG ? ": watchdog, a unit was never released" : "");
   }
   if (c->done != e.units) {
+    static const bool dbg = getenv("BT_DEBUG_ERRORS") != nullptr;
+    if (dbg) {
+      fprintf(stderr, "btask retire: buffer %d seq %llu units %llu done %llu error %u exited %u timed %d\n",
+              (int)(&e - rt->ep), (unsigned long long)e.seq, (unsigned long long)e.units,
+              (unsigned long long)c->done, c->error, c->exited, (int)e.timed);
+      rt->ev_dump();
+      if (rt->sctl) {
+        unsigned char hdr[64];
+        cudaError_t ce = cudaMemcpy(hdr, rt->sctl, 64, cudaMemcpyDeviceToHost);
+        unsigned long long tk;
+        unsigned w[4];
+        memcpy(&tk, hdr, 8);
+        memcpy(w, hdr + 8, 16);
+        unsigned pd[4];
+        memcpy(pd, hdr + 24, 16);
+        fprintf(stderr, "  StreamCtl (%d): ticket %llu published %u abort %u exited %u nsub %u pad %u %u %u %u\n",
+                (int)ce, tk, w[0], w[1], w[2], w[3], pd[0], pd[1], pd[2], pd[3]);
+        for (unsigned q = 0; q < kMaxSubs && rt->sl.bufs[q]; ++q) {
+          Counters c2;
+          cudaMemcpy(&c2, rt->sl.bufs[q]->dblob, sizeof c2, cudaMemcpyDeviceToHost);
+          fprintf(stderr, "  sub %u ctr: head %llu tail %llu error %u abort %u done %llu exited %u\n", q, c2.head,
+                  c2.tail, c2.error, c2.abort, c2.done, c2.exited);
+        }
+      }
+    }
     rt->poisoned = -EIO;
     return fail(rt, -EIO, "device scheduler ended early (%llu of %llu units)", (unsigned long long)c->done,
                 (unsigned long long)e.units);
@@ -432,6 +475,25 @@ inline void range_of(size_t n, int P, int p, size_t &lo, size_t &hi) {
   hi = n * (size_t)(p + 1) / (size_t)P;
 }
 
+// End the running stream launch early: sub-epochs next..nsub-1 are published
+// empty (zero EpochArgs: no units), so its CTAs finish.  Copies from a pinned
+// table whose contents never change (published value q + 1 at index q, then a
+// zero EpochArgs), so overlapping closes of successive launches cannot race.
+int close_stream(bt_runtime *rt) {
+  const unsigned *pub = reinterpret_cast<const unsigned *>(rt->close_h);
+  const char *zero_args = rt->close_h + 4 * kMaxSubs;
+  cudaStream_t up = rt->rstream[1];
+  for (unsigned q = rt->sl.next; q < rt->sl.nsub; ++q) {
+    CUDA_TRY(rt, cudaMemcpyAsync(&rt->sctl->subs[q], zero_args, sizeof(EpochArgs), cudaMemcpyHostToDevice, up));
+    CUDA_TRY(rt, cudaMemcpyAsync(&rt->sctl->published, &pub[q], 4, cudaMemcpyHostToDevice, up));
+  }
+  rt->ev("close stream launch at sub %u of %u", rt->sl.next, rt->sl.nsub);
+  rt->sl.next = rt->sl.nsub;
+  rt->sl.active = false;
+  rt->stats.stream_closes += 1;
+  return 0;
+}
+
 int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   Builder &B = rt->builder;
   if (B.items.empty()) {
@@ -446,13 +508,17 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   EpochBuf *pick = nullptr, *oldest = nullptr;
   for (EpochBuf &c : rt->ep) {
     if (c.held) continue;
-    if (!c.inflight || cudaEventQuery(c.done) != cudaErrorNotReady) {
+    const cudaError_t qe = c.inflight ? cudaEventQuery(c.done) : cudaSuccess;
+    if (c.inflight) rt->ev("query buf %d seq %llu -> %d", (int)(&c - rt->ep), (unsigned long long)c.seq, (int)qe);
+    if (!c.inflight || qe != cudaErrorNotReady) {
       pick = &c;
       break;
     }
     if (!oldest || c.seq < oldest->seq) oldest = &c;
   }
   EpochBuf &e = pick ? *pick : *oldest;
+  rt->ev("pick buf %d (%s) seq %llu inflight %d", (int)(&e - rt->ep), pick ? "free" : "oldest",
+         (unsigned long long)e.seq, (int)e.inflight);
   if (int r = retire(rt, e)) return r;
 
   const size_t N = B.items.size();
@@ -560,8 +626,9 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
                     !(rt->cfg.flags & BT_FLAG_SYNC_EPOCH) && rt->sctl && rt->sl.nsub >= 2;
     rt->sl.next = 0;
     rt->sl.prefetch = kernel == 3;
+    rt->sl.started = rt->sl.active;
   }
-  const bool sub = rt->sl.active;
+  bool sub = rt->sl.active;
   // device layout: ctr | items | pending | succ | factors | queue[U] | chunk_done[N] | trace
   const size_t o_ctr = 0;
   const size_t o_items = 64;
@@ -581,7 +648,27 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   const size_t o_sx_h = align_up(std::max(o_trace_h + (traced ? 36 * U : 0), o_cdone + 4 * N), 64);
   const size_t o_args_h = o_sx_h + 64;
   const size_t o_pub_h = align_up(o_args_h + sizeof(EpochArgs), 16);
+  // A sub-epoch that joins a RUNNING launch must not allocate: cudaMalloc /
+  // cudaHostAlloc / cudaFree are implicit synchronisation points and would
+  // wait for the launch, which waits for this very publication.  Such a
+  // sub-epoch closes the launch instead (the remaining sub-epochs are
+  // published empty, so it ends) and runs as an ordinary epoch.
+  if (sub && rt->sl.next > 0 && (e.hcap < o_pub_h + 16 || e.dcap < dneed)) {
+    if (int r = close_stream(rt)) return r;
+    sub = false;
+  }
   const size_t hneed = sub ? o_pub_h + 16 : align_up(o_trace_h + (traced ? 36 * U : 0), 16);
+  if (sub && rt->sl.next == 0) {
+    // before the launch: grow every reusable epoch buffer to 1.25 x this
+    // sub-epoch's needs (a run's rounds are near-equal parts of it), so the
+    // later sub-epochs find room without allocating
+    for (EpochBuf &c : rt->ep) {
+      if (&c == &e || c.held || (c.inflight && cudaEventQuery(c.done) == cudaErrorNotReady)) continue;
+      if (int r = retire(rt, c)) return r;
+      if (int r = ensure_host(rt, c, hneed + hneed / 4)) return r;
+      if (int r = ensure_dev(rt, c, dneed + dneed / 4)) return r;
+    }
+  }
   if (int r = ensure_host(rt, e, hneed)) return r;
   if (int r = ensure_dev(rt, e, dneed)) return r;
 
@@ -706,6 +793,8 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   if (sub) {
     // ---- sub-epoch r of the run's stream launch (device_abi.h StreamCtl) ----
     const unsigned r = rt->sl.next;
+    rt->ev("sub %u/%u buf %d seq %llu U %llu U0 %llu N %zu", r, rt->sl.nsub, (int)(&e - rt->ep),
+           (unsigned long long)rt->ep_seq + 1, (unsigned long long)U, (unsigned long long)U0, N);
     cudaStream_t ls = rt->rstream[0];                    // the launch
     cudaStream_t up = r == 0 ? ls : rt->rstream[1];      // this sub-epoch's copies
     if (!rt->span_open) {
@@ -797,6 +886,8 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   rt->stats.grid = (uint32_t)kgrid;
   rt->stats.sched_launches += 1;
   rt->stats.block = kernel == 2 ? (uint32_t)rt->block_wq : (uint32_t)rt->block;
+  rt->ev("epoch buf %d seq %llu U %llu kernel %d grid %d stream %p", (int)(&e - rt->ep),
+         (unsigned long long)rt->ep_seq + 1, (unsigned long long)U, kernel, kgrid, (void *)stream);
   CUDA_TRY(rt, launch_epoch(a, kgrid, stream, kernel));
   CUDA_TRY(rt, cudaEventRecord(e.end, stream));
   // write-back of host-homed ranges written for the first time since registration
@@ -999,9 +1090,26 @@ int bt_init(const bt_config *cfg_in, bt_runtime **out) {
       }
     if (!(cfg.flags & BT_FLAG_NO_STREAM) &&
         (cudaMalloc((void **)&rt->sctl, sizeof(StreamCtl)) != cudaSuccess ||
-         cudaEventCreateWithFlags(&rt->ev_pub0, cudaEventDisableTiming) != cudaSuccess)) {
+         cudaEventCreateWithFlags(&rt->ev_pub0, cudaEventDisableTiming) != cudaSuccess ||
+         cudaHostAlloc((void **)&rt->close_h, 4 * kMaxSubs + sizeof(EpochArgs), cudaHostAllocPortable) !=
+             cudaSuccess)) {
       cudaGetLastError();
+      if (rt->sctl) cudaFree(rt->sctl);
       rt->sctl = nullptr;   // pipelined runs then launch once per round
+    }
+    if (rt->sctl) {
+      for (unsigned q = 0; q < (unsigned)kMaxSubs; ++q) reinterpret_cast<unsigned *>(rt->close_h)[q] = q + 1;
+      memset(rt->close_h + 4 * kMaxSubs, 0, sizeof(EpochArgs));
+    }
+    // every epoch buffer's mapped completion record, allocated here: a
+    // sub-epoch joining a running stream launch must not allocate (flush_epoch)
+    for (auto &e : rt->ep) {
+      if (cudaHostAlloc((void **)&e.hctr, sizeof(Counters), cudaHostAllocMapped | cudaHostAllocPortable) !=
+              cudaSuccess ||
+          cudaHostGetDevicePointer((void **)&e.hctr_dev, e.hctr, 0) != cudaSuccess) {
+        delete rt;
+        return -ENOMEM;
+      }
     }
     // keep freed replicas in the pool (register/unregister loops reuse them)
     cudaMemPool_t mp;
@@ -1038,6 +1146,7 @@ int bt_shutdown(bt_runtime *rt) {
     if (rt->ev_fork) cudaEventDestroy(rt->ev_fork);
     if (rt->ev_pub0) cudaEventDestroy(rt->ev_pub0);
     if (rt->sctl) cudaFree(rt->sctl);
+    if (rt->close_h) cudaFreeHost(rt->close_h);
     for (cudaEvent_t ev : rt->ev_free) cudaEventDestroy(ev);
     if (rt->h2d) cudaStreamDestroy(rt->h2d);
     if (rt->d2h) cudaStreamDestroy(rt->d2h);
@@ -1585,6 +1694,12 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
   struct SlReset {
     bt_runtime *rt;
     ~SlReset() {
+      static const bool dbg = getenv("BT_DEBUG_ERRORS") != nullptr;
+      if (dbg && rt->sl.started && rt->sl.next != rt->sl.nsub)
+        fprintf(stderr, "btask: stream launch published %u of %u sub-epochs\n", rt->sl.next, rt->sl.nsub);
+      // a run that failed part-way: end its launch (no CTA waits for the watchdog)
+      if (rt->sl.started && rt->sl.next < rt->sl.nsub) close_stream(rt);
+      rt->sl.started = false;
       rt->sl.want = rt->sl.active = false;
       for (EpochBuf *&b : rt->sl.bufs) {   // a run that failed before its deferred launch
         if (b) b->held = false;

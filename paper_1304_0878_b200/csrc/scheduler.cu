@@ -1403,6 +1403,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sws(Stre
             __ldcg(reinterpret_cast<const unsigned long long *>(&ctl->subs[r].ctr)));
         volatile Counters *h = reinterpret_cast<volatile Counters *>(
             __ldcg(reinterpret_cast<const unsigned long long *>(&ctl->subs[r].host_ctr)));
+        if (!c || !h) continue;   // published empty (close_stream)
         h->head = atomicAdd(&c->head, 0ull);
         h->tail = atomicAdd(&c->tail, 0ull);
         h->done = atomicAdd(&c->done, 0ull);

@@ -345,7 +345,7 @@ def test_stream_launch(B, rounds, threads, fusion):
     out, st = run_device(B, p, repeats=3, flags=flags, pipeline_rounds=rounds, pipeline_min=500,
                          parallel_min=500, host_threads=threads)
     assert_bits_equal(out[0], oracle.run(repeated(p, 3))[0], f"stream launch r={rounds}")
-    assert st["epochs"] >= 2 * 3 and st["sched_launches"] == 3, st
+    assert st["epochs"] >= 2 * 3 and st["sched_launches"] == 3 and st["stream_closes"] == 0, st
     out2, st2 = run_device(B, p, repeats=1, flags=flags | B.BT_FLAG_NO_STREAM, pipeline_rounds=rounds,
                            pipeline_min=500, parallel_min=500, host_threads=threads)
     assert_bits_equal(out2[0], oracle.run(p)[0], f"per-round launches r={rounds}")
@@ -373,6 +373,31 @@ def test_stream_launch_deferred(B, tmp_path):
     r = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(os.path.dirname(__file__)), env=env,
                        capture_output=True, text=True, timeout=240)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_stream_launch_closes_early(B):
+    """Rounds of very different sizes: a later round outgrows the epoch
+    buffers sized at the first one, closes the running launch (its remaining
+    sub-epochs are published empty) and runs as ordinary epochs -- no
+    allocation while the launch waits, same results."""
+    rng = np.random.default_rng(77)
+    nparts, tile = 400, 8192
+    x = W.unit_interval_floats(rng, nparts * tile)
+    # round 0 (tiles 0-99): chains of 12 (fused: 100 items); rounds 1-3: one
+    # task per tile (300 items) -- launches are balanced by tasks, not items
+    rows = []
+    for _ in range(12):
+        for t in range(100):
+            rows.append((W.SCAL, np.float32(rng.uniform(0.9, 1.1)), 0, t, -1, -1))
+    for t in range(100, nparts):
+        rows.append((W.SCAL, np.float32(rng.uniform(0.9, 1.1)), 0, t, -1, -1))
+    tasks = W._tasks(len(rows))
+    for i, r in enumerate(rows):
+        tasks[i] = r
+    p = W.Program([x], [nparts], tasks, name="uneven rounds")
+    out, st = run_device(B, p, repeats=2, pipeline_rounds=4, pipeline_min=500, parallel_min=500, host_threads=3)
+    assert_bits_equal(out[0], oracle.run(repeated(p, 2))[0], "uneven rounds")
+    assert st["stream_closes"] >= 1, st
 
 
 def test_stream_launch_mixed_program(B):

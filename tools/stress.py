@@ -7,6 +7,8 @@ for --minutes; prints one JSON line per 50 programs and a summary; exits 1 on
 the first mismatch (with the seed to reproduce it).
 
     python tools/stress.py --minutes 10
+    python tools/stress.py --minutes 10 --device   # device-homed buffers: stream launches,
+                                                   # 1-3 submissions back to back per wait
 """
 import argparse
 import json
@@ -27,9 +29,25 @@ from paper_1304_0878_b200.programs import run_program  # noqa: E402
 KERNELS = [0, B.BT_FLAG_KERNEL_SW, B.BT_FLAG_KERNEL_RW, B.BT_FLAG_KERNEL_WQ]
 
 
-def make(seed):
+def run_device(p, repeats, **kw):
+    """Device-homed buffers (torch tensors); p submitted `repeats` times, one wait."""
+    import torch
+    from paper_1304_0878_b200.programs import Session
+    tensors = [torch.from_numpy(b.copy()).cuda() for b in p.buffers]
+    with B.Runtime(**kw) as rt:
+        s = Session(rt, p, device_tensors=tensors)
+        for _ in range(repeats):
+            s.submit()
+        rt.wait()
+        st = rt.stats()
+        s.finish()
+    torch.cuda.synchronize()
+    return [t.cpu().numpy() for t in tensors], st
+
+
+def make(seed, device=False):
     rng = np.random.default_rng(seed)
-    shape = int(rng.integers(0, 3))
+    shape = int(rng.integers(0, 3)) if not device else int(rng.choice([0, 1, 2, 2, 2]))
     if shape == 0:
         p = W.random_small_program(seed, max_tasks=int(rng.integers(5, 200)), max_handles=int(rng.integers(1, 8)),
                                    max_elems=int(rng.integers(8, 50000)))
@@ -37,7 +55,9 @@ def make(seed):
         p = W.c3_random_dag(nbuf=int(rng.integers(2, 12)), nx=int(rng.integers(1, 40000)),
                             ntasks=int(rng.integers(1, 600)), seed=seed)
     else:
-        p = W.c4_fine(ntiles=int(rng.integers(1, 400)), tile_nx=int(rng.integers(1, 3000)),
+        p = W.c4_fine(ntiles=int(rng.integers(1, 400)),
+                      tile_nx=int(rng.integers(1, 3000) if not device else rng.choice([rng.integers(1, 3000),
+                                                                                       rng.integers(4097, 20000)])),
                       sweeps=int(rng.integers(1, 40)), seed=seed,
                       order="sweep" if rng.random() < 0.5 else "tile")
     kw = dict(chunk_bytes=int(rng.choice([0, 0, 32, 96, 4096, 65536])),
@@ -46,6 +66,8 @@ def make(seed):
               pipeline_min=int(rng.integers(1, 64)), pipeline_rounds=int(rng.integers(1, 5)),
               max_fused=int(rng.choice([0, 1, 3, 7, 64, 1024])),
               epoch_tasks=int(rng.choice([0, 0, 0, 5, 37])))
+    if device:
+        kw["pipeline_rounds"] = int(rng.integers(1, 11))
     return p, kw
 
 
@@ -53,12 +75,34 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--minutes", type=float, default=10.0)
     ap.add_argument("--seed0", type=int, default=700000)
+    ap.add_argument("--device", action="store_true", help="device-homed buffers (stream launches)")
+    ap.add_argument("--count", type=int, default=0, help="stop after this many programs (0: --minutes only)")
+    ap.add_argument("--extra-flags", type=int, default=0, help="OR-ed into every configuration's flags")
     args = ap.parse_args()
+    streams = 0
     t_end = time.time() + 60 * args.minutes
     seed, n, tasks = args.seed0, 0, 0
-    while time.time() < t_end:
-        p, kw = make(seed)
-        out, st = run_program(p, device=0, **kw)
+    while time.time() < t_end and (not args.count or n < args.count):
+        p, kw = make(seed, args.device)
+        kw["flags"] |= args.extra_flags
+        if args.device:
+            reps = int(np.random.default_rng(seed + 1).integers(1, 4))
+            try:
+                t0 = time.time()
+                out, st = run_device(p, reps, **kw)
+                if os.environ.get("BT_STRESS_VERBOSE"):
+                    print(json.dumps({"seed": seed, "s": round(time.time() - t0, 3), "epochs": st["epochs"],
+                                      "sched_launches": st["sched_launches"]}), flush=True)
+                import torch
+                torch.cuda.synchronize()   # a sticky device fault surfaces at the program that caused it
+            except Exception as ex:
+                print(json.dumps({"error": str(ex), "seed": seed, "program": p.name, "repeats": reps,
+                                  "config": {k: int(v) for k, v in kw.items()}}), flush=True)
+                return 1
+            streams += st["sched_launches"] < st["epochs"]
+            p = W.Program(p.buffers, p.nparts, np.concatenate([p.tasks] * reps), name=p.name)
+        else:
+            out, st = run_program(p, device=0, **kw)
         exp = oracle.run(p)
         for b, (o, e) in enumerate(zip(out, exp)):
             if not np.array_equal(o.view(np.uint32), e.view(np.uint32)):
@@ -69,9 +113,11 @@ def main():
         n += 1
         tasks += p.ntasks
         if n % 50 == 0:
-            print(json.dumps({"programs": n, "tasks": tasks, "last_seed": seed}), flush=True)
+            print(json.dumps({"programs": n, "tasks": tasks, "last_seed": seed, "with_stream_launch": streams}),
+                  flush=True)
         seed += 1
-    print(json.dumps({"ok": True, "programs": n, "tasks": tasks, "seeds": [args.seed0, seed - 1]}), flush=True)
+    print(json.dumps({"ok": True, "programs": n, "tasks": tasks, "seeds": [args.seed0, seed - 1],
+                      "device_homed": args.device, "with_stream_launch": streams}), flush=True)
     return 0
 
 
