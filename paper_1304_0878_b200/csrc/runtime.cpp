@@ -208,6 +208,7 @@ struct bt_runtime {
     unsigned nsub = 0, next = 0;
     bool prefetch = false;
     bool started = false;
+    uint64_t run_tasks = 0, cur_tasks = 0;   // local tasks of the run / of the sub-epoch being flushed
     EpochBuf *bufs[kMaxSubs] = {};    // the sub-epochs' buffers (bufs[0]'s start/end time the launch)
   } sl;
   cudaEvent_t ev_pub0 = nullptr;
@@ -533,7 +534,11 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     sampled += B.items[i].n;
     sampled_work += B.items[i].n * std::max<uint32_t>(1, B.items[i].kind == K_SCAL ? B.items[i].k : 1);
   }
-  uint64_t CE = chunk_elems_for(rt, sampled / cnt * N);
+  uint64_t est = sampled / cnt * N;
+  // a stream launch's sub-epoch: units sized for the whole run (the launch
+  // has no per-round tail to balance), equal in every sub-epoch
+  if ((rt->sl.want || rt->sl.active) && rt->sl.cur_tasks) est = est * rt->sl.run_tasks / rt->sl.cur_tasks;
+  uint64_t CE = chunk_elems_for(rt, est);
   // a DAG's ready width can be far below the item count (C3: ~16 ready 4 MiB
   // tasks): smaller units keep all SMs busy (measured: 64 KiB units 14.6 ms
   // vs 256 KiB 17.2 ms on C3, tools/c3_chunks.py)
@@ -1701,6 +1706,7 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
       if (rt->sl.started && rt->sl.next < rt->sl.nsub) close_stream(rt);
       rt->sl.started = false;
       rt->sl.want = rt->sl.active = false;
+      rt->sl.run_tasks = rt->sl.cur_tasks = 0;
       for (EpochBuf *&b : rt->sl.bufs) {   // a run that failed before its deferred launch
         if (b) b->held = false;
         b = nullptr;
@@ -1717,6 +1723,7 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
     rt->sl.want = nsub >= 2 && nsub <= (unsigned)kMaxSubs;
     rt->sl.active = false;
     rt->sl.nsub = nsub;
+    rt->sl.run_tasks = local;
   }
   for (int rr = 0; rr < launches; ++rr) {
     const int rlo = bound[rr], rhi = bound[rr + 1];
@@ -1766,6 +1773,7 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
     const double tc = now_ms();
     if (pipelined) {
       B.ntasks = tbase + n;   // the round's epoch accounts the run (its items carry the tasks)
+      rt->sl.cur_tasks = sz;
       cudaStream_t st = rt->rstream[rr & 1];
       if (int e = flush_epoch(rt, st)) return e;
       CUDA_TRY(rt, cudaEventRecord(rt->ev_round[rr & 1], st));
