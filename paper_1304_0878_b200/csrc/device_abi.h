@@ -67,6 +67,27 @@ struct EpochArgs {
   unsigned *stream_abort;       // stream launch: the launch-wide abort flag (StreamCtl::abort), else null
 };
 
+// ---- direct launch: a tiny epoch of independent items (no edges) runs as
+// one plain grid over its items, described in the kernel parameters: no
+// queue, no counters, no blob upload (the paper's running example, C1, is
+// one such epoch: submit -> wait latency) ---------------------------------
+constexpr int kDirectItems = 16;        // items per direct launch (at most)
+constexpr int kDirectFactors = 256;     // chained factors per direct launch (at most)
+constexpr uint64_t kDirectElems = 1ull << 20;   // elements per direct launch (at most)
+struct DirectItem {
+  uint64_t x, y, n;   // as DItem
+  uint32_t kind;      // K_SCAL / K_AXPY / K_COPY
+  uint32_t k;         // SCAL: chained factors
+  uint32_t arg;       // SCAL: offset of its factors in DirectArgs::factors; AXPY: float bits of a
+  uint32_t pad;
+};
+struct DirectArgs {
+  uint32_t nitems;
+  uint32_t chunk;     // elements per CTA (grid.x covers the largest item; grid.y = items)
+  DirectItem items[kDirectItems];
+  float factors[kDirectFactors];
+};
+
 // ---- stream launch (one persistent launch consumes a growing
 // sequence of sub-epochs) ----------------------------------------------------
 // The pipelined rounds of one SCAL run are sub-epochs of ONE launch of the

@@ -31,6 +31,7 @@
 namespace bt {
 cudaError_t launch_epoch(const EpochArgs &args, int grid, cudaStream_t stream, int kernel);
 cudaError_t launch_stream(StreamCtl *ctl, uint64_t watchdog_ns, int grid, cudaStream_t stream, bool prefetch);
+cudaError_t launch_direct(const DirectArgs &args, unsigned grid_x, cudaStream_t stream);
 cudaError_t scheduler_occupancy(int *blocks_per_sm, int *block);
 cudaError_t scheduler_occupancy_wq(int *blocks_per_sm, int *block);
 cudaError_t launch_stage(void *dst, const void *src_mapped, size_t bytes, unsigned long long *q_empty, size_t nq,
@@ -858,6 +859,17 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     return 0;
   }
   e.timed = true;
+  // a tiny epoch of independent items: one direct launch, no blob (DirectArgs)
+  static const bool no_direct = getenv("BT_NO_DIRECT") != nullptr;   // comparisons
+  uint64_t total_elems = 0, max_n = 0, sum_k = 0;
+  bool direct = E == 0 && N <= (size_t)kDirectItems && !traced && !no_direct &&
+                !(rt->cfg.flags & (BT_FLAG_KERNEL_SW | BT_FLAG_KERNEL_RW | BT_FLAG_KERNEL_WQ));
+  for (size_t i = 0; direct && i < N; ++i) {
+    total_elems += B.items[i].n;
+    max_n = std::max<uint64_t>(max_n, B.items[i].n);
+    if (B.items[i].kind == K_SCAL) sum_k += B.items[i].k;
+  }
+  direct = direct && total_elems <= kDirectElems && max_n > 0 && sum_k <= (uint64_t)kDirectFactors;
   if (!rt->span_open) {
     CUDA_TRY(rt, cudaEventRecord(rt->span_start, stream));
     rt->span_open = true;
@@ -871,11 +883,15 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   bool uploads_pending = false;
   for (auto &kv2 : rt->caches) uploads_pending |= !kv2.second.uploads.empty();
   const bool sm_copy = uploads_pending || upload <= kStageBelow;
-  if (!sm_copy) CUDA_TRY(rt, cudaMemcpyAsync(d, h, upload, cudaMemcpyHostToDevice, stream));
-  rt->stats.kernel_launches += 2;   // the set-up kernel below and the scheduler kernel
-  CUDA_TRY(rt, launch_stage(d, sm_copy ? e.hblob_dev : nullptr, upload,
-                            reinterpret_cast<unsigned long long *>(d + o_queue) + U0, U - U0,
-                            reinterpret_cast<uint32_t *>(d + o_cdone), N, stream));
+  if (!direct) {
+    if (!sm_copy) CUDA_TRY(rt, cudaMemcpyAsync(d, h, upload, cudaMemcpyHostToDevice, stream));
+    rt->stats.kernel_launches += 2;   // the set-up kernel below and the scheduler kernel
+    CUDA_TRY(rt, launch_stage(d, sm_copy ? e.hblob_dev : nullptr, upload,
+                              reinterpret_cast<unsigned long long *>(d + o_queue) + U0, U - U0,
+                              reinterpret_cast<uint32_t *>(d + o_cdone), N, stream));
+  } else {
+    rt->stats.kernel_launches += 1;
+  }
 
   const int grid = (int)std::min<uint64_t>((uint64_t)rt->grid_max, U);
 
@@ -891,9 +907,35 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   rt->stats.grid = (uint32_t)kgrid;
   rt->stats.sched_launches += 1;
   rt->stats.block = kernel == 2 ? (uint32_t)rt->block_wq : (uint32_t)rt->block;
-  rt->ev("epoch buf %d seq %llu U %llu kernel %d grid %d stream %p", (int)(&e - rt->ep),
-         (unsigned long long)rt->ep_seq + 1, (unsigned long long)U, kernel, kgrid, (void *)stream);
-  CUDA_TRY(rt, launch_epoch(a, kgrid, stream, kernel));
+  rt->ev("epoch buf %d seq %llu U %llu kernel %d grid %d stream %p direct %d", (int)(&e - rt->ep),
+         (unsigned long long)rt->ep_seq + 1, (unsigned long long)U, kernel, kgrid, (void *)stream, (int)direct);
+  if (direct) {
+    DirectArgs da{};
+    da.nitems = (uint32_t)N;
+    da.chunk = 16384;
+    uint32_t fo = 0;
+    for (size_t i = 0; i < N; ++i) {
+      const HItem &it = B.items[i];
+      DirectItem &di2 = da.items[i];
+      di2.x = it.x;
+      di2.y = it.y;
+      di2.n = it.n;
+      di2.kind = it.kind;
+      di2.k = it.k;
+      if (it.kind == K_SCAL) {
+        memcpy(&da.factors[fo], B.factors(it), 4ull * it.k);
+        di2.arg = fo;
+        fo += it.k;
+      } else {
+        di2.arg = it.arg;
+      }
+    }
+    rt->stats.grid = (uint32_t)((max_n + da.chunk - 1) / da.chunk);
+    rt->stats.block = 256;
+    CUDA_TRY(rt, launch_direct(da, (unsigned)((max_n + da.chunk - 1) / da.chunk), stream));
+  } else {
+    CUDA_TRY(rt, launch_epoch(a, kgrid, stream, kernel));
+  }
   CUDA_TRY(rt, cudaEventRecord(e.end, stream));
   // write-back of host-homed ranges written for the first time since registration
   bool wb_waited = false;
@@ -919,6 +961,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   if (traced) CUDA_TRY(rt, cudaMemcpyAsync(h + o_trace_h, d + o_trace, 36 * U, cudaMemcpyDeviceToHost, stream));
   CUDA_TRY(rt, cudaEventRecord(e.done, stream));
   account();
+  if (direct) e.units = 0;   // no completion counters: retire checks done == 0
   static const bool dbg = getenv("BT_DEBUG_TIMING") != nullptr;
   if (dbg)
     fprintf(stderr, "flush_epoch N=%zu E=%zu U=%llu upload=%zu B: passA %.3f passB %.3f csr %.3f launch %.3f ms\n", N, E,

@@ -1648,6 +1648,39 @@ cudaError_t launch_stream(StreamCtl *ctl, uint64_t watchdog_ns, int grid, cudaSt
   return cudaGetLastError();
 }
 
+// Direct launch (device_abi.h DirectArgs): block (x, y) runs elements
+// [x * chunk, (x + 1) * chunk) of item y with the same bodies and the same
+// per-element arithmetic as the persistent kernels.
+__global__ void __launch_bounds__(256) direct_kernel(const __grid_constant__ DirectArgs p) {
+  __shared__ __align__(16) float sf[kDirectFactors];
+  const DirectItem &it = p.items[blockIdx.y];
+  const uint64_t lo = (uint64_t)blockIdx.x * p.chunk;
+  if (lo >= it.n) return;
+  const uint64_t n = min(it.n - lo, (uint64_t)p.chunk);
+  const int tid = threadIdx.x;
+  switch (it.kind) {
+    case K_SCAL:
+      for (uint32_t j = tid; j < it.k; j += blockDim.x) sf[j] = p.factors[it.arg + j];
+      __syncthreads();
+      scal_range<4, 256>(reinterpret_cast<float *>(it.x) + lo, n, sf, it.k, tid);
+      break;
+    case K_AXPY:
+      axpy_range<256>(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, n,
+                      __uint_as_float(it.arg), tid);
+      break;
+    case K_COPY:
+      copy_range<256>(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, n, tid);
+      break;
+    default:
+      break;
+  }
+}
+
+cudaError_t launch_direct(const DirectArgs &args, unsigned grid_x, cudaStream_t stream) {
+  direct_kernel<<<dim3(grid_x, args.nitems), 256, 0, stream>>>(args);
+  return cudaGetLastError();
+}
+
 // Host-side launcher (called from runtime.cpp).
 // kernel: 0 = sw, 1 = rw, 2 = wq, 3 = sw with prefetching SCAL bodies (short
 // chains); grid in CTAs of that kernel's block size.

@@ -50,6 +50,20 @@ def compare_program(program, **kw):
     return stats
 
 
+@pytest.mark.parametrize("seed", range(6))
+def test_direct_launch(B, seed):
+    """Epochs of independent items (each task its own epoch: epoch_tasks = 1)
+    run as direct launches -- one plain grid, items in the kernel parameters,
+    no queue -- with ragged, unaligned tiles and chained SCAL items; bit-exact."""
+    p = W.random_small_program(9000 + seed, max_tasks=60, max_handles=6, max_elems=5000)
+    stats = compare_program(p, epoch_tasks=1)
+    assert stats["epochs"] >= 1 and stats["units"] >= 1
+    p2 = W.c2_chain(nx=1 << 14, ntiles=16, sweeps=5)   # 16 fused items of k = 5 in one epoch
+    out, st = run_gpu(p2)
+    assert_bits_equal(out[0], oracle.run(p2)[0], "direct C2-shaped")
+    assert st["kernel_launches"] == 1 and st["block"] == 256, st
+
+
 def test_c1_paper_example(B):
     from tests.golden import load
     pins = load("scal_pins.txt")
