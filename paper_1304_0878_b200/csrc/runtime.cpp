@@ -210,6 +210,7 @@ struct bt_runtime {
     bool prefetch = false;
     bool started = false;
     uint64_t run_tasks = 0, cur_tasks = 0;   // local tasks of the run / of the sub-epoch being flushed
+    uint64_t max_tasks = 0;                  // local tasks of the run's largest sub-epoch
     EpochBuf *bufs[kMaxSubs] = {};    // the sub-epochs' buffers (bufs[0]'s start/end time the launch)
   } sl;
   cudaEvent_t ev_pub0 = nullptr;
@@ -496,6 +497,13 @@ int close_stream(bt_runtime *rt) {
   return 0;
 }
 
+// Default pipelined rounds of device-resident partitions are geometric
+// (bt_data_partition); BT_UNIFORM_ROUNDS=1 gives equal quarters (comparisons).
+bool geometric_rounds() {
+  static const bool uniform = getenv("BT_UNIFORM_ROUNDS") != nullptr;
+  return !uniform;
+}
+
 int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   Builder &B = rt->builder;
   if (B.items.empty()) {
@@ -666,13 +674,15 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   const size_t hneed = sub ? o_pub_h + 16 : align_up(o_trace_h + (traced ? 36 * U : 0), 16);
   if (sub && rt->sl.next == 0) {
     // before the launch: grow every reusable epoch buffer to 1.25 x this
-    // sub-epoch's needs (a run's rounds are near-equal parts of it), so the
-    // later sub-epochs find room without allocating
+    // sub-epoch's needs scaled to the run's largest sub-epoch (by tasks), so
+    // the later sub-epochs find room without allocating
+    const double grow = 1.25 * (double)std::max(rt->sl.max_tasks, rt->sl.cur_tasks) /
+                        (double)std::max<uint64_t>(1, rt->sl.cur_tasks);
     for (EpochBuf &c : rt->ep) {
       if (&c == &e || c.held || (c.inflight && cudaEventQuery(c.done) == cudaErrorNotReady)) continue;
       if (int r = retire(rt, c)) return r;
-      if (int r = ensure_host(rt, c, hneed + hneed / 4)) return r;
-      if (int r = ensure_dev(rt, c, dneed + dneed / 4)) return r;
+      if (int r = ensure_host(rt, c, (size_t)(grow * (double)hneed) + 4096)) return r;
+      if (int r = ensure_dev(rt, c, (size_t)(grow * (double)dneed) + 4096)) return r;
     }
   }
   if (int r = ensure_host(rt, e, hneed)) return r;
@@ -1344,7 +1354,15 @@ int bt_data_partition(bt_runtime *rt, bt_handle h, uint32_t nparts) {
     // pipelined rounds take contiguous quarters of the parts (so round r
     // needs only its own upload chunks and writes back one contiguous range);
     // lanes still own whole 64-slot blocks
-    const uint32_t round = (uint32_t)((uint64_t)t * rounds / nparts);
+    uint32_t round = (uint32_t)((uint64_t)t * rounds / nparts);
+    if (rounds == 4 && geometric_rounds()) {
+      // device-resident data: geometric rounds 1/16, 2/16, 4/16, 9/16 of the
+      // parts, so the device starts after building 1/16 of a run; each later
+      // round is built while the previous one runs (the host builds a round
+      // in about 0.6x the device time of one of the same size)
+      const uint64_t q = (uint64_t)t * 16 / nparts;
+      round = q < 1 ? 0 : q < 3 ? 1 : q < 7 ? 2 : 3;
+    }
     ch.grp = round * (uint32_t)rt->npool + ((c0 + t) >> 6) % (uint32_t)rt->npool;
   }
   p.nparts = nparts;
@@ -1726,8 +1744,13 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
     const size_t want = std::max<size_t>(1, std::min<size_t>((size_t)nonempty, local / per));
     size_t cum = 0;
     size_t j = 0;
+    int idx = 0;
     for (int r = 0; r < R; ++r) {
-      const size_t jr = local ? std::min(want - 1, cum * want / local) : 0;   // launch of round r
+      // every nonempty round its own launch when they are few enough, else
+      // rounds merged into `want` launches of balanced task counts
+      const size_t jr = (size_t)nonempty <= want ? (size_t)(round_size[r] ? idx++ : std::max(idx - 1, 0))
+                        : local ? std::min(want - 1, cum * want / local)
+                                : 0;   // launch of round r
       if (jr != j && round_size[r]) {
         bound.push_back(r);
         j = jr;
@@ -1758,10 +1781,12 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
   } sl_reset{rt};
   if (pipelined && rt->sctl) {
     unsigned nsub = 0;
+    rt->sl.max_tasks = 0;
     for (int rr = 0; rr < launches; ++rr) {
       size_t sz = 0;
       for (int r = bound[rr]; r < bound[rr + 1]; ++r) sz += round_size[r];
       nsub += sz != 0;
+      rt->sl.max_tasks = std::max<uint64_t>(rt->sl.max_tasks, sz);
     }
     rt->sl.want = nsub >= 2 && nsub <= (unsigned)kMaxSubs;
     rt->sl.active = false;
