@@ -678,11 +678,13 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     // the later sub-epochs find room without allocating
     const double grow = 1.25 * (double)std::max(rt->sl.max_tasks, rt->sl.cur_tasks) /
                         (double)std::max<uint64_t>(1, rt->sl.cur_tasks);
+    const size_t want_h = (size_t)(grow * (double)hneed) + 4096, want_d = (size_t)(grow * (double)dneed) + 4096;
     for (EpochBuf &c : rt->ep) {
-      if (&c == &e || c.held || (c.inflight && cudaEventQuery(c.done) == cudaErrorNotReady)) continue;
+      if (&c == &e || c.held || (c.hcap >= want_h && c.dcap >= want_d)) continue;
+      if (c.inflight && cudaEventQuery(c.done) == cudaErrorNotReady) continue;
       if (int r = retire(rt, c)) return r;
-      if (int r = ensure_host(rt, c, (size_t)(grow * (double)hneed) + 4096)) return r;
-      if (int r = ensure_dev(rt, c, (size_t)(grow * (double)dneed) + 4096)) return r;
+      if (int r = ensure_host(rt, c, want_h)) return r;
+      if (int r = ensure_dev(rt, c, want_d)) return r;
     }
   }
   if (int r = ensure_host(rt, e, hneed)) return r;
@@ -866,6 +868,10 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     e.timed = r == 0;
     if (++rt->sl.next == rt->sl.nsub) rt->sl.active = false;
     account();
+    static const bool dbg_t = getenv("BT_DEBUG_TIMING") != nullptr;
+    if (dbg_t)
+      fprintf(stderr, "flush sub %u N=%zu U=%llu: passA %.3f passB %.3f csr %.3f copies+launch %.3f ms\n", r, N,
+              (unsigned long long)U, tA - t0, tB - tA, tC - tB, now_ms() - tC);
     return 0;
   }
   e.timed = true;
