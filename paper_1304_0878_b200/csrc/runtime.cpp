@@ -1361,11 +1361,14 @@ int bt_data_partition(bt_runtime *rt, bt_handle h, uint32_t nparts) {
     // needs only its own upload chunks and writes back one contiguous range);
     // lanes still own whole 64-slot blocks
     uint32_t round = (uint32_t)((uint64_t)t * rounds / nparts);
-    if (rounds == 4 && geometric_rounds()) {
-      // device-resident data: geometric rounds 1/16, 2/16, 4/16, 9/16 of the
-      // parts, so the device starts after building 1/16 of a run; each later
-      // round is built while the previous one runs (the host builds a round
-      // in about 0.6x the device time of one of the same size)
+    if (rounds == 4 && rt->builder.fusion && geometric_rounds()) {
+      // device-resident data, fusion on: geometric rounds 1/16, 2/16, 4/16,
+      // 9/16 of the parts, so the device starts after building 1/16 of a run;
+      // each later round is built while the previous one runs (fused chains
+      // make the device the slower side: C5 step 2.51 -> 2.40-2.45 ms).
+      // Unfused runs are host-bound (C4: ~4 ns of build per task on 14
+      // threads vs ~1 ns of device time), where a large last round would
+      // leave the device the whole 9/16 after the host is done: equal rounds
       const uint64_t q = (uint64_t)t * 16 / nparts;
       round = q < 1 ? 0 : q < 3 ? 1 : q < 7 ? 2 : 3;
     }
