@@ -209,6 +209,7 @@ struct bt_runtime {
     unsigned nsub = 0, next = 0;
     bool prefetch = false;
     bool started = false;
+    bool launched = false;   // the run's launch is enqueued
     uint64_t run_tasks = 0, cur_tasks = 0;   // local tasks of the run / of the sub-epoch being flushed
     uint64_t max_tasks = 0;                  // local tasks of the run's largest sub-epoch
     EpochBuf *bufs[kMaxSubs] = {};    // the sub-epochs' buffers (bufs[0]'s start/end time the launch)
@@ -478,6 +479,28 @@ inline void range_of(size_t n, int P, int p, size_t &lo, size_t &hi) {
   hi = n * (size_t)(p + 1) / (size_t)P;
 }
 
+// Enqueue the run's stream launch on rstream[0] (after sub-epoch 0's copies;
+// deferred: after the last publication).  Held (deferred) sub-epochs complete
+// with it.
+int enqueue_stream_launch(bt_runtime *rt) {
+  cudaStream_t ls = rt->rstream[0];
+  EpochBuf &e0 = *rt->sl.bufs[0];
+  CUDA_TRY(rt, cudaEventRecord(e0.start, ls));
+  rt->stats.grid = (uint32_t)rt->grid_max;
+  rt->stats.block = (uint32_t)rt->block;
+  rt->stats.kernel_launches += 1;
+  rt->stats.sched_launches += 1;
+  CUDA_TRY(rt, launch_stream(rt->sctl, kWatchdogNs, rt->grid_max, ls, rt->sl.prefetch));
+  CUDA_TRY(rt, cudaEventRecord(e0.end, ls));
+  for (EpochBuf *b : rt->sl.bufs)
+    if (b && b->held) {
+      CUDA_TRY(rt, cudaEventRecord(b->done, ls));
+      b->held = false;
+    }
+  rt->sl.launched = true;
+  return 0;
+}
+
 // End the running stream launch early: sub-epochs next..nsub-1 are published
 // empty (zero EpochArgs: no units), so its CTAs finish.  Copies from a pinned
 // table whose contents never change (published value q + 1 at index q, then a
@@ -491,6 +514,11 @@ int close_stream(bt_runtime *rt) {
     CUDA_TRY(rt, cudaMemcpyAsync(&rt->sctl->published, &pub[q], 4, cudaMemcpyHostToDevice, up));
   }
   rt->ev("close stream launch at sub %u of %u", rt->sl.next, rt->sl.nsub);
+  if (!rt->sl.launched && rt->sl.bufs[0]) {   // deferred launch not enqueued yet: enqueue it now
+    CUDA_TRY(rt, cudaEventRecord(rt->ev_pub0, up));
+    CUDA_TRY(rt, cudaStreamWaitEvent(rt->rstream[0], rt->ev_pub0, 0));
+    if (int rc = enqueue_stream_launch(rt)) return rc;
+  }
   rt->sl.next = rt->sl.nsub;
   rt->sl.active = false;
   rt->stats.stream_closes += 1;
@@ -639,6 +667,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     rt->sl.active = (kernel == 0 || kernel == 3) && !traced && rt->caches.empty() &&
                     !(rt->cfg.flags & BT_FLAG_SYNC_EPOCH) && rt->sctl && rt->sl.nsub >= 2;
     rt->sl.next = 0;
+    rt->sl.launched = false;
     rt->sl.prefetch = kernel == 3;
     rt->sl.started = rt->sl.active;
   }
@@ -847,20 +876,8 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
       CUDA_TRY(rt, cudaEventRecord(rt->ev_pub0, up));
       CUDA_TRY(rt, cudaStreamWaitEvent(ls, rt->ev_pub0, 0));
     }
-    if (defer ? r + 1 == rt->sl.nsub : r == 0) {
-      EpochBuf &e0 = *rt->sl.bufs[0];
-      CUDA_TRY(rt, cudaEventRecord(e0.start, ls));
-      rt->stats.grid = (uint32_t)rt->grid_max;
-      rt->stats.block = (uint32_t)rt->block;
-      rt->stats.kernel_launches += 1;
-      rt->stats.sched_launches += 1;
-      CUDA_TRY(rt, launch_stream(rt->sctl, kWatchdogNs, rt->grid_max, ls, rt->sl.prefetch));
-      CUDA_TRY(rt, cudaEventRecord(e0.end, ls));
-      for (unsigned q = 0; q < r; ++q) {   // deferred: the earlier sub-epochs complete with the launch
-        CUDA_TRY(rt, cudaEventRecord(rt->sl.bufs[q]->done, ls));
-        rt->sl.bufs[q]->held = false;
-      }
-    }
+    if (defer ? r + 1 == rt->sl.nsub : r == 0)
+      if (int rc = enqueue_stream_launch(rt)) return rc;
     // after the launch (which ends once every sub-epoch ran); deferred and not
     // yet launched: held (not reusable) until the launch is enqueued
     e.held = defer && r + 1 < rt->sl.nsub;
@@ -1779,7 +1796,7 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
         fprintf(stderr, "btask: stream launch published %u of %u sub-epochs\n", rt->sl.next, rt->sl.nsub);
       // a run that failed part-way: end its launch (no CTA waits for the watchdog)
       if (rt->sl.started && rt->sl.next < rt->sl.nsub) close_stream(rt);
-      rt->sl.started = false;
+      rt->sl.started = rt->sl.launched = false;
       rt->sl.want = rt->sl.active = false;
       rt->sl.run_tasks = rt->sl.cur_tasks = 0;
       for (EpochBuf *&b : rt->sl.bufs) {   // a run that failed before its deferred launch

@@ -381,6 +381,12 @@ def test_stream_launch_deferred(B, tmp_path):
         "                         parallel_min=200, host_threads=3)\n"
         "    assert_bits_equal(out[0], oracle.run(repeated(p, 2))[0], 'deferred stream launch')\n"
         "    assert st['sched_launches'] == 2 and st['epochs'] >= 4, st\n"
+        "from tests.test_gpu import uneven_rounds_program\n"
+        "q = uneven_rounds_program()\n"
+        "out, st = run_device(B, q, repeats=2, pipeline_rounds=4, pipeline_min=500, parallel_min=500,\n"
+        "                     host_threads=3)\n"
+        "assert_bits_equal(out[0], oracle.run(repeated(q, 2))[0], 'deferred launch closed early')\n"
+        "assert st['stream_closes'] >= 1, st\n"
         "print('ok')\n")
     import os
     env = dict(os.environ, BT_STREAM_DEFER="1")
@@ -389,11 +395,7 @@ def test_stream_launch_deferred(B, tmp_path):
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
-def test_stream_launch_closes_early(B):
-    """Rounds of very different sizes: a later round outgrows the epoch
-    buffers sized at the first one, closes the running launch (its remaining
-    sub-epochs are published empty) and runs as ordinary epochs -- no
-    allocation while the launch waits, same results."""
+def uneven_rounds_program():
     rng = np.random.default_rng(77)
     nparts, tile = 400, 8192
     x = W.unit_interval_floats(rng, nparts * tile)
@@ -408,7 +410,15 @@ def test_stream_launch_closes_early(B):
     tasks = W._tasks(len(rows))
     for i, r in enumerate(rows):
         tasks[i] = r
-    p = W.Program([x], [nparts], tasks, name="uneven rounds")
+    return W.Program([x], [nparts], tasks, name="uneven rounds")
+
+
+def test_stream_launch_closes_early(B):
+    """Rounds of very different sizes: a later round outgrows the epoch
+    buffers sized at the first one, closes the running launch (its remaining
+    sub-epochs are published empty) and runs as ordinary epochs -- no
+    allocation while the launch waits, same results."""
+    p = uneven_rounds_program()
     out, st = run_device(B, p, repeats=2, pipeline_rounds=4, pipeline_min=500, parallel_min=500, host_threads=3)
     assert_bits_equal(out[0], oracle.run(repeated(p, 2))[0], "uneven rounds")
     assert st["stream_closes"] >= 1, st
