@@ -1081,7 +1081,7 @@ int bt_init(const bt_config *cfg_in, bt_runtime **out) {
   rt->host_only = (cfg.flags & BT_FLAG_HOST_ONLY) != 0;
   rt->builder.fusion = (cfg.flags & BT_FLAG_NO_FUSION) == 0;
   rt->builder.max_fused = cfg.max_fused;
-  rt->builder.record_tasks = rt->host_only;
+  rt->builder.record_tasks = rt->host_only && getenv("BT_HOST_NORECORD") == nullptr;   // (env: host benchmarks)
   int threads = cfg.host_threads;
   if (threads == 0) {
     // leave two cores to the CUDA driver / caller threads (measured: 14 of 16 beats 16 of 16)

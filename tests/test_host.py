@@ -347,3 +347,36 @@ def test_rank_filter_and_cross_rank_error(B):
     rt.unregister(hx)
     rt.unregister(hy)
     rt.close()
+
+
+def test_stats_struct_matches_header(B):
+    """The binding's bt_stats mirrors the header's field order (ABI drift guard)."""
+    src = open(HEADER).read()
+    body = re.search(r"typedef struct bt_stats \{(.*?)\} bt_stats;", src, flags=re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = re.findall(r"\b(\w+)\s*;", body)
+    assert [f for f, _ in B.bt_stats._fields_] == fields
+
+
+def test_device_abi_layout(tmp_path):
+    """Host-written offsets of the device ABI (runtime.cpp writes StreamCtl's
+    header by offset; DirectArgs travels as a kernel parameter, <= 4 KiB)."""
+    src = tmp_path / "abi.cpp"
+    src.write_text('#include <cstdio>\n#include <cstddef>\n#include "device_abi.h"\nusing namespace bt;\n'
+                   'int main() { printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(EpochArgs), offsetof(StreamCtl, nsub), '
+                   'offsetof(StreamCtl, subs), sizeof(StreamCtl), sizeof(DirectArgs), sizeof(DirectItem)); }\n')
+    exe = tmp_path / "abi"
+    subprocess.check_call(["g++", "-std=c++17", "-I", os.path.join(ROOT, "paper_1304_0878_b200", "csrc"), str(src),
+                           "-o", str(exe)])
+    ea, nsub, subs, sc, da, di = map(int, subprocess.check_output([str(exe)], text=True).split())
+    assert nsub == 20 and subs == 64 and sc % 64 == 0 and sc >= 64 + 16 * ea
+    assert da <= 4096 and di == 40
+
+
+def test_library_contains_every_kernel(B):
+    """sm_100a SASS for the persistent kernels, the stream launch, the direct
+    launch and the set-up kernel."""
+    out = subprocess.check_output(["cuobjdump", "--list-text", B.LIB_PATH], text=True)
+    for k in ("scheduler_kernel_sw", "scheduler_kernel_sws", "scheduler_kernel_rw", "scheduler_kernel_wq",
+              "direct_kernel", "stage_kernel"):
+        assert k in out, k
