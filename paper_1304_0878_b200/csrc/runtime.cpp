@@ -576,6 +576,11 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   // has no per-round tail to balance), equal in every sub-epoch
   if ((rt->sl.want || rt->sl.active) && rt->sl.cur_tasks) est = est * rt->sl.run_tasks / rt->sl.cur_tasks;
   uint64_t CE = chunk_elems_for(rt, est);
+  // the last sub-epoch of a stream launch ends the launch: smaller units there
+  // shorten its tail (BT_TAIL_SPLIT = divisor, experiments)
+  static const uint64_t tail_split = getenv("BT_TAIL_SPLIT") ? strtoull(getenv("BT_TAIL_SPLIT"), nullptr, 10) : 1;
+  if (rt->sl.active && rt->sl.next + 1 == rt->sl.nsub && tail_split > 1 && !rt->cfg.chunk_bytes)
+    CE = std::max<uint64_t>(kMinChunkElems, CE / tail_split) / 8 * 8;
   // a DAG's ready width can be far below the item count (C3: ~16 ready 4 MiB
   // tasks): smaller units keep all SMs busy (measured: 64 KiB units 14.6 ms
   // vs 256 KiB 17.2 ms on C3, tools/c3_chunks.py)
