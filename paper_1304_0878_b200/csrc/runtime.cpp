@@ -103,6 +103,8 @@ struct Slot {
   bool owns_dev = false;      // root only: runtime-allocated replica
   bool ipc_alloc = false;     // root only: replica from cudaMalloc (shareable with other ranks)
   uint64_t reg_key = 0;       // root only: registration ordinal (equal on all ranks)
+  uint8_t prounds = 0;        // partitioned parent: rounds its parts were dealt to
+  bool pgeo = false;          // ... geometrically (round_of)
 };
 
 struct EpochBuf {
@@ -530,6 +532,16 @@ int close_stream(bt_runtime *rt) {
 bool geometric_rounds() {
   static const bool uniform = getenv("BT_UNIFORM_ROUNDS") != nullptr;
   return !uniform;
+}
+
+// Round of part t of n dealt to `rounds` rounds: contiguous equal shares, or
+// (geo, 4 rounds) geometric shares 1/16, 2/16, 4/16, 9/16 -- see bt_data_partition.
+uint32_t round_of(uint64_t t, uint64_t n, uint32_t rounds, bool geo) {
+  if (geo) {
+    const uint64_t q = t * 16 / n;
+    return q < 1 ? 0 : q < 3 ? 1 : q < 7 ? 2 : 3;
+  }
+  return (uint32_t)(t * rounds / n);
 }
 
 int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
@@ -1382,18 +1394,18 @@ int bt_data_partition(bt_runtime *rt, bt_handle h, uint32_t nparts) {
     // pipelined rounds take contiguous quarters of the parts (so round r
     // needs only its own upload chunks and writes back one contiguous range);
     // lanes still own whole 64-slot blocks
-    uint32_t round = (uint32_t)((uint64_t)t * rounds / nparts);
-    if (rounds == 4 && rt->builder.fusion && geometric_rounds()) {
-      // device-resident data, fusion on: geometric rounds 1/16, 2/16, 4/16,
-      // 9/16 of the parts, so the device starts after building 1/16 of a run;
-      // each later round is built while the previous one runs (fused chains
-      // make the device the slower side: C5 step 2.51 -> 2.40-2.45 ms).
-      // Unfused runs are host-bound (C4: ~4 ns of build per task on 14
-      // threads vs ~1 ns of device time), where a large last round would
-      // leave the device the whole 9/16 after the host is done: equal rounds
-      const uint64_t q = (uint64_t)t * 16 / nparts;
-      round = q < 1 ? 0 : q < 3 ? 1 : q < 7 ? 2 : 3;
-    }
+    // device-resident data, fusion on: geometric rounds 1/16, 2/16, 4/16,
+    // 9/16 of the parts, so the device starts after building 1/16 of a run;
+    // each later round is built while the previous one runs (fused chains
+    // make the device the slower side: C5 step 2.51 -> 2.40-2.45 ms).
+    // Unfused runs are host-bound (C4: ~4 ns of build per task on 14
+    // threads vs ~1 ns of device time), where a large last round would
+    // leave the device the whole 9/16 after the host is done: equal rounds.
+    // (Parts owned by several ranks are re-dealt per rank: scal_run_parallel.)
+    const bool geo = rounds == 4 && rt->builder.fusion && geometric_rounds();
+    const uint32_t round = round_of(t, nparts, rounds, geo);
+    p.prounds = (uint8_t)rounds;
+    p.pgeo = geo;
     ch.grp = round * (uint32_t)rt->npool + ((c0 + t) >> 6) % (uint32_t)rt->npool;
   }
   p.nparts = nparts;
@@ -1643,6 +1655,22 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
     };
     if (nslots >= 65536) rt->par(fill);
     else fill(0);
+    // a partition whose parts are spread over ranks (owner-computes): deal
+    // THIS rank's parts to the rounds, so its share of a run still pipelines
+    for (size_t x = 0; x < nslots; ++x) {
+      const Slot &ps = rt->slots[x];
+      if (!ps.nparts || !ps.prounds || !(hot[x].flags & F_LIVE)) continue;
+      const uint32_t c0 = ps.first_child, n = ps.nparts;
+      uint64_t L = 0;
+      for (uint32_t t = 0; t < n; ++t) L += hot[c0 + t].rank == myrank;
+      if (L == 0 || L == n) continue;
+      uint64_t j = 0;
+      for (uint32_t t = 0; t < n; ++t) {
+        if (hot[c0 + t].rank != myrank) continue;
+        const uint32_t grp = round_of(j++, L, ps.prounds, ps.pgeo) * (uint32_t)P + ((c0 + t) >> 6) % (uint32_t)P;
+        key[c0 + t] = (key[c0 + t] & ~0xFFFFFFFEull) | ((uint64_t)(grp & 0x7FFFFFFFu) << 1);
+      }
+    }
     rt->key_dirty = false;
   }
   const uint64_t *kt = rt->key.data();

@@ -620,6 +620,23 @@ def test_cross_rank_reads_random_programs(B, batch):
         _check_owned(p, results, owners)
 
 
+def test_cross_rank_c3_dag_and_sharded_sweeps(B):
+    """C3-shaped random DAG (AXPY/COPY across owners -> many rendezvous) and a
+    C5-shaped owner-computes sweep (tile halves per rank; each rank's local
+    run is a pipelined stream launch) over two ranks: every owner's data is
+    the oracle's."""
+    from tests import xrank
+    p = W.c3_random_dag(nbuf=12, nx=1 << 13, ntasks=400, seed=4711)
+    results, stats, owners = xrank.run(p, nranks=2, seed=5)
+    _check_owned(p, results, owners)
+    q = W.c5_sharded(nx=512 * 8192, ntiles=512, sweeps=8)
+    owners = [[0 if t < 256 else 1 for t in range(512)]]
+    results, stats, owners = xrank.run(q, nranks=2, owners=owners,
+                                       rt_kwargs=dict(pipeline_min=256, parallel_min=256))
+    _check_owned(q, results, owners)
+    assert all(st["sched_launches"] < st["epochs"] for st in stats), [(st["epochs"], st["sched_launches"], st["stream_closes"], st["kernel_launches"], st["grid"], st["block"]) for st in stats]
+
+
 def test_cross_rank_write_after_read(B):
     """WAR across ranks: X (rank 0) is read by rank 1 (COPY X->Y), then
     overwritten by rank 0 right away; rank 1 must still see the old X.  Also

@@ -37,7 +37,8 @@ def leaf_ranges(program, b: int):
     return [(t, *tile_range(nx, program.nparts[b], t)) for t in range(program.nparts[b])]
 
 
-def worker(rank: int, nranks: int, name: str, program, owners, batch: bool, barrier, q, flags: int = 0):
+def worker(rank: int, nranks: int, name: str, program, owners, batch: bool, barrier, q, flags: int = 0,
+           rt_kwargs=None):
     try:
         sys.path.insert(0, ROOT)
         import numpy as np
@@ -47,7 +48,7 @@ def worker(rank: int, nranks: int, name: str, program, owners, batch: bool, barr
         torch.cuda.set_device(0)
         tensors = [torch.from_numpy(b.copy()).cuda() for b in program.buffers]
         torch.cuda.synchronize()
-        rt = B.Runtime(rank=rank, nranks=nranks, flags=flags)
+        rt = B.Runtime(rank=rank, nranks=nranks, flags=flags, **(rt_kwargs or {}))
         rt.comm_init(name)
         s = Session(rt, program, device_tensors=tensors)
         for b, own in enumerate(owners):
@@ -76,7 +77,7 @@ def worker(rank: int, nranks: int, name: str, program, owners, batch: bool, barr
 
 
 def run(program, nranks: int = 2, seed: int = 0, batch: bool = True, timeout: float = 240.0, owners=None,
-        flags: int = 0):
+        flags: int = 0, rt_kwargs=None):
     """Run `program` on nranks processes; returns ({(b, tile): owned data}, [stats per rank], owners)."""
     import multiprocessing as mp
     import uuid
@@ -86,7 +87,7 @@ def run(program, nranks: int = 2, seed: int = 0, batch: bool = True, timeout: fl
     name = f"/bt-test-{os.getpid()}-{uuid.uuid4().hex[:8]}"
     q = ctx.Queue()
     barrier = ctx.Barrier(nranks)
-    procs = [ctx.Process(target=worker, args=(r, nranks, name, program, owners, batch, barrier, q, flags))
+    procs = [ctx.Process(target=worker, args=(r, nranks, name, program, owners, batch, barrier, q, flags, rt_kwargs))
              for r in range(nranks)]
     for p in procs:
         p.start()
