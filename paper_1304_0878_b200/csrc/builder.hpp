@@ -411,11 +411,42 @@ void Builder::lane_runs(Lane &L, const LaneEntry *const *chunks, const uint32_t 
         prev = w;
       }
     }
+    const auto g = geom(s);
+    auto chain_rest = [&]() {
+      if (!(i < m && prev != NONE)) return;
+      // the rest of the run: a chain of items, each the single successor of
+      // the previous one (the common case: unfused sweeps, long fused runs);
+      // written in place, no per-item vector growth
+      const uint32_t step = fusion ? max_fused : 1u;
+      const uint32_t cnt_items = (m - i + step - 1) / step;
+      size_t li = L.items.size(), le = L.edges.size();
+      L.items.resize(li + cnt_items);
+      L.edges.resize(le + cnt_items);
+      HItem *IT = L.items.data();
+      uint64_t *ED = L.edges.data();
+      if (prev & TAG) ++IT[prev & ~TAG].nsucc;
+      else __atomic_fetch_add(&items[prev].nsucc, 1u, __ATOMIC_RELAXED);
+      for (uint32_t q = 0; q < cnt_items; ++q, ++li, ++le) {
+        const uint32_t take = std::min(m - i, step);
+        const uint32_t t = TAG | (uint32_t)li;
+        IT[li] = HItem{1, take, s, NONE, g.first, 0, g.second, 0, TAG | (b + i), take, 1, q + 1 < cnt_items ? 1u : 0u,
+                       NONE};
+        ED[le] = ((uint64_t)prev << 32) | t;
+        if (record_tasks)
+          for (uint32_t r = 0; r < take; ++r) {
+            L.recorded.push_back(((uint64_t)L.tasks[b + i + r] << 32) | t);
+            task_pos[L.tasks[b + i + r]] = r;
+          }
+        L.fused += take - 1;
+        prev = t;
+        i += take;
+      }
+    };
+    chain_rest();
     while (i < m) {
       const uint32_t take = fusion ? std::min(m - i, max_fused) : 1u;
       const uint32_t local = (uint32_t)L.items.size();
       const uint32_t t = TAG | local;
-      const auto g = geom(s);
       L.items.push_back(HItem{1, take, s, NONE, g.first, 0, g.second, 0, TAG | (b + i), take, 0, 0, NONE});
       uint32_t np = 0;
       auto link = [&](uint32_t p) {
@@ -450,6 +481,7 @@ void Builder::lane_runs(Lane &L, const LaneEntry *const *chunks, const uint32_t 
       L.fused += take - 1;
       prev = t;
       i += take;
+      chain_rest();
     }
     st.writer = prev;
     st.ext = NONE;
