@@ -67,13 +67,16 @@ struct EpochArgs {
   unsigned *stream_abort;       // stream launch: the launch-wide abort flag (StreamCtl::abort), else null
 };
 
-// ---- direct launch: a tiny epoch of independent items (no edges) runs as
-// one plain grid over its items, described in the kernel parameters: no
-// queue, no counters, no blob upload (the paper's running example, C1, is
-// one such epoch: submit -> wait latency) ---------------------------------
-constexpr int kDirectItems = 16;        // items per direct launch (at most)
-constexpr int kDirectFactors = 256;     // chained factors per direct launch (at most)
-constexpr uint64_t kDirectElems = 1ull << 20;   // elements per direct launch (at most)
+// ---- direct launch: an epoch of a few hundred independent items (no edges)
+// runs as one plain grid over its items, described in the kernel parameters:
+// no queue, no counters, no blob upload (the paper's running example C1 and
+// the fused C2 chain -- 256 items of k = 16 -- are such epochs) --------------
+// Two sizes: a small parameter block for tiny epochs (the launch copies the
+// whole block: C1's latency), a large one (kernel parameters may take up to
+// 32,764 bytes since CUDA 12.1) for epochs of up to 512 items.
+constexpr int kDirectItemsSmall = 16, kDirectFactorsSmall = 256;
+constexpr int kDirectItems = 512;       // items per direct launch (at most)
+constexpr int kDirectFactors = 1024;    // distinct chained factors per direct launch (at most)
 struct DirectItem {
   uint64_t x, y, n;   // as DItem
   uint32_t kind;      // K_SCAL / K_AXPY / K_COPY
@@ -81,12 +84,15 @@ struct DirectItem {
   uint32_t arg;       // SCAL: offset of its factors in DirectArgs::factors; AXPY: float bits of a
   uint32_t pad;
 };
-struct DirectArgs {
+template <int NI, int NF>
+struct DirectArgsT {
   uint32_t nitems;
   uint32_t chunk;     // elements per CTA (grid.x covers the largest item; grid.y = items)
-  DirectItem items[kDirectItems];
-  float factors[kDirectFactors];
+  DirectItem items[NI];
+  float factors[NF];
 };
+using DirectArgs = DirectArgsT<kDirectItems, kDirectFactors>;
+using DirectArgsSmall = DirectArgsT<kDirectItemsSmall, kDirectFactorsSmall>;
 
 // ---- stream launch (one persistent launch consumes a growing
 // sequence of sub-epochs) ----------------------------------------------------

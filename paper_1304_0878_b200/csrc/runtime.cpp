@@ -911,15 +911,17 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   e.timed = true;
   // a tiny epoch of independent items: one direct launch, no blob (DirectArgs)
   static const bool no_direct = getenv("BT_NO_DIRECT") != nullptr;   // comparisons
-  uint64_t total_elems = 0, max_n = 0, sum_k = 0;
+  uint64_t max_n = 0;
   bool direct = E == 0 && N <= (size_t)kDirectItems && !traced && !no_direct &&
                 !(rt->cfg.flags & (BT_FLAG_KERNEL_SW | BT_FLAG_KERNEL_RW | BT_FLAG_KERNEL_WQ));
+  // distinct factor lists (consecutive equal lists shared, as in pass B)
+  uint64_t dfac = 0;
   for (size_t i = 0; direct && i < N; ++i) {
-    total_elems += B.items[i].n;
-    max_n = std::max<uint64_t>(max_n, B.items[i].n);
-    if (B.items[i].kind == K_SCAL) sum_k += B.items[i].k;
+    const HItem &it = B.items[i];
+    max_n = std::max<uint64_t>(max_n, it.n);
+    if (it.kind == K_SCAL && (it.k == 1 || !rt->cursor[i])) dfac += it.k;
   }
-  direct = direct && total_elems <= kDirectElems && max_n > 0 && sum_k <= (uint64_t)kDirectFactors;
+  direct = direct && max_n > 0 && dfac <= (uint64_t)kDirectFactors;
   if (!rt->span_open) {
     CUDA_TRY(rt, cudaEventRecord(rt->span_start, stream));
     rt->span_open = true;
@@ -963,7 +965,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     DirectArgs da{};
     da.nitems = (uint32_t)N;
     da.chunk = 16384;
-    uint32_t fo = 0;
+    uint32_t fo = 0, prev_fo = 0;
     for (size_t i = 0; i < N; ++i) {
       const HItem &it = B.items[i];
       DirectItem &di2 = da.items[i];
@@ -973,9 +975,14 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
       di2.kind = it.kind;
       di2.k = it.k;
       if (it.kind == K_SCAL) {
-        memcpy(&da.factors[fo], B.factors(it), 4ull * it.k);
-        di2.arg = fo;
-        fo += it.k;
+        if (it.k == 1 || !rt->cursor[i]) {   // rt->cursor[i] == 1: same list as the previous k > 1 item
+          memcpy(&da.factors[fo], B.factors(it), 4ull * it.k);
+          if (it.k > 1) prev_fo = fo;
+          di2.arg = fo;
+          fo += it.k;
+        } else {
+          di2.arg = prev_fo;
+        }
       } else {
         di2.arg = it.arg;
       }

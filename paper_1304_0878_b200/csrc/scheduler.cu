@@ -1651,8 +1651,9 @@ cudaError_t launch_stream(StreamCtl *ctl, uint64_t watchdog_ns, int grid, cudaSt
 // Direct launch (device_abi.h DirectArgs): block (x, y) runs elements
 // [x * chunk, (x + 1) * chunk) of item y with the same bodies and the same
 // per-element arithmetic as the persistent kernels.
-__global__ void __launch_bounds__(256) direct_kernel(const __grid_constant__ DirectArgs p) {
-  __shared__ __align__(16) float sf[kDirectFactors];
+template <class Args>
+__global__ void __launch_bounds__(256) direct_kernel(const __grid_constant__ Args p) {
+  __shared__ __align__(16) float sf[sizeof(p.factors) / sizeof(float)];
   const DirectItem &it = p.items[blockIdx.y];
   const uint64_t lo = (uint64_t)blockIdx.x * p.chunk;
   if (lo >= it.n) return;
@@ -1677,7 +1678,22 @@ __global__ void __launch_bounds__(256) direct_kernel(const __grid_constant__ Dir
 }
 
 cudaError_t launch_direct(const DirectArgs &args, unsigned grid_x, cudaStream_t stream) {
-  direct_kernel<<<dim3(grid_x, args.nitems), 256, 0, stream>>>(args);
+  if (args.nitems <= (uint32_t)kDirectItemsSmall) {
+    // the small parameter block, if the factors fit
+    uint32_t nf = 0;
+    for (uint32_t i = 0; i < args.nitems; ++i)
+      if (args.items[i].kind == K_SCAL) nf = max(nf, args.items[i].arg + args.items[i].k);
+    if (nf <= (uint32_t)kDirectFactorsSmall) {
+      DirectArgsSmall sm;
+      sm.nitems = args.nitems;
+      sm.chunk = args.chunk;
+      memcpy(sm.items, args.items, sizeof(DirectItem) * args.nitems);
+      memcpy(sm.factors, args.factors, 4 * nf);
+      direct_kernel<DirectArgsSmall><<<dim3(grid_x, args.nitems), 256, 0, stream>>>(sm);
+      return cudaGetLastError();
+    }
+  }
+  direct_kernel<DirectArgs><<<dim3(grid_x, args.nitems), 256, 0, stream>>>(args);
   return cudaGetLastError();
 }
 

@@ -360,7 +360,7 @@ def test_stats_struct_matches_header(B):
 
 def test_device_abi_layout(tmp_path):
     """Host-written offsets of the device ABI (runtime.cpp writes StreamCtl's
-    header by offset; DirectArgs travels as a kernel parameter, <= 4 KiB)."""
+    header by offset; DirectArgs travels as a kernel parameter, <= 32,764 bytes)."""
     src = tmp_path / "abi.cpp"
     src.write_text('#include <cstdio>\n#include <cstddef>\n#include "device_abi.h"\nusing namespace bt;\n'
                    'int main() { printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(EpochArgs), offsetof(StreamCtl, nsub), '
@@ -370,7 +370,7 @@ def test_device_abi_layout(tmp_path):
                            "-o", str(exe)])
     ea, nsub, subs, sc, da, di = map(int, subprocess.check_output([str(exe)], text=True).split())
     assert nsub == 20 and subs == 64 and sc % 64 == 0 and sc >= 64 + 16 * ea
-    assert da <= 4096 and di == 40
+    assert da <= 32764 and di == 40   # kernel parameter limit (CUDA >= 12.1)
 
 
 def test_library_contains_every_kernel(B):
