@@ -449,6 +449,7 @@ def main():
         roof["work_per_launch"] = work
         roof["launches_per_step"] = launches_per_step
         roof["epochs_per_step"] = epochs_per_step
+        roof["stream_closes"] = int(st.get("stream_closes", 0))   # stream launches ended early (expected 0)
         roof["device_span_ms_per_step"] = span_ms
         roof["span_share_ms"] = share_ms
         roof["achieved_span_share"] = work / (share_ms * 1e-3) / scale
