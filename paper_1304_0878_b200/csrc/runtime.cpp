@@ -104,7 +104,7 @@ struct Slot {
   bool ipc_alloc = false;     // root only: replica from cudaMalloc (shareable with other ranks)
   uint64_t reg_key = 0;       // root only: registration ordinal (equal on all ranks)
   uint8_t prounds = 0;        // partitioned parent: rounds its parts were dealt to
-  bool pgeo = false;          // ... geometrically (round_of)
+  int8_t pgeo = 0;            // ... geometrically (round_of: 1 growing, 2 shrinking)
 };
 
 struct EpochBuf {
@@ -535,11 +535,16 @@ bool geometric_rounds() {
 }
 
 // Round of part t of n dealt to `rounds` rounds: contiguous equal shares, or
-// (geo, 4 rounds) geometric shares 1/16, 2/16, 4/16, 9/16 -- see bt_data_partition.
-uint32_t round_of(uint64_t t, uint64_t n, uint32_t rounds, bool geo) {
-  if (geo) {
+// (4 rounds) geometric shares growing 1/16, 2/16, 4/16, 9/16 (geo = 1) or
+// shrinking 9/16, 4/16, 2/16, 1/16 (geo = 2) -- see bt_data_partition.
+uint32_t round_of(uint64_t t, uint64_t n, uint32_t rounds, int geo) {
+  if (geo == 1) {
     const uint64_t q = t * 16 / n;
     return q < 1 ? 0 : q < 3 ? 1 : q < 7 ? 2 : 3;
+  }
+  if (geo == 2) {
+    const uint64_t q = t * 16 / n;
+    return q < 9 ? 0 : q < 13 ? 1 : q < 15 ? 2 : 3;
   }
   return (uint32_t)(t * rounds / n);
 }
@@ -1407,12 +1412,14 @@ int bt_data_partition(bt_runtime *rt, bt_handle h, uint32_t nparts) {
     // make the device the slower side: C5 step 2.51 -> 2.40-2.45 ms).
     // Unfused runs are host-bound (C4: ~4 ns of build per task on 14
     // threads vs ~1 ns of device time), where a large last round would
-    // leave the device the whole 9/16 after the host is done: equal rounds.
+    // leave the device the whole 9/16 after the host is done; shrinking rounds
+    // (9/16 ... 1/16, round_of geo = 2) measured worse too (C4 unfused 4.9 ->
+    // 6.3 ms: a 560k-item round builds slower per item): equal rounds.
     // (Parts owned by several ranks are re-dealt per rank: scal_run_parallel.)
-    const bool geo = rounds == 4 && rt->builder.fusion && geometric_rounds();
+    const int geo = rounds == 4 && geometric_rounds() && rt->builder.fusion ? 1 : 0;
     const uint32_t round = round_of(t, nparts, rounds, geo);
     p.prounds = (uint8_t)rounds;
-    p.pgeo = geo;
+    p.pgeo = (int8_t)geo;
     ch.grp = round * (uint32_t)rt->npool + ((c0 + t) >> 6) % (uint32_t)rt->npool;
   }
   p.nparts = nparts;
