@@ -562,8 +562,8 @@ def test_c_example_program(B, tmp_path):
 def test_bench_launch_configuration_c5(B):
     """bench.py's exact path at full size: device-homed 4 GiB tensor, 16,384
     tiles, the C5 task stream through bt_insert_task_batch with the default
-    configuration (pipelined rounds on the "sw" kernel), two steps; sampled
-    elements against the oracle."""
+    configuration (pipelined rounds as sub-epochs of one stream launch of the
+    "sw" kernel per step), two steps; sampled elements against the oracle."""
     import importlib.util
     import os
     import torch
@@ -589,6 +589,7 @@ def test_bench_launch_configuration_c5(B):
         rt.unpartition(h)
         rt.unregister(h)
     assert st["epochs"] >= 8 and st["items"] == 2 * T
+    assert st["sched_launches"] == 2 and st["stream_closes"] == 0, st   # one stream launch per step
     got = x[torch.from_numpy(idx).cuda()].cpu().numpy()
     exp = oracle.scal_chain(oracle.scal_chain(x0, f), f)
     assert_bits_equal(got, exp, "bench configuration, two steps")
