@@ -1811,7 +1811,12 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
   // are the rounds of launch j.  Empty rounds belong to another round policy.
   std::vector<int> bound{0};
   if (pipelined) {
-    const size_t per = std::max<size_t>(1, rt->cfg.pipeline_min / 2);
+    // a round that joins a stream launch costs ~20 us of host flush, a
+    // separate launch much more: with stream launches possible, rounds of at
+    // least pipeline_min / 8 tasks stay separate (an N = 8 rank's shard of C5
+    // starts after 1/16 of it is built instead of 7/16)
+    const bool streamable = rt->sctl && rt->caches.empty() && !(rt->cfg.flags & BT_FLAG_TIMESTAMPS);
+    const size_t per = std::max<size_t>(1, rt->cfg.pipeline_min / (streamable ? 8 : 2));
     int nonempty = 0;
     for (int r = 0; r < R; ++r) nonempty += round_size[r] != 0;
     const size_t want = std::max<size_t>(1, std::min<size_t>((size_t)nonempty, local / per));
