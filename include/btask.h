@@ -302,6 +302,18 @@ int bt_dag_snapshot(bt_runtime *rt, bt_dag_view *out);
  * until the next flush.  -ENODATA if no trace is available. */
 int bt_trace(bt_runtime *rt, const uint64_t **t, const uint32_t **item, uint64_t *n);
 
+/* ---- test hook --------------------------------------------------------- */
+/* Hold the runtime's stream: work enqueued on it after this call (the next
+ * epochs' kernels, the copies of cross-rank reads) starts only once the caller
+ * stores a nonzero value into **flag_out, a word of mapped pinned host memory
+ * owned by the runtime (valid until bt_shutdown).  Implemented as a stream
+ * memory wait (cuStreamWaitValue32), else a one-thread gate kernel polling the
+ * word (60 s watchdog).  Nothing else waits: other ranks' streams keep running,
+ * which makes a missing cross-rank RAW/WAR ordering (bt_comm_init) observable
+ * with all ranks on one GPU (tests/test_gpu.py::test_cross_rank_gated_*).
+ * -EINVAL, -ENODEV (host-only runtime), -ENOMEM, -EIO. */
+int bt_debug_gate(bt_runtime *rt, volatile uint32_t **flag_out);
+
 #ifdef __cplusplus
 }
 #endif

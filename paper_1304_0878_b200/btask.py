@@ -93,6 +93,7 @@ _SIGS = {
     "bt_stats_reset": (_c.c_int, [_c.c_void_p]),
     "bt_dag_snapshot": (_c.c_int, [_c.c_void_p, _P(bt_dag_view)]),
     "bt_trace": (_c.c_int, [_c.c_void_p, _P(_P(_c.c_uint64)), _P(_P(_c.c_uint32)), _P(_c.c_uint64)]),
+    "bt_debug_gate": (_c.c_int, [_c.c_void_p, _P(_P(_c.c_uint32))]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -277,6 +278,15 @@ class Runtime:
 
     def last_error(self) -> str:
         return bt_last_error(self.rt).decode()
+
+    def debug_gate(self):
+        """Test hook: hold the runtime's stream; returns a callable that opens the gate."""
+        flag = ctypes.POINTER(ctypes.c_uint32)()
+        self._check(bt_debug_gate(self.rt, ctypes.byref(flag)), "bt_debug_gate")
+
+        def release():
+            flag[0] = 1
+        return release
 
     def __enter__(self):
         return self

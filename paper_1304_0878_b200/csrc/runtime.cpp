@@ -36,6 +36,7 @@ cudaError_t scheduler_occupancy(int *blocks_per_sm, int *block);
 cudaError_t scheduler_occupancy_wq(int *blocks_per_sm, int *block);
 cudaError_t launch_stage(void *dst, const void *src_mapped, size_t bytes, unsigned long long *q_empty, size_t nq,
                          uint32_t *zero, size_t nz, cudaStream_t stream);
+cudaError_t launch_gate(const volatile unsigned *flag_dev, uint64_t watchdog_ns, cudaStream_t stream);
 int max_factors();
 }  // namespace bt
 
@@ -246,6 +247,9 @@ struct bt_runtime {
   // last trace
   std::vector<uint64_t> trace_t;
   std::vector<uint32_t> trace_item;
+
+  // bt_debug_gate flags (mapped pinned words, freed at shutdown)
+  std::vector<uint32_t *> gates;
 
   // pack scratch
   std::vector<uint32_t> succ_off, cursor;
@@ -1258,6 +1262,7 @@ int bt_shutdown(bt_runtime *rt) {
     if (rt->sctl) cudaFree(rt->sctl);
     if (rt->close_h) cudaFreeHost(rt->close_h);
     for (cudaEvent_t ev : rt->ev_free) cudaEventDestroy(ev);
+    for (uint32_t *g : rt->gates) cudaFreeHost(g);
     if (rt->h2d) cudaStreamDestroy(rt->h2d);
     if (rt->d2h) cudaStreamDestroy(rt->d2h);
     if (rt->span_start) cudaEventDestroy(rt->span_start);
@@ -2203,6 +2208,43 @@ int bt_dag_snapshot(bt_runtime *rt, bt_dag_view *out) {
   rt->stats.edges += B.edges.size();
   rt->stats.fused_tasks += B.fused;
   B.next_epoch();
+  return 0;
+}
+
+// Test hook (btask.h): hold rt->stream until the caller sets a mapped flag.
+// A stream memory wait occupies no SM; the gate kernel (fallback) one thread.
+int bt_debug_gate(bt_runtime *rt, volatile uint32_t **flag_out) {
+  if (int r = check_live(rt)) return r;
+  if (!flag_out) return fail(rt, -EINVAL, "null flag pointer");
+  if (rt->host_only) return fail(rt, -ENODEV, "host-only runtime: nothing executes");
+  cudaSetDevice(rt->device);
+  uint32_t *flag = nullptr;
+  if (cudaHostAlloc((void **)&flag, 64, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(rt, -ENOMEM, "cannot allocate the gate flag");
+  }
+  rt->gates.push_back(flag);
+  __atomic_store_n(flag, 0u, __ATOMIC_SEQ_CST);
+  uint32_t *dflag = nullptr;
+  CUDA_TRY(rt, cudaHostGetDevicePointer((void **)&dflag, flag, 0));
+  // CUresult cuStreamWaitValue32(CUstream, CUdeviceptr, cuuint32_t, unsigned flags); GEQ = 0
+  using WaitValue32 = int (*)(cudaStream_t, unsigned long long, uint32_t, unsigned);
+  static WaitValue32 wait_value = [] {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (getenv("BT_GATE_KERNEL") || cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      fn = nullptr;
+    }
+    return reinterpret_cast<WaitValue32>(fn);
+  }();
+  if (!wait_value || wait_value(rt->stream, reinterpret_cast<unsigned long long>(dflag), 1u, 0u) != 0) {
+    cudaGetLastError();
+    CUDA_TRY(rt, launch_gate(dflag, 60ull * 1000 * 1000 * 1000, rt->stream));
+    ++rt->stats.kernel_launches;
+  }
+  *flag_out = flag;
   return 0;
 }
 

@@ -1445,6 +1445,18 @@ cudaError_t launch_stage(void *dst, const void *src_mapped, size_t bytes, unsign
   return cudaGetLastError();
 }
 
+// Test hook (bt_debug_gate): one thread holds the stream until the host sets
+// the mapped word; gives up after watchdog_ns (the stream then runs on).
+__global__ void gate_kernel(const volatile unsigned *flag, uint64_t watchdog_ns) {
+  const uint64_t t0 = globaltimer();
+  while (*flag == 0u && globaltimer() - t0 < watchdog_ns) __nanosleep(1000);
+}
+
+cudaError_t launch_gate(const volatile unsigned *flag_dev, uint64_t watchdog_ns, cudaStream_t stream) {
+  gate_kernel<<<1, 1, 0, stream>>>(flag_dev, watchdog_ns);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // "wq": every warp is an independent worker (pop, body, release), for epochs of
 // small units (<= 16 KiB): a CTA-wide unit of 4 KiB leaves most threads idle

@@ -89,6 +89,73 @@ def test_subnormal_inputs_not_flushed(B):
 KERNELS = {"auto": 0, "sw": 1 << 8, "rw": 1 << 9, "wq": 1 << 10}   # BT_FLAG_KERNEL_*
 
 
+# ---- IEEE special values on every device path -------------
+
+def special_programs(n=24, finite_scalars=False, base=5100, **kw):
+    """Seeded special-value programs (+-0, +-inf, max finite, subnormals; scalars
+    +-0, +-inf, 1e+-30) whose sequential result holds no NaN (NaN bit patterns
+    are not portable, reading R11): a NaN-producing program is skipped."""
+    out, seed = [], base
+    while len(out) < n:
+        p = W.special_value_program(seed, finite_scalars=finite_scalars, **kw)
+        seed += 1
+        if not any(np.isnan(b).any() for b in oracle.run(p)):
+            out.append(p)
+    return out
+
+
+def _has_specials(programs):
+    """The drawn programs do exercise the special cases (not vacuous)."""
+    res = [oracle.run(p) for p in programs]
+    allv = np.concatenate([np.concatenate(r) for r in res])
+    bits = allv.view(np.uint32)
+    assert np.isinf(allv).any() and (bits == 0x80000000).any() and (bits == 0).any()
+    assert ((bits & 0x7F800000) == 0).any() and ((bits & 0x7FFFFF) != 0).any()
+
+
+@pytest.mark.parametrize("kernel", ["sw", "rw", "wq"])
+def test_special_values_per_kernel(B, kernel):
+    """+-0, +-inf, overflow to +-inf, underflow to +-0 and subnormals, through
+    each persistent scheduler variant (forced), fused and unfused, with
+    multi-chunk items: bit-exact against the oracle."""
+    progs = special_programs()
+    _has_specials(progs)
+    for fusion in (True, False):
+        flags = (0 if fusion else B.BT_FLAG_NO_FUSION) | KERNELS[kernel]
+        for p in progs:
+            compare_program(p, flags=flags, chunk_bytes=96)
+
+
+def test_special_values_direct_launch(B):
+    """The same programs as direct launches (one epoch per task: independent
+    items in the kernel parameters) and as whole-program epochs (auto choice)."""
+    for p in special_programs():
+        compare_program(p, epoch_tasks=1)
+        compare_program(p)
+
+
+def test_special_values_stream_launch(B):
+    """Special values through the bench's stream launch: device-homed tiles,
+    pipelined sweep-major SCAL runs (fused and unfused) with factors that
+    overflow finite values to +-inf (1e30) and underflow them through the
+    subnormals to +-0 (1e-30); +-inf and +-0 elements stay put (no factor is
+    0 or inf, so no NaN)."""
+    rng = np.random.default_rng(W.SEED_BASE + 95)
+    ntiles, tile = 400, 8192
+    x = W.special_floats(rng, ntiles * tile, frac=0.3)
+    f = np.array([1e30, 3.14, -1e-30, 0.5, 1e30, -1.0, 1e-30, 2.0], np.float32)
+    p = W.sweep_program(ntiles * tile, ntiles, f, x, name="special-value sweeps")
+    exp = oracle.run(repeated(p, 2))[0]
+    e = exp.view(np.uint32)
+    assert np.isinf(exp).any() and (e == 0x80000000).any() and ((e & 0x7F800000) == 0).any()
+    assert not np.isnan(exp).any()
+    for flags in (0, B.BT_FLAG_NO_FUSION):
+        out, st = run_device(B, p, repeats=2, flags=flags, pipeline_rounds=4, pipeline_min=500, parallel_min=500,
+                             host_threads=3)
+        assert_bits_equal(out[0], exp, f"special-value stream launch flags={flags}")
+        assert st["sched_launches"] == 2 and st["epochs"] >= 4, st
+
+
 @pytest.mark.parametrize("kernel", ["sw", "rw", "wq"])
 @pytest.mark.parametrize("fusion", [True, False])
 @pytest.mark.parametrize("chunk_bytes", [0, 96, 4096])
@@ -678,6 +745,46 @@ def test_cross_rank_read_after_long_write(B):
         p.tasks[i] = r
     results, stats, owners = xrank.run(p, nranks=2, owners=[0, 1], batch=False, flags=B.BT_FLAG_NO_FUSION)
     _check_owned(p, results, owners)
+
+
+def _gated_program():
+    """X (rank 0) scaled, copied into Y (rank 1 reads X: RAW across ranks), then
+    scaled again (rank 0 overwrites what rank 1 read: WAR across ranks)."""
+    n = 1 << 20
+    rng = np.random.default_rng(W.SEED_BASE + 93)
+    bufs = [W.unit_interval_floats(rng, n), np.zeros(n, np.float32)]
+    rows = [(W.SCAL, np.float32(3.14), 0, -1, -1, -1), (W.COPY, 0.0, 0, -1, 1, -1),
+            (W.SCAL, np.float32(0.5), 0, -1, -1, -1)]
+    p = W.Program(bufs, [0, 0], W._tasks(len(rows)), name="gated cross-rank RAW/WAR")
+    for i, r in enumerate(rows):
+        p.tasks[i] = r
+    return p
+
+
+@pytest.mark.parametrize("gate_rank", [0, 1])
+def test_cross_rank_gated_orderings(B, gate_rank):
+    """bt_debug_gate holds one rank's stream for 0.5 s: the owner's (rank 0:
+    its SCAL before the copy is late -- the reader's copy must wait for it,
+    RAW) or the reader's (rank 1: its copy is late -- the owner's next SCAL of
+    X must wait for it, WAR).  Y must hold 3.14 * X either way."""
+    from tests import xrank
+    p = _gated_program()
+    results, stats, owners = xrank.run(p, nranks=2, owners=[0, 1], gate=(gate_rank, 0.5), batch=False)
+    _check_owned(p, results, owners)
+
+
+@pytest.mark.parametrize("mutant,gate_rank", [("BT_COMM_MUTANT_NO_RAW", 0), ("BT_COMM_MUTANT_NO_WAR", 1)])
+def test_cross_rank_gated_mutants_fail(B, tmp_path, mutant, gate_rank):
+    """Test sensitivity: a library built without the RAW (resp. WAR) stream
+    ordering of cross-rank reads must FAIL the gated test above on one GPU."""
+    from paper_1304_0878_b200 import build
+    from tests import xrank
+    lib = build.build(out=str(tmp_path / "libbtask_mutant.so"), defines=[mutant])
+    p = _gated_program()
+    results, stats, owners = xrank.run(p, nranks=2, owners=[0, 1], gate=(gate_rank, 0.5), batch=False,
+                                       lib_path=lib)
+    with pytest.raises(AssertionError):
+        _check_owned(p, results, owners)
 
 
 @pytest.mark.parametrize("kernel", ["auto", "sw", "rw", "wq"])

@@ -38,9 +38,12 @@ def leaf_ranges(program, b: int):
 
 
 def worker(rank: int, nranks: int, name: str, program, owners, batch: bool, barrier, q, flags: int = 0,
-           rt_kwargs=None):
+           rt_kwargs=None, gate=None, lib_path=None):
     try:
         sys.path.insert(0, ROOT)
+        if lib_path:   # a test-sensitivity build of the library (tests/test_gpu.py mutants)
+            os.environ["BT_LIB_PATH"] = lib_path
+        import time
         import numpy as np
         import torch
         from paper_1304_0878_b200 import btask as B
@@ -57,7 +60,13 @@ def worker(rank: int, nranks: int, name: str, program, owners, batch: bool, barr
                     rt.set_rank(s.subs[b][t], r)
             else:
                 rt.set_rank(s.roots[b], own)
+        # gate = (rank, seconds): that rank's stream is held (bt_debug_gate)
+        # from before its first task until `seconds` after its submission
+        release = rt.debug_gate() if gate and gate[0] == rank else None
         s.submit(batch=batch)
+        if release:
+            time.sleep(gate[1])
+            release()
         rt.wait()
         torch.cuda.synchronize()
         mine = {}
@@ -77,7 +86,7 @@ def worker(rank: int, nranks: int, name: str, program, owners, batch: bool, barr
 
 
 def run(program, nranks: int = 2, seed: int = 0, batch: bool = True, timeout: float = 240.0, owners=None,
-        flags: int = 0, rt_kwargs=None):
+        flags: int = 0, rt_kwargs=None, gate=None, lib_path=None):
     """Run `program` on nranks processes; returns ({(b, tile): owned data}, [stats per rank], owners)."""
     import multiprocessing as mp
     import uuid
@@ -87,7 +96,8 @@ def run(program, nranks: int = 2, seed: int = 0, batch: bool = True, timeout: fl
     name = f"/bt-test-{os.getpid()}-{uuid.uuid4().hex[:8]}"
     q = ctx.Queue()
     barrier = ctx.Barrier(nranks)
-    procs = [ctx.Process(target=worker, args=(r, nranks, name, program, owners, batch, barrier, q, flags, rt_kwargs))
+    procs = [ctx.Process(target=worker, args=(r, nranks, name, program, owners, batch, barrier, q, flags, rt_kwargs, gate,
+                                                  lib_path))
              for r in range(nranks)]
     for p in procs:
         p.start()

@@ -197,3 +197,42 @@ def random_small_program(seed: int, max_tasks: int = 10, max_handles: int = 4, m
                 np.float32(rng.uniform(-0.5, 0.5)) if kind == 1 else np.float32(0),
                 b0, t0, b1, t1)
     return Program(bufs, nparts, t, name=f"random small program seed {seed}")
+
+
+# IEEE special and extreme binary32 values (SURVEY Q11/Q12): signed zeros,
+# infinities, the largest finite value, subnormals, values near overflow.
+# Bit patterns only; NaN is never drawn (its bits are not portable, R11).
+SPECIAL_BITS = np.array([0x00000000, 0x80000000, 0x7F800000, 0xFF800000, 0x7F7FFFFF, 0xFF7FFFFF,
+                         0x00000001, 0x80000001, 0x007FFFFF, 0x00800000, 0x80800000, 0x7E967699,
+                         0xFE967699, 0x3F800000, 0xBF800000, 0x4048F5C3, 0x0DA24260, 0x8DA24260],
+                        dtype=np.uint32)
+# scalars: +-0, +-inf, huge, tiny, ordinary
+SPECIAL_SCALAR_BITS = np.array([0x00000000, 0x80000000, 0x7F800000, 0xFF800000, 0x7149F2CA, 0xF149F2CA,
+                                0x0DA24260, 0x8DA24260, 0x4048F5C3, 0xC048F5C3, 0x3F000000, 0x3F800000],
+                               dtype=np.uint32)
+
+
+def special_floats(rng: np.random.Generator, n: int, frac: float = 0.5) -> np.ndarray:
+    """[1,2) floats with a fraction `frac` of elements replaced by SPECIAL_BITS."""
+    x = unit_interval_floats(rng, n).view(np.uint32).copy()
+    sel = rng.random(n) < frac
+    x[sel] = rng.choice(SPECIAL_BITS, size=int(sel.sum()))
+    return x.view(np.float32)
+
+
+def special_value_program(seed: int, max_tasks: int = 10, max_handles: int = 4, max_elems: int = 300,
+                          finite_scalars: bool = False) -> Program:
+    """random_small_program with special values in the buffers and special
+    scalars (finite_scalars: only the nonzero finite ones, so no SCAL can turn
+    inf into NaN).  The caller rejects programs whose result holds a NaN."""
+    p = random_small_program(seed, max_tasks=max_tasks, max_handles=max_handles, max_elems=max_elems)
+    rng = np.random.default_rng(seed + 7777)
+    pal = SPECIAL_SCALAR_BITS
+    if finite_scalars:
+        pal = pal[(pal & 0x7F800000) != 0x7F800000]
+        pal = pal[(pal & 0x7FFFFFFF) != 0]
+    bufs = [special_floats(rng, len(b)) for b in p.buffers]
+    t = p.tasks.copy()
+    t["scalar"] = np.where(t["codelet"] == COPY, np.float32(0),
+                           rng.choice(pal, size=len(t)).view(np.float32))
+    return Program(bufs, p.nparts, t, name=f"special-value program seed {seed}")
