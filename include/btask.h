@@ -53,8 +53,8 @@
 extern "C" {
 #endif
 
-#define BT_ABI_VERSION 3   /* 2: bt_stats.kernel_launches, BT_FLAG_KERNEL_*; 3: bt_stats.sched_launches,
-                               BT_FLAG_NO_STREAM */
+#define BT_ABI_VERSION 4   /* 2: bt_stats.kernel_launches, BT_FLAG_KERNEL_*; 3: bt_stats.sched_launches,
+                               BT_FLAG_NO_STREAM; 4: bt_stats.stream_resumes, bt_debug_gate */
 
 typedef struct bt_runtime bt_runtime;
 typedef uint64_t bt_handle;
@@ -273,7 +273,10 @@ typedef struct bt_stats {
   uint64_t kernel_launches;   /* this library's kernel launches (per epoch: set-up + scheduler) */
   uint64_t sched_launches;    /* of which scheduler-kernel launches (a stream launch runs several epochs);
                                  device_ms / sched_launches = average launch duration */
-  uint64_t stream_closes;     /* stream launches ended early (a later round needed a larger epoch buffer) */
+  uint64_t stream_closes;     /* stream launches ended early by the host (a later round needed a larger
+                                 epoch buffer, or the run failed part-way) */
+  uint64_t stream_resumes;    /* stream launches that closed themselves (no publication for 50 ms, e.g.
+                                 under a launch-serialising tool) and were finished by their resume launch */
 } bt_stats;
 int bt_stats_get(bt_runtime *rt, bt_stats *out);
 int bt_stats_reset(bt_runtime *rt);

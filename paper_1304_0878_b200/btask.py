@@ -18,7 +18,7 @@ import numpy as np
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BT_LIB_PATH") or os.path.join(_PKG, "libbtask.so")   # override: experiments only
 
-BT_ABI_VERSION = 3
+BT_ABI_VERSION = 4
 BT_R, BT_W, BT_RW = 1, 2, 3
 BT_CL_SCAL, BT_CL_AXPY, BT_CL_COPY = 1, 2, 3
 BT_FLAG_NO_FUSION, BT_FLAG_HOST_ONLY, BT_FLAG_TIMESTAMPS, BT_FLAG_SYNC_EPOCH, BT_FLAG_NO_STREAM = 1, 2, 4, 8, 16
@@ -41,7 +41,8 @@ class bt_stats(ctypes.Structure):
                 ("epochs", ctypes.c_uint64), ("upload_bytes", ctypes.c_uint64), ("host_build_ms", ctypes.c_double),
                 ("device_ms", ctypes.c_double), ("device_span_ms", ctypes.c_double), ("grid", ctypes.c_uint32),
                 ("block", ctypes.c_uint32), ("kernel_launches", ctypes.c_uint64),
-                ("sched_launches", ctypes.c_uint64), ("stream_closes", ctypes.c_uint64)]
+                ("sched_launches", ctypes.c_uint64), ("stream_closes", ctypes.c_uint64),
+                ("stream_resumes", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

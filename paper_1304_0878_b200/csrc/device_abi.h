@@ -1,6 +1,7 @@
 // device_abi.h -- layouts shared by the host packer (runtime.cpp) and the
 // persistent scheduler kernel (scheduler.cu).  Internal to libbtask.so.
 #pragma once
+#include <stddef.h>
 #include <stdint.h>
 
 namespace bt {
@@ -108,15 +109,37 @@ using DirectArgsSmall = DirectArgsT<kDirectItemsSmall, kDirectFactorsSmall>;
 // the copy of its blob); the kernel reads subs[r] only after observing
 // published > r with ld.acquire.
 constexpr int kMaxSubs = 16;
+constexpr int kMaxStreamGrid = 2048;   // CTAs of a stream launch (abandoned-ticket slots)
+constexpr unsigned kStreamClosed = 1u << 31;
+//
+// Closing (launch-serialising tools, a stalled host): the host may be unable to
+// publish while the launch runs -- under ncu, compute-sanitizer or
+// CUDA_LAUNCH_BLOCKING=1 the launch call itself returns only when the kernel
+// ends.  A CTA waiting for a publication counts itself in `state`; when EVERY
+// CTA has waited longer than the quiescence limit, one of them closes the
+// launch with a CAS (count == grid -> count | kStreamClosed).  A CTA leaving
+// its wait decrements `state` and, if the returned value carries the closed
+// bit, abandons too; the CAS and the decrements are RMWs of one word, so no
+// CTA starts a sub-epoch the closer has given up.  Every CTA then holds one
+// ticket of an unpublished sub-epoch; it appends it to abandoned[] and exits
+// (its other slot drained), so the tickets taken are exactly those run plus
+// those abandoned.  The run's RESUME launch (same kernel, enqueued after the
+// last publication) exits at once unless the last CTA of the first launch set
+// `resume`; then it runs the abandoned tickets first, then fresh ones.
 struct alignas(64) StreamCtl {
   unsigned long long ticket;    // next launch-wide ticket
   unsigned published;           // sub-epochs whose args and blobs are in device memory
   unsigned abort;               // any sub-epoch's fault stops every CTA
   unsigned exited;              // CTAs that left the kernel
   unsigned nsub;                // sub-epochs of this launch (fixed at its start)
-  unsigned pad[10];
+  unsigned state;               // CTAs waiting for a publication | kStreamClosed
+  unsigned resume;              // the first launch closed: the resume launch runs the rest
+  unsigned nabandoned;          // tickets abandoned at the close
+  unsigned ab_take;             // ... taken again by the resume launch
+  unsigned pad[6];
   EpochArgs subs[kMaxSubs];
+  unsigned long long abandoned[kMaxStreamGrid];
 };
-static_assert(sizeof(StreamCtl) % 64 == 0, "StreamCtl layout");
+static_assert(sizeof(StreamCtl) % 64 == 0 && offsetof(StreamCtl, subs) == 64, "StreamCtl layout");
 
 }  // namespace bt

@@ -30,7 +30,8 @@
 
 namespace bt {
 cudaError_t launch_epoch(const EpochArgs &args, int grid, cudaStream_t stream, int kernel);
-cudaError_t launch_stream(StreamCtl *ctl, uint64_t watchdog_ns, int grid, cudaStream_t stream, bool prefetch);
+cudaError_t launch_stream(StreamCtl *ctl, uint64_t watchdog_ns, uint64_t quiesce_ns, int grid, cudaStream_t stream,
+                          bool prefetch, bool resume);
 cudaError_t launch_direct(const DirectArgs &args, unsigned grid_x, cudaStream_t stream);
 cudaError_t scheduler_occupancy(int *blocks_per_sm, int *block);
 cudaError_t scheduler_occupancy_wq(int *blocks_per_sm, int *block);
@@ -58,6 +59,7 @@ constexpr int kRoundsUploading = BT_ROUNDS_UPLOADING;   // rounds for partitions
 constexpr uint32_t kDefaultPipelineMin = 131072;
 constexpr int kEpochRing = 12;                      // epoch buffers in flight (>= rounds + 2)
 constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;   // 20 s
+constexpr uint64_t kQuiesceNs = 50ull * 1000 * 1000;             // stream launch: close after 50 ms without a publication
 constexpr size_t kParallelPack = 4096;              // items above which the pack runs on the pool
 constexpr uint64_t kWarpUnitMax = 4096;             // units of at most this many elements use "wq"
 constexpr uint64_t kPrefetchBelowK = 32;            // "sw" epochs with shorter average chains prefetch
@@ -140,10 +142,36 @@ struct UploadChunk {
   uint64_t lo, hi;            // device byte range
   cudaEvent_t ev;             // recorded after its H2D copy
 };
+// Disjoint half-open byte ranges, merged on insertion (a long-lived host-homed
+// vector written by many epochs keeps a handful of ranges, not one per epoch).
+struct RangeSet {
+  std::map<uint64_t, uint64_t> m;   // lo -> hi
+  bool overlaps(uint64_t lo, uint64_t hi) const {
+    auto it = m.lower_bound(hi);    // first range starting at or after hi
+    if (it == m.begin()) return false;
+    --it;
+    return it->second > lo;
+  }
+  void add(uint64_t lo, uint64_t hi) {
+    auto it = m.upper_bound(lo);
+    if (it != m.begin() && std::prev(it)->second >= lo) {
+      --it;
+      lo = it->first;
+      hi = std::max(hi, it->second);
+      it = m.erase(it);
+    }
+    while (it != m.end() && it->first <= hi) {
+      hi = std::max(hi, it->second);
+      it = m.erase(it);
+    }
+    m.emplace(lo, hi);
+  }
+};
+
 struct RootCache {
   uint64_t dlo = 0, dhi = 0;  // device byte range of the replica
   std::vector<UploadChunk> uploads;
-  std::vector<std::pair<uint64_t, uint64_t>> written;   // device byte ranges written by epochs
+  RangeSet written;           // device byte ranges written by epochs
   bool dirty = false;         // a write not covered by an eager write-back
   bool wb = false;            // eager write-backs issued
 };
@@ -213,6 +241,7 @@ struct bt_runtime {
     bool prefetch = false;
     bool started = false;
     bool launched = false;   // the run's launch is enqueued
+    bool defer = false;      // the launch is enqueued after the last publication
     uint64_t run_tasks = 0, cur_tasks = 0;   // local tasks of the run / of the sub-epoch being flushed
     uint64_t max_tasks = 0;                  // local tasks of the run's largest sub-epoch
     EpochBuf *bufs[kMaxSubs] = {};    // the sub-epochs' buffers (bufs[0]'s start/end time the launch)
@@ -400,6 +429,9 @@ int ensure_host(bt_runtime *rt, EpochBuf &e, size_t need) {
 
 int ensure_dev(bt_runtime *rt, EpochBuf &e, size_t need) {
   if (e.dcap >= need) return 0;
+  // tests: BT_DEBUG_FAIL_DEV_ALLOC=n fails the n-th epoch allocation (1-based)
+  static long fail_at = getenv("BT_DEBUG_FAIL_DEV_ALLOC") ? atol(getenv("BT_DEBUG_FAIL_DEV_ALLOC")) : 0;
+  if (fail_at > 0 && --fail_at == 0) return fail(rt, -ENOMEM, "cannot allocate epoch memory (injected failure)");
   if (e.dblob) cudaFree(e.dblob);
   e.dblob = nullptr;
   size_t cap = std::max({need, e.dcap + e.dcap / 2, rt->dcap_max});
@@ -423,6 +455,12 @@ int retire(bt_runtime *rt, EpochBuf &e) {
   float ms = 0.f;
   if (e.timed && cudaEventElapsedTime(&ms, e.start, e.end) == cudaSuccess) rt->stats.device_ms += ms;
   const Counters *c = e.hctr;
+  // a stream launch that closed (no publication for kQuiesceNs): its resume
+  // launch ran the rest, until e.done
+  if (e.timed && c->pad && cudaEventElapsedTime(&ms, e.end, e.done) == cudaSuccess) {
+    rt->stats.device_ms += ms;
+    rt->stats.stream_resumes += 1;
+  }
   if (c->error != ERR_NONE) {
     rt->poisoned = -EIO;
     return fail(rt, -EIO, "device scheduler fault (code %u%s)", c->error,
@@ -444,7 +482,8 @@ int retire(bt_runtime *rt, EpochBuf &e) {
         memcpy(w, hdr + 8, 16);
         unsigned pd[4];
         memcpy(pd, hdr + 24, 16);
-        fprintf(stderr, "  StreamCtl (%d): ticket %llu published %u abort %u exited %u nsub %u pad %u %u %u %u\n",
+        fprintf(stderr, "  StreamCtl (%d): ticket %llu published %u abort %u exited %u nsub %u state %x resume %u "
+                        "abandoned %u taken %u\n",
                 (int)ce, tk, w[0], w[1], w[2], w[3], pd[0], pd[1], pd[2], pd[3]);
         for (unsigned q = 0; q < kMaxSubs && rt->sl.bufs[q]; ++q) {
           Counters c2;
@@ -485,9 +524,29 @@ inline void range_of(size_t n, int P, int p, size_t &lo, size_t &hi) {
   hi = n * (size_t)(p + 1) / (size_t)P;
 }
 
+// Launch-serialising tools (ncu, compute-sanitizer, CUDA_LAUNCH_BLOCKING=1)
+// return from a launch only when the kernel ends: a stream launch enqueued
+// before its last publication would wait for publications the blocked host
+// cannot make (until it closes, kQuiesceNs later).  Under them, and with
+// BT_STREAM_DEFER=1, the launch is enqueued after the last publication.
+bool stream_defer() {
+  static const bool d = [] {
+    const char *lb = getenv("CUDA_LAUNCH_BLOCKING");
+    if (getenv("BT_STREAM_NODEFER")) return false;   // tests: exercise the close + resume path
+    return getenv("BT_STREAM_DEFER") != nullptr || getenv("CUDA_INJECTION64_PATH") != nullptr ||
+           (lb && lb[0] == '1');
+  }();
+  return d;
+}
+
+uint64_t quiesce_ns() {
+  static const uint64_t q = getenv("BT_QUIESCE_US") ? strtoull(getenv("BT_QUIESCE_US"), nullptr, 10) * 1000
+                                                    : kQuiesceNs;
+  return q;
+}
+
 // Enqueue the run's stream launch on rstream[0] (after sub-epoch 0's copies;
-// deferred: after the last publication).  Held (deferred) sub-epochs complete
-// with it.
+// deferred: after the last publication).
 int enqueue_stream_launch(bt_runtime *rt) {
   cudaStream_t ls = rt->rstream[0];
   EpochBuf &e0 = *rt->sl.bufs[0];
@@ -496,14 +555,35 @@ int enqueue_stream_launch(bt_runtime *rt) {
   rt->stats.block = (uint32_t)rt->block;
   rt->stats.kernel_launches += 1;
   rt->stats.sched_launches += 1;
-  CUDA_TRY(rt, launch_stream(rt->sctl, kWatchdogNs, rt->grid_max, ls, rt->sl.prefetch));
+  CUDA_TRY(rt, launch_stream(rt->sctl, kWatchdogNs, quiesce_ns(), rt->grid_max, ls, rt->sl.prefetch, false));
   CUDA_TRY(rt, cudaEventRecord(e0.end, ls));
+  rt->sl.launched = true;
+  return 0;
+}
+
+// Every sub-epoch of the run is published (or closed): order the launch
+// stream after the last publication; a deferred launch is enqueued now,
+// otherwise the RESUME launch (device_abi.h StreamCtl: it exits at once unless
+// the running launch closed for want of publications, then runs the rest).
+// The sub-epochs' buffers complete (done events) after that.
+int finish_stream_run(bt_runtime *rt) {
+  if (!rt->sl.bufs[0]) return 0;   // nothing enqueued for this run
+  cudaStream_t ls = rt->rstream[0];
+  CUDA_TRY(rt, cudaEventRecord(rt->ev_pub0, rt->rstream[1]));
+  CUDA_TRY(rt, cudaStreamWaitEvent(ls, rt->ev_pub0, 0));
+  if (!rt->sl.launched) {
+    if (int rc = enqueue_stream_launch(rt)) return rc;
+  } else {
+    rt->stats.kernel_launches += 1;
+    CUDA_TRY(rt, launch_stream(rt->sctl, kWatchdogNs, quiesce_ns(), rt->grid_max, ls, rt->sl.prefetch, true));
+  }
   for (EpochBuf *b : rt->sl.bufs)
     if (b && b->held) {
       CUDA_TRY(rt, cudaEventRecord(b->done, ls));
       b->held = false;
     }
-  rt->sl.launched = true;
+  // the run's join (scal_run_parallel) waits for ev_round[0]: after all of it
+  CUDA_TRY(rt, cudaEventRecord(rt->ev_round[0], ls));
   return 0;
 }
 
@@ -512,23 +592,20 @@ int enqueue_stream_launch(bt_runtime *rt) {
 // table whose contents never change (published value q + 1 at index q, then a
 // zero EpochArgs), so overlapping closes of successive launches cannot race.
 int close_stream(bt_runtime *rt) {
-  const unsigned *pub = reinterpret_cast<const unsigned *>(rt->close_h);
-  const char *zero_args = rt->close_h + 4 * kMaxSubs;
-  cudaStream_t up = rt->rstream[1];
-  for (unsigned q = rt->sl.next; q < rt->sl.nsub; ++q) {
-    CUDA_TRY(rt, cudaMemcpyAsync(&rt->sctl->subs[q], zero_args, sizeof(EpochArgs), cudaMemcpyHostToDevice, up));
-    CUDA_TRY(rt, cudaMemcpyAsync(&rt->sctl->published, &pub[q], 4, cudaMemcpyHostToDevice, up));
-  }
   rt->ev("close stream launch at sub %u of %u", rt->sl.next, rt->sl.nsub);
-  if (!rt->sl.launched && rt->sl.bufs[0]) {   // deferred launch not enqueued yet: enqueue it now
-    CUDA_TRY(rt, cudaEventRecord(rt->ev_pub0, up));
-    CUDA_TRY(rt, cudaStreamWaitEvent(rt->rstream[0], rt->ev_pub0, 0));
-    if (int rc = enqueue_stream_launch(rt)) return rc;
+  rt->stats.stream_closes += 1;
+  if (rt->sl.bufs[0]) {   // else nothing of this run reached the device: no kernel reads *sctl
+    const unsigned *pub = reinterpret_cast<const unsigned *>(rt->close_h);
+    const char *zero_args = rt->close_h + 4 * kMaxSubs;
+    cudaStream_t up = rt->rstream[1];
+    for (unsigned q = rt->sl.next; q < rt->sl.nsub; ++q) {
+      CUDA_TRY(rt, cudaMemcpyAsync(&rt->sctl->subs[q], zero_args, sizeof(EpochArgs), cudaMemcpyHostToDevice, up));
+      CUDA_TRY(rt, cudaMemcpyAsync(&rt->sctl->published, &pub[q], 4, cudaMemcpyHostToDevice, up));
+    }
   }
   rt->sl.next = rt->sl.nsub;
   rt->sl.active = false;
-  rt->stats.stream_closes += 1;
-  return 0;
+  return finish_stream_run(rt);
 }
 
 // Default pipelined rounds of device-resident partitions are geometric
@@ -696,6 +773,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     rt->sl.launched = false;
     rt->sl.prefetch = kernel == 3;
     rt->sl.started = rt->sl.active;
+    rt->sl.defer = stream_defer();
   }
   bool sub = rt->sl.active;
   // device layout: ctr | items | pending | succ | factors | queue[U] | chunk_done[N] | trace
@@ -874,6 +952,10 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
       CUDA_TRY(rt, cudaEventRecord(rt->span_start, ls));
       rt->span_open = true;
     }
+    // tests: a host that publishes late (BT_DEBUG_PUBLISH_DELAY_US before every
+    // sub-epoch after the first) makes the running launch close and resume
+    static const long pub_delay_us = getenv("BT_DEBUG_PUBLISH_DELAY_US") ? atol(getenv("BT_DEBUG_PUBLISH_DELAY_US")) : 0;
+    if (r > 0 && pub_delay_us > 0) std::this_thread::sleep_for(std::chrono::microseconds(pub_delay_us));
     // the launch is already running (r > 0): no set-up kernel, so the queue's
     // unpublished slots read EMPTY and the chunk counters zero in the blob
     for (uint64_t i = U0; i < U; ++i) q[i] = Q_EMPTY;
@@ -888,29 +970,22 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     CUDA_TRY(rt, cudaMemcpyAsync(d, h, o_cdone + 4 * N, cudaMemcpyHostToDevice, up));
     CUDA_TRY(rt, cudaMemcpyAsync(&rt->sctl->subs[r], h + o_args_h, sizeof(EpochArgs), cudaMemcpyHostToDevice, up));
     CUDA_TRY(rt, cudaMemcpyAsync(&rt->sctl->published, h + o_pub_h, 4, cudaMemcpyHostToDevice, up));
-    // BT_STREAM_DEFER=1: launch after the last sub-epoch is published, for
-    // tools that serialise kernel launches (ncu, compute-sanitizer): the
-    // launch call does not return before the kernel ends there, so a running
-    // kernel would wait for publications the host cannot make
-    static const bool defer = getenv("BT_STREAM_DEFER") != nullptr;
     if (r == 0) {   // later sub-epochs' copies follow the header reset
       CUDA_TRY(rt, cudaEventRecord(rt->ev_pub0, ls));
       CUDA_TRY(rt, cudaStreamWaitEvent(rt->rstream[1], rt->ev_pub0, 0));
     }
     rt->sl.bufs[r] = &e;
-    if (defer && r + 1 == rt->sl.nsub) {
-      CUDA_TRY(rt, cudaEventRecord(rt->ev_pub0, up));
-      CUDA_TRY(rt, cudaStreamWaitEvent(ls, rt->ev_pub0, 0));
-    }
-    if (defer ? r + 1 == rt->sl.nsub : r == 0)
+    if (r == 0 && !rt->sl.defer)
       if (int rc = enqueue_stream_launch(rt)) return rc;
-    // after the launch (which ends once every sub-epoch ran); deferred and not
-    // yet launched: held (not reusable) until the launch is enqueued
-    e.held = defer && r + 1 < rt->sl.nsub;
-    if (!e.held) CUDA_TRY(rt, cudaEventRecord(e.done, ls));
+    // held (not reusable) until the run's last launch is enqueued
+    // (finish_stream_run records its done event after it)
+    e.held = true;
     e.timed = r == 0;
-    if (++rt->sl.next == rt->sl.nsub) rt->sl.active = false;
+    const bool last = ++rt->sl.next == rt->sl.nsub;
+    if (last) rt->sl.active = false;
     account();
+    if (last)
+      if (int rc = finish_stream_run(rt)) return rc;
     static const bool dbg_t = getenv("BT_DEBUG_TIMING") != nullptr;
     if (dbg_t)
       fprintf(stderr, "flush sub %u N=%zu U=%llu: passA %.3f passB %.3f csr %.3f copies+launch %.3f ms\n", r, N,
@@ -1009,9 +1084,8 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     RootCache &c = kv2.second;
     const uint64_t lo = std::max(tot.wlo, c.dlo), hi = std::min(tot.whi, c.dhi);
     if (lo >= hi) continue;
-    bool again = false;
-    for (const auto &wr : c.written) again |= (wr.first < hi && lo < wr.second);
-    c.written.emplace_back(lo, hi);
+    const bool again = c.written.overlaps(lo, hi);
+    c.written.add(lo, hi);
     if (again || c.dirty) {
       c.dirty = true;
       continue;
@@ -1202,7 +1276,7 @@ int bt_init(const bt_config *cfg_in, bt_runtime **out) {
         delete rt;
         return -ENOMEM;
       }
-    if (!(cfg.flags & BT_FLAG_NO_STREAM) &&
+    if (!(cfg.flags & BT_FLAG_NO_STREAM) && rt->grid_max <= kMaxStreamGrid &&
         (cudaMalloc((void **)&rt->sctl, sizeof(StreamCtl)) != cudaSuccess ||
          cudaEventCreateWithFlags(&rt->ev_pub0, cudaEventDisableTiming) != cudaSuccess ||
          cudaHostAlloc((void **)&rt->close_h, 4 * kMaxSubs + sizeof(EpochArgs), cudaHostAllocPortable) !=
@@ -1572,6 +1646,7 @@ int cross_rank_read(bt_runtime *rt, uint32_t x, int peer, bool send) {
 }
 
 int submit(bt_runtime *rt, int codelet, float scalar, bt_handle h0, bt_handle h1) {
+  if (rt->poisoned) return fail(rt, rt->poisoned, "runtime poisoned by an earlier device error");
   int64_t s0 = operand(rt, codelet, h0);
   if (s0 < 0) return (int)s0;
   if (codelet == BT_CL_SCAL) {
@@ -1636,7 +1711,10 @@ int submit(bt_runtime *rt, int codelet, float scalar, bt_handle h0, bt_handle h1
 // handles; a fork/join of events orders them after earlier work and before
 // later work on the runtime's stream).  Returns 1 (nothing changed) if any
 // task of the run would fail, so that the caller replays it sequentially and
-// stops at the first error exactly like bt_insert_task.
+// stops at the first error exactly like bt_insert_task; 0 when the whole run
+// is submitted; a negative errno when submission failed after the run began
+// to change state (items merged, rounds flushed): the runtime is then
+// poisoned (-EIO from every later call), never replayed.
 int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scalars, const bt_handle *h0, size_t i0,
                       size_t i1) {
   const int P = rt->pool->size();
@@ -1653,8 +1731,9 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
   const SlotHot *hot = rt->hot.data();
   static const bool dbg = getenv("BT_DEBUG_TIMING") != nullptr;
   // task indices are epoch-relative; a pipelined run starts a fresh epoch
+  // (a failure here changed nothing of the run: returned as is)
   if (pipelined && !B.items.empty())
-    if (int r = flush_epoch(rt)) return r;
+    if (int r = flush_epoch(rt)) return r < 0 ? r : -EIO;
   const uint64_t tbase = B.ntasks;
   const bool record = B.record_tasks;
   double tp0 = now_ms();
@@ -1790,6 +1869,17 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
   for (int c = 0; c < P; ++c) rem += remote[c];
   rt->stats.tasks_submitted += n;
   rt->stats.tasks_local += n - rem;
+  // from here on the dependency states change: a failure poisons the runtime
+  struct PoisonOnFail {
+    bt_runtime *rt;
+    bool ok = false;
+    ~PoisonOnFail() {
+      if (!ok && !rt->poisoned) {
+        rt->poisoned = -EIO;
+        fail(rt, -EIO, "SCAL run failed part-way (%s): runtime poisoned", rt->last_error.c_str());
+      }
+    }
+  } poison_on_fail{rt};
   if (pipelined) {
     CUDA_TRY(rt, cudaEventRecord(rt->ev_fork, rt->stream));
     for (int i = 0; i < 2; ++i) CUDA_TRY(rt, cudaStreamWaitEvent(rt->rstream[i], rt->ev_fork, 0));
@@ -1945,6 +2035,7 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
             tp1 - tp0, t_p2, t_merge, t_flush);
   if (dbg)
     for (size_t j = 0; j < t_launch.size(); ++j) fprintf(stderr, "  launch %zu issued at %.3f ms\n", j, t_launch[j]);
+  poison_on_fail.ok = true;
   return 0;
 }
 
@@ -1989,19 +2080,35 @@ int bt_insert_task_batch(bt_runtime *rt, size_t ntasks, const int32_t *codelets,
   int rc = 0;
   const size_t pmin = rt->cfg.parallel_min;
   // common case first: the whole batch is one long valid SCAL run
-  if (ntasks >= pmin && scal_run_parallel(rt, codelets, scalars, h0, 0, ntasks) == 0) {
-    i = ntasks;
-    if (rt->cfg.epoch_tasks && rt->builder.ntasks >= rt->cfg.epoch_tasks && !rt->host_only) rc = flush_epoch(rt);
+  // (scal_run_parallel: 1 = rejected, nothing changed -> per-task path below;
+  // negative = failed part-way -> the error, nothing counted as submitted)
+  if (ntasks >= pmin) {
+    const int pr = scal_run_parallel(rt, codelets, scalars, h0, 0, ntasks);
+    if (pr < 0) {
+      rt->stats.host_build_ms += now_ms() - t0;
+      return pr;
+    }
+    if (pr == 0) {
+      i = ntasks;
+      if (rt->cfg.epoch_tasks && rt->builder.ntasks >= rt->cfg.epoch_tasks && !rt->host_only) rc = flush_epoch(rt);
+    }
   }
   while (i < ntasks && rc == 0) {
     if (codelets[i] == BT_CL_SCAL) {
       size_t j = i;
       while (j < ntasks && codelets[j] == BT_CL_SCAL) ++j;
-      if (j - i >= pmin && j - i < ntasks && scal_run_parallel(rt, codelets, scalars, h0, i, j) == 0) {
-        i = j;
-        if (rt->cfg.epoch_tasks && rt->builder.ntasks >= rt->cfg.epoch_tasks && !rt->host_only)
-          rc = flush_epoch(rt);
-        continue;
+      if (j - i >= pmin && j - i < ntasks) {
+        const int pr = scal_run_parallel(rt, codelets, scalars, h0, i, j);
+        if (pr < 0) {
+          rc = pr;
+          break;
+        }
+        if (pr == 0) {
+          i = j;
+          if (rt->cfg.epoch_tasks && rt->builder.ntasks >= rt->cfg.epoch_tasks && !rt->host_only)
+            rc = flush_epoch(rt);
+          continue;
+        }
       }
       for (; i < j; ++i) {      // short run, or a task of the run fails: sequential
         rc = submit(rt, BT_CL_SCAL, scalars[i], h0[i], 0);
@@ -2048,8 +2155,7 @@ int sync_to_host(bt_runtime *rt, uint32_t root, uint64_t lo, uint64_t hi) {
   auto it = rt->caches.find(root);
   if (it == rt->caches.end()) return 0;
   RootCache &c = it->second;
-  bool touched = false;
-  for (const auto &wr : c.written) touched |= (wr.first < hi && lo < wr.second);
+  const bool touched = c.written.overlaps(lo, hi);
   if (touched && c.dirty) {
     char *host = static_cast<char *>(rt->slots[root].hptr) + (lo - c.dlo);
     CUDA_TRY(rt, cudaMemcpyAsync(host, reinterpret_cast<const void *>(lo), hi - lo, cudaMemcpyDeviceToHost, rt->d2h));

@@ -336,6 +336,17 @@ __device__ void copy_range(const float *x, float *y, uint64_t n, int tid) {
   for (uint64_t t = head + 8 * nv + tid; t < n; t += C) __stcg(y + t, __ldcg(x + t));
 }
 
+// Loads of an epoch's read-only descriptors (items, successors, factors): the
+// non-coherent path (ld.global.nc) for ordinary launches; L2-only loads
+// (ld.global.cg) in stream launches, whose sub-epoch blobs are copied in while
+// the kernel runs (ld.global.nc is defined only for data read-only for the
+// whole kernel).
+template <bool NC, class T>
+__device__ __forceinline__ T ldro(const T *p) {
+  if constexpr (NC) return __ldg(p);
+  else return __ldcg(p);
+}
+
 // ---- scheduler-warp helpers (lane 0 only) ---------------------------------
 __device__ __forceinline__ void raise_error(const EpochArgs &a, unsigned code) {
   atomicCAS(&a.ctr->error, 0u, code);
@@ -430,6 +441,7 @@ struct RelMeta {
   bool s0stage;                // a continuation candidate that needs no factor list
 };
 // self: the item's descriptor already staged in shared memory, or null.
+template <bool NC = true>
 __device__ __forceinline__ RelMeta release_meta(const EpochArgs &a, uint32_t item, const DItem *self = nullptr) {
   RelMeta m;
   if (self) {
@@ -438,19 +450,19 @@ __device__ __forceinline__ RelMeta release_meta(const EpochArgs &a, uint32_t ite
     m.off = self->succ_off;
   } else {
     const DItem &it = a.items[item];
-    m.nchunks = __ldg(&it.nchunks);
-    m.nsucc = __ldg(&it.nsucc);
-    m.off = __ldg(&it.succ_off);
+    m.nchunks = ldro<NC>(&it.nchunks);
+    m.nsucc = ldro<NC>(&it.nsucc);
+    m.off = ldro<NC>(&it.succ_off);
   }
   m.s0 = m.s0kind = m.s0nc = 0;
   m.s0stage = false;
   m.i0 = m.i1 = m.i2 = uint4{};
   if (m.nsucc) {
-    m.s0 = m.nsucc == 1 ? m.off : __ldg(&a.succ[m.off]);   // a single successor is stored inline
+    m.s0 = m.nsucc == 1 ? m.off : ldro<NC>(&a.succ[m.off]);   // a single successor is stored inline
     const uint4 *src = reinterpret_cast<const uint4 *>(a.items + m.s0);
-    m.i0 = __ldg(src);
-    m.i1 = __ldg(src + 1);   // n (x, y), kind (z), k (w)
-    m.i2 = __ldg(src + 2);   // arg (x), nchunks (y), succ_off (z), nsucc (w)
+    m.i0 = ldro<NC>(src);
+    m.i1 = ldro<NC>(src + 1);   // n (x, y), kind (z), k (w)
+    m.i2 = ldro<NC>(src + 2);   // arg (x), nchunks (y), succ_off (z), nsucc (w)
     static_assert(offsetof(DItem, kind) == 24 && offsetof(DItem, k) == 28 && offsetof(DItem, nchunks) == 36,
                   "DItem layout");
     m.s0kind = m.i1.z;
@@ -460,9 +472,10 @@ __device__ __forceinline__ RelMeta release_meta(const EpochArgs &a, uint32_t ite
   return m;
 }
 
+template <bool NC = true>
 __device__ __forceinline__ void release_unit(const EpochArgs &a, uint32_t item, const Mailbox &mb = Mailbox{},
                                              const RelMeta *pre = nullptr) {
-  const RelMeta m = pre ? *pre : release_meta(a, item);
+  const RelMeta m = pre ? *pre : release_meta<NC>(a, item);
   const uint32_t nchunks = m.nchunks, nsucc = m.nsucc, off = m.off;
   if (nchunks > 1) {
     const unsigned c = atom_add_acq_rel(&a.chunk_done[item], 1u);
@@ -472,15 +485,15 @@ __device__ __forceinline__ void release_unit(const EpochArgs &a, uint32_t item, 
     }
   }
   for (uint32_t i = 0; i < nsucc; ++i) {
-    const uint32_t s = i == 0 ? m.s0 : __ldg(&a.succ[off + i]);
-    const uint32_t skind = i == 0 ? m.s0kind : __ldg(&a.items[s].kind);
+    const uint32_t s = i == 0 ? m.s0 : ldro<NC>(&a.succ[off + i]);
+    const uint32_t skind = i == 0 ? m.s0kind : ldro<NC>(&a.items[s].kind);
     // a single-predecessor successor is ready now (no counter); with more
     // predecessors the acq_rel RMW both releases ours and acquires theirs
     const bool ready = mb.unit && (skind & K_SINGLE_PRED)
                            ? true
                            : atom_add_acq_rel(reinterpret_cast<unsigned *>(&a.pending[s]), 0xFFFFFFFFu) == 1u;
     if (ready) {
-      const uint32_t nc = i == 0 ? m.s0nc : __ldg(&a.items[s].nchunks);
+      const uint32_t nc = i == 0 ? m.s0nc : ldro<NC>(&a.items[s].nchunks);
       if (nc == 1 && mailbox_put(mb, (unsigned long long)s << 32, i == 0 && m.s0stage, m.i0, m.i1, m.i2))
         continue;   // run it here
       const unsigned long long pos = atomicAdd(&a.ctr->tail, (unsigned long long)nc);
@@ -549,9 +562,10 @@ struct SlotState {
   unsigned long long ticket;
 };
 
+template <bool NC = true>
 __device__ __forceinline__ void finish_slot(const EpochArgs &a, SlotState &s) {
   const long long c1 = a.trace ? clock64() : 0;
-  release_unit(a, (uint32_t)(s.unit >> 32));
+  release_unit<NC>(a, (uint32_t)(s.unit >> 32));
   s.unreleased = false;
   if (a.trace) {
     const long long c2 = clock64();
@@ -564,18 +578,20 @@ __device__ __forceinline__ void finish_slot(const EpochArgs &a, SlotState &s) {
 }
 
 // Block until the unit in slot s is done by the compute warps, then release it.
+template <bool NC = true>
 __device__ __forceinline__ void drain_slot(const EpochArgs &a, SlotState &s, uint64_t *empty) {
   if (!s.unreleased) return;
   mbar_wait(empty, s.parity);
   s.parity ^= 1;
-  finish_slot(a, s);
+  finish_slot<NC>(a, s);
 }
 
 // If the unit in slot s is already done, release it now (non-blocking).
+template <bool NC = true>
 __device__ __forceinline__ void poll_slot(const EpochArgs &a, SlotState &s, uint64_t *empty) {
   if (s.unreleased && mbar_test(empty, s.parity)) {
     s.parity ^= 1;
-    finish_slot(a, s);
+    finish_slot<NC>(a, s);
   }
 }
 
@@ -892,17 +908,18 @@ __device__ __forceinline__ unsigned long long pop_ticket(const EpochArgs &a, uns
 
 // Stage a unit for the compute warps: its item descriptor (48 bytes, lanes
 // 0-2) and, for SCAL, its factor list into shared memory.
+template <bool NC = true>
 __device__ __forceinline__ void stage_unit(const EpochArgs &a, unsigned long long unit, DItem *item_dst,
                                            float *fac_dst, int lane) {
   if (unit == kStop) return;
   const DItem *it = a.items + (uint32_t)(unit >> 32);
-  if (lane < 3) reinterpret_cast<uint4 *>(item_dst)[lane] = __ldg(reinterpret_cast<const uint4 *>(it) + lane);
-  if ((__ldg(&it->kind) & K_MASK) == K_SCAL) {
-    const uint32_t k = __ldg(&it->k), arg = __ldg(&it->arg);
+  if (lane < 3) reinterpret_cast<uint4 *>(item_dst)[lane] = ldro<NC>(reinterpret_cast<const uint4 *>(it) + lane);
+  if ((ldro<NC>(&it->kind) & K_MASK) == K_SCAL) {
+    const uint32_t k = ldro<NC>(&it->k), arg = ldro<NC>(&it->arg);
     if (k == 1) {   // a single factor travels inline in arg: no dependent load
       if (lane == 0) fac_dst[0] = __uint_as_float(arg);
     } else {
-      for (uint32_t j = lane; j < k; j += 32) fac_dst[j] = __ldg(a.factors + arg + j);
+      for (uint32_t j = lane; j < k; j += 32) fac_dst[j] = ldro<NC>(a.factors + arg + j);
     }
   }
 }
@@ -1064,6 +1081,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
       }
       unit = __shfl_sync(0xffffffffu, unit, 0);
       staged = __shfl_sync(0xffffffffu, staged, 0);
+      __syncwarp();   // memory order: lane 0's ld.acquire of the unit before the other lanes' descriptor loads
       if (!staged) {
         stage_unit(a, unit, &s_item[b], s_fac[b], lane);
       } else if (lane == 0 && (s_item[b].kind & K_MASK) == K_SCAL) {
@@ -1231,6 +1249,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sw(Epoch
         }
       }
       unit = __shfl_sync(0xffffffffu, unit, 0);
+      __syncwarp();   // memory order: lane 0's ld.acquire of the unit before the other lanes' descriptor loads
       stage_unit(a, unit, &s_item[b], s_fac[b], lane);
       if (lane == 0) s_unit[b] = unit;
       __syncwarp();
@@ -1263,21 +1282,35 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
   return v;
 }
 
+// Give up ticket t at a close (device_abi.h, StreamCtl): the resume launch runs it.
+__device__ __forceinline__ void abandon_ticket(StreamCtl *ctl, unsigned long long t) {
+  const unsigned i = atomicAdd(&ctl->nabandoned, 1u);
+  if (i < (unsigned)kMaxStreamGrid) ctl->abandoned[i] = t;
+}
+
+// resume = 0: the run's launch; 1: its resume launch (after the last
+// publication), which runs what a closed first launch left.  quiesce_ns: how
+// long every CTA must have waited for a publication before the launch closes.
 template <bool PF>
-__global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sws(StreamCtl *ctl, uint64_t watchdog_ns) {
+__global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sws(StreamCtl *ctl, uint64_t watchdog_ns,
+                                                                             uint64_t quiesce_ns, int resume) {
   constexpr int kCompute = kComputeSW;
   __shared__ unsigned long long s_unit[2];
   __shared__ DItem s_item[2];
   __shared__ __align__(8) uint64_t s_empty[2];
   __shared__ __align__(16) float s_fac[2][kMaxFactors];
   __shared__ __align__(16) EpochArgs s_args[2];
+  __shared__ unsigned s_go;
   static_assert(sizeof(EpochArgs) % 8 == 0, "EpochArgs layout");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     mbar_init(&s_empty[0], kCompute / 32);
     mbar_init(&s_empty[1], kCompute / 32);
+    // a resume launch after a first launch that ran every sub-epoch: nothing to do
+    s_go = resume ? ld_acquire_u32(&ctl->resume) : 1u;
   }
   __syncthreads();
+  if (!s_go) return;
 
   if (warp == 0) {
     SlotState st[2];
@@ -1287,8 +1320,11 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sws(Stre
       st[b].unreleased = false;
     }
     int slot_sub[2] = {-1, -1};   // warp-uniform: the sub-epoch whose arguments s_args[b] holds
-    // lane 0: the sub-epoch this CTA's tickets have reached (tickets only grow)
+    // lane 0: the sub-epoch this CTA's tickets have reached (fresh tickets only
+    // grow; an abandoned one taken by the resume launch may lie lower: rescan)
     const unsigned nsub = __ldcg(&ctl->nsub);
+    const unsigned nab = resume ? min(__ldcg(&ctl->nabandoned), (unsigned)kMaxStreamGrid) : 0u;
+    bool fresh = !resume;            // lane 0: abandoned tickets exhausted
     unsigned cur = 0, pub = 0;
     unsigned long long base = 0, cur_units = ~0ull;   // ~0: not loaded yet
     unsigned long long *cur_queue = nullptr;
@@ -1298,9 +1334,20 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sws(Stre
       unsigned long long unit = kStop;
       unsigned sub = 0;
       if (lane == 0) {
-        drain_slot(s_args[b], st[b], &s_empty[b]);   // slot b's previous unit (u-2), with its sub-epoch's args
-        const unsigned long long t = atomicAdd(&ctl->ticket, 1ull);
-        bool stop = false;
+        drain_slot<false>(s_args[b], st[b], &s_empty[b]);   // slot b's previous unit (u-2), with its sub-epoch's args
+        unsigned long long t = 0;
+        if (!fresh) {
+          const unsigned i = atomicAdd(&ctl->ab_take, 1u);
+          if (i < nab) t = __ldcg(&ctl->abandoned[i]);
+          else fresh = true;
+        }
+        if (fresh) t = atomicAdd(&ctl->ticket, 1ull);
+        if (t < base) {   // (resume) an abandoned ticket below the current sub-epoch
+          cur = 0;
+          base = 0;
+          cur_units = ~0ull;
+        }
+        bool stop = false, waiting = false;
         uint64_t start = 0;
         // the sub-epoch holding ticket t (waiting for its publication)
         for (unsigned spin = 0;;) {
@@ -1311,17 +1358,42 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sws(Stre
           if (cur >= pub) {
             pub = ld_acquire_u32(&ctl->published);
             if (cur >= pub) {
-              if (spin == 0) start = globaltimer();
-              poll_slot(s_args[b ^ 1], st[b ^ 1], &s_empty[b ^ 1]);
+              if (spin == 0) {
+                start = globaltimer();
+                if (!resume) {   // counted while waiting (closing needs every CTA here)
+                  atomicAdd(&ctl->state, 1u);
+                  waiting = true;
+                }
+              }
+              poll_slot<false>(s_args[b ^ 1], st[b ^ 1], &s_empty[b ^ 1]);
               __nanosleep(spin < 64 ? 64 : 512);
               if ((++spin & 63) == 0) {
-                if (ld_relaxed_u32(&ctl->abort) || globaltimer() - start > watchdog_ns) {
+                const uint64_t waited = globaltimer() - start;
+                if (waiting && waited > quiesce_ns) {
+                  // every CTA waiting that long: close (one CAS), or join a close
+                  unsigned s = ld_relaxed_u32(&ctl->state);
+                  if (s == gridDim.x) s = atomicCAS(&ctl->state, gridDim.x, gridDim.x | kStreamClosed);
+                  if ((s & kStreamClosed) || s == gridDim.x) {
+                    abandon_ticket(ctl, t);
+                    stop = true;
+                    break;
+                  }
+                }
+                if (ld_relaxed_u32(&ctl->abort) || waited > watchdog_ns) {
                   atomicExch(&ctl->abort, 1u);   // the host sees the unfinished sub-epochs
                   stop = true;
                   break;
                 }
               }
               continue;
+            }
+          }
+          if (waiting) {   // leaving the wait: unless the launch was closed meanwhile
+            waiting = false;
+            if (atomicSub(&ctl->state, 1u) & kStreamClosed) {
+              abandon_ticket(ctl, t);
+              stop = true;
+              break;
             }
           }
           if (cur_units == ~0ull) {   // read past ld.acquire(published), L2 only
@@ -1341,7 +1413,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sws(Stre
           if (unit == Q_EMPTY) {
             const uint64_t t0 = globaltimer();
             for (unsigned spin = 0;; ++spin) {
-              poll_slot(s_args[b ^ 1], st[b ^ 1], &s_empty[b ^ 1]);
+              poll_slot<false>(s_args[b ^ 1], st[b ^ 1], &s_empty[b ^ 1]);
               __nanosleep(spin < 64 ? 32 : 256);
               unit = ld_acquire_u64(&cur_queue[lt]);
               if (unit != Q_EMPTY) break;
@@ -1369,6 +1441,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sws(Stre
       }
       unit = __shfl_sync(0xffffffffu, unit, 0);
       sub = __shfl_sync(0xffffffffu, sub, 0);
+      __syncwarp();   // memory order: lane 0's ld.acquire loads before the other lanes' reads of sub-epoch data
       if (unit != kStop && (int)sub != slot_sub[b]) {
         // stage the sub-epoch's arguments for slot b (its previous unit is
         // released); L2-only loads: subs[] is written during the launch
@@ -1378,39 +1451,54 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sws(Stre
         __syncwarp();
         slot_sub[b] = (int)sub;
       }
-      stage_unit(s_args[b], unit, &s_item[b], s_fac[b], lane);
+      stage_unit<false>(s_args[b], unit, &s_item[b], s_fac[b], lane);
       if (lane == 0) s_unit[b] = unit;
       __syncwarp();
       bar_arrive(kBarFull + b, 32 + kCompute);
       if (unit == kStop) {
-        if (lane == 0) drain_slot(s_args[b ^ 1], st[b ^ 1], &s_empty[b ^ 1]);   // unit u-1 still in flight
+        if (lane == 0) drain_slot<false>(s_args[b ^ 1], st[b ^ 1], &s_empty[b ^ 1]);   // unit u-1 still in flight
         break;
       }
     }
   } else {
     compute_loop<kCompute, kSlotsSW, PF, true>(s_args[0], s_args, s_unit, s_item, s_fac, s_empty, lane);
   }
-  // the last CTA to leave copies every published sub-epoch's counters to its
-  // mapped host copy (the host retires the sub-epochs one by one)
+  // the last CTA to leave: after a close, hand over to the resume launch
+  // (reset the launch-wide counts it reuses); otherwise copy every published
+  // sub-epoch's counters to its mapped host copy (the host retires the
+  // sub-epochs one by one)
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&ctl->exited, 1u) == gridDim.x - 1) {
       __threadfence();
-      const unsigned n = min(__ldcg(&ctl->nsub), ld_acquire_u32(&ctl->published));
-      for (unsigned r = 0; r < n; ++r) {
-        Counters *c = reinterpret_cast<Counters *>(
-            __ldcg(reinterpret_cast<const unsigned long long *>(&ctl->subs[r].ctr)));
-        volatile Counters *h = reinterpret_cast<volatile Counters *>(
-            __ldcg(reinterpret_cast<const unsigned long long *>(&ctl->subs[r].host_ctr)));
-        if (!c || !h) continue;   // published empty (close_stream)
-        h->head = atomicAdd(&c->head, 0ull);
-        h->tail = atomicAdd(&c->tail, 0ull);
-        h->done = atomicAdd(&c->done, 0ull);
-        h->error = atomicAdd(&c->error, 0u);
-        h->exited = gridDim.x;
+      if (!resume && (atomicAdd(&ctl->state, 0u) & kStreamClosed)) {
+        ctl->state = 0u;
+        ctl->exited = 0u;
+        ctl->ab_take = 0u;
+        __threadfence();
+        atomicExch(&ctl->resume, 1u);
+        // sub-epoch 0's mapped record: the resume launch did work (its time counts)
+        volatile Counters *h0 = reinterpret_cast<volatile Counters *>(
+            __ldcg(reinterpret_cast<const unsigned long long *>(&ctl->subs[0].host_ctr)));
+        if (h0) h0->pad = 1u;
+        __threadfence_system();
+      } else {
+        const unsigned n = min(__ldcg(&ctl->nsub), ld_acquire_u32(&ctl->published));
+        for (unsigned r = 0; r < n; ++r) {
+          Counters *c = reinterpret_cast<Counters *>(
+              __ldcg(reinterpret_cast<const unsigned long long *>(&ctl->subs[r].ctr)));
+          volatile Counters *h = reinterpret_cast<volatile Counters *>(
+              __ldcg(reinterpret_cast<const unsigned long long *>(&ctl->subs[r].host_ctr)));
+          if (!c || !h) continue;   // published empty (close_stream)
+          h->head = atomicAdd(&c->head, 0ull);
+          h->tail = atomicAdd(&c->tail, 0ull);
+          h->done = atomicAdd(&c->done, 0ull);
+          h->error = atomicAdd(&c->error, 0u);
+          h->exited = gridDim.x;
+        }
+        __threadfence_system();
       }
-      __threadfence_system();
     }
   }
 }
@@ -1654,9 +1742,10 @@ __global__ void __launch_bounds__(kBlockWQ, BT_WQ_MIN_CTAS) scheduler_kernel_wq(
 
 // Stream launch (runtime.cpp, flush_epoch): the "sw" kernel over the
 // sub-epochs the host publishes in *ctl.
-cudaError_t launch_stream(StreamCtl *ctl, uint64_t watchdog_ns, int grid, cudaStream_t stream, bool prefetch) {
-  if (prefetch) scheduler_kernel_sws<true><<<grid, kBlock, 0, stream>>>(ctl, watchdog_ns);
-  else scheduler_kernel_sws<false><<<grid, kBlock, 0, stream>>>(ctl, watchdog_ns);
+cudaError_t launch_stream(StreamCtl *ctl, uint64_t watchdog_ns, uint64_t quiesce_ns, int grid, cudaStream_t stream,
+                          bool prefetch, bool resume) {
+  if (prefetch) scheduler_kernel_sws<true><<<grid, kBlock, 0, stream>>>(ctl, watchdog_ns, quiesce_ns, resume ? 1 : 0);
+  else scheduler_kernel_sws<false><<<grid, kBlock, 0, stream>>>(ctl, watchdog_ns, quiesce_ns, resume ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -462,6 +462,87 @@ def test_stream_launch_deferred(B, tmp_path):
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
 
+_STREAM_ENV_CODE = (
+    "import numpy as np, oracle, workloads as W\n"
+    "from tests.test_gpu import run_device, repeated, assert_bits_equal\n"
+    "from paper_1304_0878_b200 import btask as B\n"
+    "p = W.c5_sharded(nx=300 * 8192, ntiles=300, sweeps=8)\n"
+    "res = 0\n"
+    "for flags in (0, B.BT_FLAG_NO_FUSION):\n"
+    "    out, st = run_device(B, p, repeats=2, flags=flags, pipeline_rounds=4, pipeline_min=200,\n"
+    "                         parallel_min=200, host_threads=3)\n"
+    "    assert_bits_equal(out[0], oracle.run(repeated(p, 2))[0], 'stream launch')\n"
+    "    assert st['epochs'] >= 4 and st['stream_closes'] == 0, st\n"
+    "    res += st['stream_resumes']\n"
+    "print('ok resumes', res)\n")
+
+
+def _run_stream_env(env_extra):
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, **env_extra)
+    r = subprocess.run([sys.executable, "-c", _STREAM_ENV_CODE], cwd=os.path.dirname(os.path.dirname(__file__)),
+                       env=env, capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+    return int(r.stdout.split("ok resumes")[1].split()[0])
+
+
+def test_stream_launch_auto_defer_launch_blocking(B):
+    """CUDA_LAUNCH_BLOCKING=1 serialises launches (as ncu and compute-sanitizer
+    do): the stream launch is deferred automatically after the last
+    publication -- no close, no resume, same bits."""
+    assert _run_stream_env({"CUDA_LAUNCH_BLOCKING": "1"}) == 0
+
+
+def test_stream_launch_closes_and_resumes_when_blocked(B):
+    """The same with auto-deferral disabled: the launch call blocks until the
+    kernel ends, the kernel runs sub-epoch 0, waits 50 ms for publications
+    that cannot come, closes itself, and the run's resume launch runs the
+    abandoned tickets and the rest -- bit-exact, never the watchdog."""
+    assert _run_stream_env({"CUDA_LAUNCH_BLOCKING": "1", "BT_STREAM_NODEFER": "1"}) >= 2
+
+
+def test_stream_launch_closes_and_resumes_slow_host(B):
+    """A host that publishes late (2 ms per sub-epoch, quiescence limit 0.2 ms)
+    while the launch really runs: closes race with publications; every run
+    stays bit-exact (the resume launch picks up what the close left)."""
+    n = _run_stream_env({"BT_DEBUG_PUBLISH_DELAY_US": "2000", "BT_QUIESCE_US": "200"})
+    assert n >= 1
+
+
+def test_failed_pipelined_run_reports_and_poisons(B):
+    """An epoch-memory allocation that fails inside a pipelined run (injected:
+    BT_DEBUG_FAIL_DEV_ALLOC) is returned from bt_insert_task_batch with no task
+    counted as submitted, and the runtime is poisoned -- never a silent
+    sequential replay that would scale tiles twice."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import errno, numpy as np, torch, workloads as W\n"
+        "from paper_1304_0878_b200 import btask as B\n"
+        "from paper_1304_0878_b200.programs import Session\n"
+        "p = W.c5_sharded(nx=300 * 8192, ntiles=300, sweeps=8)\n"
+        "x = torch.from_numpy(p.buffers[0].copy()).cuda()\n"
+        "rt = B.Runtime(pipeline_rounds=4, pipeline_min=200, parallel_min=200, host_threads=3)\n"
+        "s = Session(rt, p, device_tensors=[x])\n"
+        "h0, _ = s.handle_arrays()\n"
+        "c = np.ascontiguousarray(p.tasks['codelet']); f = np.ascontiguousarray(p.tasks['scalar'])\n"
+        "import ctypes\n"
+        "n = ctypes.c_size_t(12345)\n"
+        "rc = B.bt_insert_task_batch(rt.rt, len(c), c.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),\n"
+        "    f.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), h0.ctypes.data_as(ctypes.POINTER(B.bt_handle)),\n"
+        "    None, ctypes.byref(n))\n"
+        "assert rc < 0 and n.value == 0, (rc, n.value)\n"
+        "assert B.bt_task_wait_for_all(rt.rt) == -errno.EIO\n"
+        "print('ok', rc, rt.last_error())\n")
+    env = dict(os.environ, BT_DEBUG_FAIL_DEV_ALLOC="3")
+    r = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(os.path.dirname(__file__)), env=env,
+                       capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
 def uneven_rounds_program():
     rng = np.random.default_rng(77)
     nparts, tile = 400, 8192
