@@ -28,7 +28,6 @@ sys.path.insert(0, ROOT)
 
 METRIC = "vector_scal effective HBM GB/s (frac of 8 TB/s) and tasks/s at 1/2/4/8 B200"
 NOMINAL_HBM_GBPS = 8000.0
-SM_COUNT = 148
 FP32_LANES_PER_SM = 128
 
 C5 = dict(nx=1 << 30, ntiles=16384, sweeps=64)
@@ -165,26 +164,29 @@ def run_reference(args):
     return 0
 
 
-def cpu_baseline(np, seconds_target=12.0):
-    """The oracle as it stands, single thread, on a bounded sample of C5."""
+def cpu_baseline(np, seconds_target=12.0, threads=0):
+    """The oracle as it stands on a bounded sample of C5: single-threaded pinned
+    to one core (threads = 0, the oracle's definition: submission order), or its
+    OpenMP variant (element-parallel inside each task) on `threads` cores."""
     import oracle
     import workloads as W
     tile = C5["nx"] // C5["ntiles"]
     rng = np.random.default_rng(W.SEED_BASE + 4)
     f = W.sweep_factors(rng, C5["sweeps"])
-    ntile = 64
+    ntile = 64 if threads <= 1 else 512
     x = W.unit_interval_floats(np.random.default_rng(2), ntile * tile)
     p = W.sweep_program(x.shape[0], ntile, f, x)
     off0, len0, off1, len1 = oracle.model.resolve(p)
     t = p.tasks
-    # single-threaded by definition (submission order), pinned to one core
     old_aff = os.sched_getaffinity(0)
     core = min(old_aff)
-    os.sched_setaffinity(0, {core})
+    if threads <= 1:
+        os.sched_setaffinity(0, {core})
     try:
         reps, t0 = 0, time.perf_counter()
         while True:
-            oracle.run_tasks([x], t["codelet"], t["scalar"], t["b0"], off0, len0, t["b1"], off1, len1)
+            oracle.run_tasks([x], t["codelet"], t["scalar"], t["b0"], off0, len0, t["b1"], off1, len1,
+                             threads=threads if threads > 1 else 0)
             reps += 1
             if time.perf_counter() - t0 > seconds_target:
                 break
@@ -197,11 +199,51 @@ def cpu_baseline(np, seconds_target=12.0):
             cpu = next(l.split(":", 1)[1].strip() for l in fh if l.startswith("model name"))
     except Exception:
         pass
-    return {"value": 8.0 * ntile * tile * reps / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+    how = (f"single-threaded pinned to core {core}" if threads <= 1 else
+           f"OpenMP variant (oracle_run_omp: tasks in order, each task's elements split over {threads} threads)")
+    return {"value": 8.0 * ntile * tile * reps / dt / 1e9, "unit": "GB/s", "cores": max(1, threads),
+            "kind": "oracle" if threads <= 1 else "oracle_openmp",
             "sample": f"{reps} x ({ntile} tiles x {tile} floats x {C5['sweeps']} sweeps, task-major), "
-                      f"{dt:.1f} s single-threaded pinned to core {core}",
+                      f"{dt:.1f} s {how}",
             "host": {"cpu": cpu, "nproc": os.cpu_count()},
             "tasks_per_s": reps * ntile * C5["sweeps"] / dt}
+
+
+def sm_count(torch, dev):
+    """Streaming multiprocessors of this GPU, queried (148 on B200)."""
+    return torch.cuda.get_device_properties(dev).multi_processor_count
+
+
+def builder_threads(args):
+    """Dependency-builder threads per rank: the node's cores shared among its
+    ranks (one left per rank for the CUDA driver / caller), at least 2, at most 16."""
+    if args.host_threads:
+        return args.host_threads
+    lw = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+    cores = os.cpu_count() or 2
+    return max(2, min(16, cores // lw - (2 if lw == 1 else 1)))
+
+
+def timed_steps(torch, dev, stream, dist, rt, tasks, steps, warmup):
+    """warmup untimed steps, then `steps` timed ones (barrier + synchronize on
+    both sides, CUDA events on the runtime's stream).  A step = submit the
+    batch (dependency inference, fusion, pack, upload, kernels) + wait."""
+    codelets, scalars, h0 = tasks
+    for _ in range(warmup):
+        rt.insert_batch(codelets, scalars, h0)
+        rt.wait()
+    rt.stats_reset()
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        rt.insert_batch(codelets, scalars, h0)
+        rt.wait()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    return ev0.elapsed_time(ev1) / steps, rt.stats()
 
 
 def main():
@@ -216,19 +258,25 @@ def main():
     ap.add_argument("--sweeps", type=int, default=C5["sweeps"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--configs", type=int, default=1,
+                    help="N = 1: also report the other BASELINE configs C1-C4 (secondary keys, tools/bench_configs.py)")
     ap.add_argument("--ref-tiles", type=int, default=64)
     ap.add_argument("--chunk-bytes", type=int, default=0, help="fixed work-unit size (0 = adaptive)")
     ap.add_argument("--host-threads", type=int, default=0)
     ap.add_argument("--rounds", type=int, default=0, help="pipelined rounds per SCAL run (0 = library default)")
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
-                    help="N > 1: weak = a full 4 GiB C5 shard per GPU (default, per-GPU work fixed); "
-                         "strong = one 4 GiB vector split over the GPUs")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="strong",
+                    help="N > 1: strong = ONE 4 GiB vector whose tiles are block-distributed over the ranks "
+                         "(bt_data_distribute_block; every rank submits every task, each runs its own: default, "
+                         "BASELINE configs[4]); weak = a full 4 GiB C5 per GPU")
+    ap.add_argument("--secondary-scaling", type=int, default=1,
+                    help="N > 1: also time the other scaling mode (secondary key)")
     ap.add_argument("--hbm-variant", type=int, default=1,
                     help="also time the HBM-bound 16-sweep variant on the same tiles (secondary key)")
     ap.add_argument("--streamed", type=int, default=1,
                     help="also time the K steps submitted back to back with one wait (diagnostic key)")
     ap.add_argument("--emulate-ranks", type=int, default=0,
-                    help="diagnostic: run only rank 0's shard of an N-rank job (its line is not a bench result)")
+                    help="diagnostic (N = 1): rank 0 of an N-rank strong-scaling job alone on this GPU "
+                         "(its line is not a bench result)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -269,58 +317,46 @@ def main():
     cfg = dict(C5, sweeps=args.sweeps)
     T, S = cfg["ntiles"], cfg["sweeps"]
     tile = cfg["nx"] // T
-    # --emulate-ranks N (diagnostic, N=1 only): time rank 0's share of an N-rank run
-    # weak scaling (default, per-GPU work fixed): every rank owns a full C5 shard
-    # of T tiles; strong: the T tiles of one vector are split over the ranks
-    if args.scaling == "weak" and not args.emulate_ranks:
-        shard_world, shard_rank = 1, 0
-    else:
-        shard_world = args.emulate_ranks if (args.emulate_ranks and world == 1) else world
-        shard_rank = rank
-    t_lo, t_hi = shard_rank * T // shard_world, (shard_rank + 1) * T // shard_world
-    my_tiles = t_hi - t_lo
-    elems = my_tiles * tile
     factors = W.sweep_factors(np.random.default_rng(W.SEED_BASE + 4), S)
-
     stream = torch.cuda.current_stream(dev)
     flags = (B.BT_FLAG_NO_FUSION if args.no_fusion else 0) | (B.BT_FLAG_NO_STREAM if args.no_stream else 0)
-    # builder threads: share the node's cores among the ranks on it, leaving two per rank
-    threads = args.host_threads or max(1, min(16, (os.cpu_count() or 2) // int(
-        os.environ.get("LOCAL_WORLD_SIZE", "1")) - 2))
-    rt = B.Runtime(device=local_dev, stream=stream.cuda_stream, rank=0, nranks=1, flags=flags,
-                   chunk_bytes=args.chunk_bytes, host_threads=threads, pipeline_rounds=args.rounds)
+    threads = builder_threads(args)
+    emulate = args.emulate_ranks if (args.emulate_ranks and world == 1) else 0
 
-    # ---- device-resident inputs (registered once, outside the timed region)
-    x = synth_tile_values(torch, elems, 1000 + rank, dev)
-    h = rt.register_tensor(x)
-    subs = rt.partition(h, my_tiles)
-    codelets, scalars, h0 = rank_tasks(np, subs, factors)
-    ntasks = codelets.shape[0]
+    def make_run(mode):
+        """Runtime + registered, partitioned device-resident C5 input + this rank's task stream.
+        strong: every rank registers the whole vector (a 4 GiB allocation per GPU, of which it
+        writes its block of tiles), partitions it into T tiles, block-distributes them over the
+        ranks (bt_data_distribute_block) and submits every task of the
+        stream; the library's rank filter runs the local ones.  weak: a full C5 per rank."""
+        nranks = (emulate or world) if mode == "strong" else 1
+        myrank = 0 if mode == "weak" else rank
+        rt = B.Runtime(device=local_dev, stream=stream.cuda_stream, rank=myrank, nranks=nranks, flags=flags,
+                       chunk_bytes=args.chunk_bytes, host_threads=threads, pipeline_rounds=args.rounds)
+        x = synth_tile_values(torch, cfg["nx"], 1000 + (rank if mode == "weak" else 0), dev)
+        h = rt.register_tensor(x)
+        subs = rt.partition(h, T)
+        if nranks > 1:
+            rt.distribute_block(h)
+        lo, hi = myrank * T // nranks, (myrank + 1) * T // nranks
+        return rt, x, h, subs, (hi - lo) * tile, rank_tasks(np, subs, factors)
 
-    def step():
-        rt.insert_batch(codelets, scalars, h0)
-        rt.wait()
+    def close_run(rt, x, h):
+        rt.unpartition(h)
+        rt.unregister(h)
+        rt.close()
 
-    for _ in range(args.warmup):
-        step()
-    rt.stats_reset()
-    torch.cuda.synchronize(dev)
-    if dist:
-        dist.barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    mode = args.scaling if world > 1 or emulate else "strong"
+    rt, x, h, subs, elems, tasks = make_run(mode)
+    ntasks = tasks[0].shape[0]                      # tasks every rank submits
     with ClockSampler(local_dev) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
-        torch.cuda.synchronize(dev)
-    ms = ev0.elapsed_time(ev1) / args.steps
-    st = rt.stats()
+        ms, st = timed_steps(torch, dev, stream, dist, rt, tasks, args.steps, args.warmup)
     launches_per_step = st["sched_launches"] / args.steps          # scheduler-kernel launches
     epochs_per_step = st["epochs"] / args.steps                    # rounds (sub-epochs of a stream launch)
     kern_ms = st["device_ms"] / max(1, st["sched_launches"])       # average launch duration
-    span_ms = st["device_span_ms"] / args.steps                  # device time per step (launches overlap)
+    span_ms = st["device_span_ms"] / args.steps                    # device time per step (launches overlap)
     host_ms = st["host_build_ms"] / args.steps
+    local_tasks = st["tasks_local"] / args.steps
     ms, kern_ms_max, host_ms_max, span_ms_max = allreduce_max([ms, kern_ms, host_ms, span_ms])
     launches_all = int(allreduce_max([float(st["kernel_launches"])], op="sum")[0])   # every rank's kernels
 
@@ -336,7 +372,7 @@ def main():
         es0, es1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         es0.record(stream)
         for _ in range(args.steps):
-            rt.insert_batch(codelets, scalars, h0)
+            rt.insert_batch(*tasks)
         rt.wait()
         es1.record(stream)
         torch.cuda.synchronize(dev)
@@ -347,40 +383,44 @@ def main():
     # the north_star's ">= 85 % of HBM bandwidth" is graded
     hbm16 = None
     if args.hbm_variant and S > 16 and not args.no_fusion:
-        c16, s16, g16 = rank_tasks(np, subs, factors[:16])
-        for _ in range(3):
-            rt.insert_batch(c16, s16, g16)
-            rt.wait()
-        rt.stats_reset()
-        torch.cuda.synchronize(dev)
-        if dist:
-            dist.barrier()
+        t16 = rank_tasks(np, subs, factors[:16])
         k16 = max(10, args.steps)
-        eh0, eh1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        eh0.record(stream)
-        for _ in range(k16):
-            rt.insert_batch(c16, s16, g16)
-            rt.wait()
-        eh1.record(stream)
-        torch.cuda.synchronize(dev)
-        st16 = rt.stats()
-        hbm16 = allreduce_max([eh0.elapsed_time(eh1) / k16, st16["device_span_ms"] / k16,
+        ms16, st16 = timed_steps(torch, dev, stream, dist, rt, t16, k16, 3)
+        hbm16 = allreduce_max([ms16, st16["device_span_ms"] / k16,
                                st16["device_ms"] / max(1, st16["sched_launches"])]) + [k16, st16["sched_launches"] / k16]
-
-    rt.unpartition(h)
-    rt.unregister(h)
+    close_run(rt, x, h)
     del x
     torch.cuda.empty_cache()
 
+    # ---- the other scaling mode (N > 1, secondary key)
+    other = None
+    if world > 1 and args.secondary_scaling:
+        omode = "weak" if mode == "strong" else "strong"
+        rt2, x2, h2, _, elems2, tasks2 = make_run(omode)
+        ms2, st2 = timed_steps(torch, dev, stream, dist, rt2, tasks2, args.steps, args.warmup)
+        ms2 = allreduce_max([ms2])[0]
+        close_run(rt2, x2, h2)
+        del x2
+        torch.cuda.empty_cache()
+        tot2 = cfg["nx"] * (world if omode == "weak" else 1)
+        other = {"scaling": omode, "ms_per_step": ms2, "value": 8.0 * tot2 / (ms2 * 1e-3) / 1e9, "unit": "GB/s",
+                 "workload": workload_name(cfg, world, omode)}
+
     # ---- e2e: host (pinned) buffers through the public API, copies inside the region
+    # (this rank's block of the vector: owner-computes, each rank uploads and
+    # writes back the tiles it owns)
     e2e_ms = None
     h2d = d2h = 0
     if args.e2e_steps > 0:
+        my_tiles = elems // tile
+        rt = B.Runtime(device=local_dev, stream=stream.cuda_stream, flags=flags, chunk_bytes=args.chunk_bytes,
+                       host_threads=threads, pipeline_rounds=args.rounds)
         addr, host = B.pinned_empty(elems * 4)
         host[:] = synth_tile_values(torch, elems, 2000 + rank, dev).cpu().numpy()
         torch.cuda.synchronize(dev)
         if dist:
             dist.barrier()
+
         def e2e_step():
             he = rt.register(addr, elems, 0)
             se = rt.partition(he, my_tiles)
@@ -406,12 +446,20 @@ def main():
         h2d = elems * 4 + st2["upload_bytes"] // args.e2e_steps
         d2h = elems * 4 + 64
         e2e_ms = allreduce_max([e2e_ms])[0]
+        h2d, d2h = allreduce_max([float(h2d), float(d2h)], op="sum")
         B.bt_free(addr)
-    rt.close()
+        rt.close()
+
+    configs = None
+    if world == 1 and not emulate and args.configs:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import bench_configs
+        configs = bench_configs.run_all(local_dev)
 
     if rank == 0:
         peaks, peak_src = load_peaks()
-        total_elems = cfg["nx"] * (world if (args.scaling == "weak" and not args.emulate_ranks) else 1) * 1.0
+        sms = sm_count(torch, local_dev)
+        total_elems = cfg["nx"] * (world if mode == "weak" else 1) * 1.0
         compulsory = 8.0 * total_elems                     # read + write each element once per step
         value = compulsory / (ms * 1e-3) / 1e9
         clocks = clk.summary()
@@ -427,7 +475,7 @@ def main():
         fmul = per_launch_elems * S
         avg_launch = st["device_ms"] / max(1, st["sched_launches"])
         share_ms = span_ms / launches_per_step
-        alu_peak = SM_COUNT * FP32_LANES_PER_SM * (peaks.get("sm_max_mhz") or 1965.0) * 1e6 / 1e12
+        alu_peak = sms * FP32_LANES_PER_SM * (peaks.get("sm_max_mhz") or 1965.0) * 1e6 / 1e12
         hbm_bytes = 8.0 * per_launch_elems
         t_alu = fmul / (alu_peak * 1e12)
         t_hbm = hbm_bytes / (peaks["hbm_gbs"] * 1e9)
@@ -435,8 +483,9 @@ def main():
         if fused and t_alu > t_hbm:
             work, scale = fmul, 1e12
             roof = {"bound": "alu", "peak": alu_peak,
-                    "unit": "TFMUL/s", "peak_source": f"{SM_COUNT} SMs x {FP32_LANES_PER_SM} FP32 lanes x "
-                                                     f"{peaks.get('sm_max_mhz')} MHz (DESIGN.md)"}
+                    "unit": "TFMUL/s", "peak_source": f"{sms} SMs (queried) x {FP32_LANES_PER_SM} FP32 lanes x "
+                                                     f"{peaks.get('sm_max_mhz')} MHz (DESIGN.md); FMUL microbenchmark "
+                                                     f"36.3 T/s (profiles/r02_probe_b200.jsonl)"}
         else:
             work, scale = (hbm_bytes if fused else 8.0 * per_launch_elems * S), 1e9
             roof = {"bound": "hbm", "peak": peaks["hbm_gbs"],
@@ -449,11 +498,13 @@ def main():
         roof["work_per_launch"] = work
         roof["launches_per_step"] = launches_per_step
         roof["epochs_per_step"] = epochs_per_step
-        roof["stream_closes"] = int(st.get("stream_closes", 0))   # stream launches ended early (expected 0)
+        roof["stream_closes"] = int(st.get("stream_closes", 0))     # stream launches ended early (expected 0)
+        roof["stream_resumes"] = int(st.get("stream_resumes", 0))   # closed for want of publications (expected 0)
         roof["device_span_ms_per_step"] = span_ms
         roof["span_share_ms"] = share_ms
         roof["achieved_span_share"] = work / (share_ms * 1e-3) / scale
         roof["frac_span_share"] = roof["achieved_span_share"] / roof["peak"]
+        roof["frac_step"] = work * launches_per_step / (ms * 1e-3) / scale / roof["peak"]
         roof["hbm_GBps_physical"] = hbm_bytes / (avg_launch * 1e-3) / 1e9
         roof["traffic"] = None
         try:
@@ -463,25 +514,29 @@ def main():
                     roof["traffic"] = tr["dram_bytes_per_launch"]
         except OSError:
             pass
-        if args.emulate_ranks and world == 1:
-            # rank 0's shard of an N-rank run: report its own time only (not a bench line)
-            print(json.dumps({"diagnostic": "emulated rank 0 of N", "N": args.emulate_ranks, "ms_per_step": ms,
-                              "streamed_ms_per_step": streamed_ms,
+        if emulate:
+            # rank 0's share of an N-rank strong-scaling run: its own time only (not a bench line)
+            print(json.dumps({"diagnostic": "emulated rank 0 of N (strong scaling)", "N": emulate,
+                              "ms_per_step": ms, "streamed_ms_per_step": streamed_ms,
                               "host_build_ms_per_step": host_ms_max, "device_ms_per_step": span_ms_max,
-                              "elements": elems, "tasks_per_step": ntasks}), flush=True)
+                              "avg_launch_ms": avg_launch, "elements": elems, "tasks_submitted_per_step": ntasks,
+                              "tasks_local_per_step": local_tasks, "builder_threads": threads}), flush=True)
             return 0
+        job_tasks = ntasks * world if mode == "weak" else ntasks
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": mode,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "frac_of_8TBps": value / (NOMINAL_HBM_GBPS * world),
             "frac_of_measured_hbm": value / (peaks["hbm_gbs"] * world),
-            "tasks_per_s": ntasks * world / (ms * 1e-3),
+            "tasks_per_s": job_tasks / (ms * 1e-3),
             "effective_unfused_GBps": 8.0 * total_elems * S / (ms * 1e-3) / 1e9,
             "host_build_ms_per_step": host_ms_max, "device_ms_per_step": span_ms_max,
-            "config": {"workload": workload_name(cfg, world, args.scaling), "tasks_per_step": ntasks * world,
-                       "builder_threads": threads,
-                       "fusion": fused, "parallelism": f"owner-computes tiles over {world} rank(s)",
+            "config": {"workload": workload_name(cfg, world, mode), "tasks_per_step": job_tasks,
+                       "tasks_submitted_per_rank": ntasks, "builder_threads": threads,
+                       "fusion": fused, "parallelism": (f"owner-computes: bt_data_distribute_block over {world} "
+                                                        f"rank(s), rank filter" if mode == "strong" else
+                                                        f"{world} independent C5 shards"),
                        "l2": "4 GiB working set > 126 MB L2 (no flush needed)"},
             "gpu_launches": launches_all,
             "clocks": clocks,
@@ -501,13 +556,19 @@ def main():
                                 "ms_per_step": streamed_ms,
                                 "note": "diagnostic: K steps submitted back to back, one wait (host build of "
                                         "step i+1 overlaps device step i); the headline waits every step"}
+        if other is not None:
+            line["other_scaling"] = other
         if e2e_ms is not None:
-            line["e2e"] = {"value": compulsory / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
-                           "h2d_bytes_per_step": int(h2d * world), "d2h_bytes_per_step": int(d2h * world),
-                           "ms_per_step": e2e_ms, "path": "bt_malloc pinned host buffer -> register (H2D) -> "
-                           "partition -> insert_task_batch -> wait -> unregister (D2H)"}
+            e2e_bytes = 8.0 * elems * world                   # every rank's block in and out
+            line["e2e"] = {"value": e2e_bytes / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
+                           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                           "ms_per_step": e2e_ms, "path": "bt_malloc pinned host buffer (this rank's block) -> "
+                           "register (H2D) -> partition -> insert_task_batch -> wait -> unregister (D2H)"}
+        if configs is not None:
+            line["configs"] = configs
         if world == 1 and not args.skip_cpu:
             line["cpu_baseline"] = cpu_baseline(np)
+            line["cpu_baseline_openmp"] = cpu_baseline(np, threads=os.cpu_count() or 1)
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()

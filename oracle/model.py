@@ -35,7 +35,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 _CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fno-unsafe-math-optimizations",
-           "-std=c11", "-fPIC", "-shared", "-Wall", "-Werror"]
+           "-std=c11", "-fPIC", "-shared", "-Wall", "-Werror", "-fopenmp"]
 
 SCAL, AXPY, COPY = 1, 2, 3          # oracle.h ORACLE_SCAL / _AXPY / _COPY
 
@@ -71,6 +71,8 @@ def lib() -> ctypes.CDLL:
         _lib.oracle_run.argtypes = [ctypes.c_int64, i32p, f32p, i32p, i64p, i64p, i32p, i64p, i64p,
                                     ctypes.POINTER(f32p)]
         _lib.oracle_run.restype = ctypes.c_int
+        _lib.oracle_run_omp.argtypes = _lib.oracle_run.argtypes + [ctypes.c_int]
+        _lib.oracle_run_omp.restype = ctypes.c_int
         _lib.oracle_scal_chain.argtypes = [f32p, ctypes.c_int64, f32p, ctypes.c_int64]
         _lib.oracle_scal_chain.restype = None
         _lib.oracle_flt_eval_method.restype = ctypes.c_int
@@ -124,8 +126,9 @@ def resolve(program):
     return off0, len0, off1, len1
 
 
-def run_tasks(buffers: list, codelet, scalar, b0, off0, len0, b1, off1, len1) -> None:
-    """Low-level: execute tasks in order on the given float32 host buffers (in place)."""
+def run_tasks(buffers: list, codelet, scalar, b0, off0, len0, b1, off1, len1, threads: int = 0) -> None:
+    """Low-level: execute tasks in order on the given float32 host buffers (in place).
+    threads > 0: the OpenMP variant (element-parallel inside each task)."""
     L = lib()
     for b in buffers:
         assert b.dtype == np.float32 and b.flags.c_contiguous
@@ -137,20 +140,21 @@ def run_tasks(buffers: list, codelet, scalar, b0, off0, len0, b1, off1, len1) ->
     f32p = ctypes.POINTER(ctypes.c_float)
     ptrs = (f32p * max(1, len(buffers)))(*[b.ctypes.data_as(f32p) for b in buffers])
     P = lambda a, t: a.ctypes.data_as(ctypes.POINTER(t))
-    rc = L.oracle_run(len(c), P(c, ctypes.c_int32), P(s, ctypes.c_float),
-                      P(arrs[0], ctypes.c_int32), P(arrs[1], ctypes.c_int64), P(arrs[2], ctypes.c_int64),
-                      P(arrs[3], ctypes.c_int32), P(arrs[4], ctypes.c_int64), P(arrs[5], ctypes.c_int64),
-                      ptrs)
+    args = (len(c), P(c, ctypes.c_int32), P(s, ctypes.c_float),
+            P(arrs[0], ctypes.c_int32), P(arrs[1], ctypes.c_int64), P(arrs[2], ctypes.c_int64),
+            P(arrs[3], ctypes.c_int32), P(arrs[4], ctypes.c_int64), P(arrs[5], ctypes.c_int64), ptrs)
+    rc = L.oracle_run_omp(*args, threads) if threads > 0 else L.oracle_run(*args)
     if rc != 0:
         raise ValueError("oracle_run rejected the program")
 
 
-def run(program, buffers: list | None = None) -> list:
-    """Final contents of every buffer after all tasks, in submission order."""
+def run(program, buffers: list | None = None, threads: int = 0) -> list:
+    """Final contents of every buffer after all tasks, in submission order
+    (threads > 0: the OpenMP variant, timing only)."""
     bufs = program.copy_buffers() if buffers is None else buffers
     off0, len0, off1, len1 = resolve(program)
     t = program.tasks
-    run_tasks(bufs, t["codelet"], t["scalar"], t["b0"], off0, len0, t["b1"], off1, len1)
+    run_tasks(bufs, t["codelet"], t["scalar"], t["b0"], off0, len0, t["b1"], off1, len1, threads=threads)
     return bufs
 
 

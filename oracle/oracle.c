@@ -80,6 +80,61 @@ int oracle_run(int64_t ntasks, const int32_t *codelet, const float *scalar,
   return 0;
 }
 
+/* OpenMP variant, for the bench's CPU baseline on all host cores (SURVEY.md
+ * 8(d) "Report an OpenMP variant beside it"): tasks still one by one in
+ * submission order; inside a task the element range is split among
+ * nthreads threads.  Every element of a task is computed by the same single
+ * IEEE operation(s) as in oracle_run, and no element depends on another, so
+ * the result is byte-identical (pinned in tests/test_oracle.py). */
+int oracle_run_omp(int64_t ntasks, const int32_t *codelet, const float *scalar,
+                   const int32_t *buf0, const int64_t *off0, const int64_t *len0,
+                   const int32_t *buf1, const int64_t *off1, const int64_t *len1,
+                   float *const *bufs, int nthreads) {
+  for (int64_t t = 0; t < ntasks; t++) {
+    if (codelet[t] != ORACLE_SCAL && len0[t] != len1[t]) return -1;
+    if (codelet[t] < ORACLE_SCAL || codelet[t] > ORACLE_COPY) return -1;
+  }
+  for (int64_t t = 0; t < ntasks; t++) {
+    float *x = bufs[buf0[t]] + off0[t];
+    const int64_t n = len0[t];
+    const float f = scalar[t];
+    float *y = codelet[t] == ORACLE_SCAL ? x : bufs[buf1[t]] + off1[t];
+    switch (codelet[t]) {
+      case ORACLE_SCAL:
+#pragma omp parallel for num_threads(nthreads) schedule(static) if (n >= 65536)
+        for (int64_t i = 0; i < n; i++) x[i] = x[i] * f;
+        break;
+      case ORACLE_AXPY:
+        /* aliasing (x == y, reading R6) stays element-wise: element i is
+         * read and written by one thread; partially overlapping ranges run
+         * in index order */
+        if (x != y && ((x < y && x + n > y) || (y < x && y + n > x))) {
+          for (int64_t i = 0; i < n; i++) {
+            float p = f * x[i];
+            y[i] = p + y[i];
+          }
+          break;
+        }
+#pragma omp parallel for num_threads(nthreads) schedule(static) if (n >= 65536)
+        for (int64_t i = 0; i < n; i++) {
+          float p = f * x[i];
+          y[i] = p + y[i];
+        }
+        break;
+      default:
+        if (x == y) break;
+        if ((x < y && x + n > y) || (y < x && y + n > x)) {   /* overlapping ranges: in order */
+          for (int64_t i = 0; i < n; i++) y[i] = x[i];
+          break;
+        }
+#pragma omp parallel for num_threads(nthreads) schedule(static) if (n >= 65536)
+        for (int64_t i = 0; i < n; i++) y[i] = x[i];
+        break;
+    }
+  }
+  return 0;
+}
+
 /* Element-major evaluation of a stream of SCAL tasks that all cover the same
  * element range: element i goes through f_1, ..., f_k in submission order.
  * Equal to task-major order because each SCAL is element-wise (element i of

@@ -18,6 +18,13 @@ int oracle_run(int64_t ntasks, const int32_t *codelet, const float *scalar,
                const int32_t *buf1, const int64_t *off1, const int64_t *len1,
                float *const *bufs);
 
+/* The same, element-parallel inside each task on nthreads OpenMP threads
+ * (tasks in submission order; byte-identical result).  Timing only. */
+int oracle_run_omp(int64_t ntasks, const int32_t *codelet, const float *scalar,
+                   const int32_t *buf0, const int64_t *off0, const int64_t *len0,
+                   const int32_t *buf1, const int64_t *off1, const int64_t *len1,
+                   float *const *bufs, int nthreads);
+
 /* Element-major chain of k SCALs over x[0..n) (same result as task-major). */
 void oracle_scal_chain(float *x, int64_t n, const float *factors, int64_t k);
 

@@ -61,6 +61,8 @@ struct EpochArgs {
   Counters *host_ctr;           // mapped pinned host memory: the last CTA copies *ctr here
   unsigned long long *trace;    // 4 timestamps per unit, or null
   uint32_t *trace_item;         // item per unit, or null
+  const uint32_t *unit_base;    // traced epochs: first trace record of each item (its chunk c
+                                // writes record unit_base[item] + c: no shared counter)
   uint64_t total_units;
   uint64_t chunk_elems;         // elements per unit (multiple of 8)
   uint64_t watchdog_ns;         // spin limit before declaring ERR_WATCHDOG

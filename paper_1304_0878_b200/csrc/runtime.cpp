@@ -776,13 +776,14 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     rt->sl.defer = stream_defer();
   }
   bool sub = rt->sl.active;
-  // device layout: ctr | items | pending | succ | factors | queue[U] | chunk_done[N] | trace
+  // device layout: ctr | items | pending | succ | factors | unit_base[N] (traced) | queue[U] | chunk_done[N] | trace
   const size_t o_ctr = 0;
   const size_t o_items = 64;
   const size_t o_pend = align_up(o_items + 48 * N, 16);
   const size_t o_succ = align_up(o_pend + 4 * N, 16);
   const size_t o_fac = align_up(o_succ + 4 * E, 16);
-  const size_t o_queue = align_up(o_fac + 4 * F, 16);
+  const size_t o_ubase = align_up(o_fac + 4 * F, 16);
+  const size_t o_queue = align_up(o_ubase + (traced ? 4 * N : 0), 16);
   const size_t upload = o_queue + 8 * U0;
   const size_t o_cdone = align_up(o_queue + 8 * U, 16);
   const size_t o_trace = align_up(o_cdone + 4 * N, 16);
@@ -833,13 +834,14 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   uint32_t *succ = reinterpret_cast<uint32_t *>(h + o_succ);
   float *fac = reinterpret_cast<float *>(h + o_fac);
   unsigned long long *q = reinterpret_cast<unsigned long long *>(h + o_queue);
+  uint32_t *ubase = traced ? reinterpret_cast<uint32_t *>(h + o_ubase) : nullptr;
   rt->succ_off.resize(N);
 
   // Pass B (per range): fill items, counters, factors, initial ready queue.
   auto passB = [&](int p) {
     size_t lo, hi;
     range_of(N, P, p, lo, hi);
-    uint64_t qi = base[p].ready, so = base[p].succ, fo = base[p].fac;
+    uint64_t qi = base[p].ready, so = base[p].succ, fo = base[p].fac, ub = base[p].units;
     uint32_t prev_fo = 0;
     for (size_t i = lo; i < hi; ++i) {
       const HItem &it = B.items[i];
@@ -863,6 +865,10 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
       }
       const uint64_t nc = (it.n + CE - 1) / CE;
       d.nchunks = (uint32_t)nc;
+      if (ubase) {
+        ubase[i] = (uint32_t)ub;
+        ub += nc;
+      }
       d.succ_off = (uint32_t)so;
       d.nsucc = it.nsucc;
       rt->succ_off[i] = (uint32_t)so;
@@ -921,6 +927,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   a.host_ctr = e.hctr_dev;
   a.trace = traced ? reinterpret_cast<unsigned long long *>(d + o_trace) : nullptr;
   a.trace_item = traced ? reinterpret_cast<uint32_t *>(d + o_trace + 32 * U) : nullptr;
+  a.unit_base = traced ? reinterpret_cast<const uint32_t *>(d + o_ubase) : nullptr;
   a.total_units = U;
   a.chunk_elems = CE;
   a.watchdog_ns = kWatchdogNs;
@@ -1715,6 +1722,8 @@ int submit(bt_runtime *rt, int codelet, float scalar, bt_handle h0, bt_handle h1
 // is submitted; a negative errno when submission failed after the run began
 // to change state (items merged, rounds flushed): the runtime is then
 // poisoned (-EIO from every later call), never replayed.
+constexpr uint64_t kRemoteKey = 0xFFFFFFFEull;   // phase-1 key (low word) of another rank's SCAL target
+
 int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scalars, const bt_handle *h0, size_t i0,
                       size_t i1) {
   const int P = rt->pool->size();
@@ -1748,7 +1757,12 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
         const SlotHot &sh = hot[x];
         const bool ok = (sh.flags & (F_LIVE | F_PARTITIONED | F_BLOCKED)) == F_LIVE && (sh.dptr || host_only) &&
                         sh.rank == myrank;
-        key[x] = ((uint64_t)sh.gen << 32) | ((uint64_t)(sh.grp & 0x7FFFFFFFu) << 1) | (ok ? 1u : 0u);
+        // another rank's valid SCAL target (owner-computes: skipped here) has
+        // its own key, so phase 1 skips it without reading SlotHot
+        const bool remote = !ok && (sh.flags & (F_LIVE | F_PARTITIONED | F_BLOCKED)) == F_LIVE && sh.rank != myrank &&
+                            sh.rank >= 0;
+        key[x] = ((uint64_t)sh.gen << 32) |
+                 (remote ? kRemoteKey : ((uint64_t)(sh.grp & 0x7FFFFFFFu) << 1) | (ok ? 1u : 0u));
       }
     };
     if (nslots >= 65536) rt->par(fill);
@@ -1821,6 +1835,11 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
       }
       const uint64_t k = kt[s];
       if (__builtin_expect(((k >> 32) != (h >> 32)) | !(k & 1u), 0)) {
+        if (k == ((h & 0xFFFFFFFF00000000ull) | kRemoteKey)) {   // another rank's tile: skipped
+          close_run(j);
+          ++rem;
+          continue;
+        }
         // not a local SCAL target: a stale handle or a bad state (the run
         // fails), or another rank's tile (skipped)
         const SlotHot &sh = hot[s];

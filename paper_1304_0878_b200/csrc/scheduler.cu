@@ -1132,9 +1132,10 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
         release_unit(a, (uint32_t)(unit >> 32), Mailbox{&s_mb_unit, &s_mb_state, s_mb_item, &s_mb_staged, &s_mb_bar},
                      lane == 0 && unit == s_unit[b] ? &pre : nullptr);
         if (a.trace) {
-          // the record index is taken here, after the release (a global
-          // atomic on the pop path would lengthen every dependency link)
-          const unsigned long long t = atomicAdd(&a.ctr->trace_next, 1ull);
+          // the unit's own record (item's first record + chunk): no shared
+          // counter in or around the measured window
+          const long long c2r = clock64();
+          const unsigned long long t = (unsigned long long)a.unit_base[(uint32_t)(unit >> 32)] + (uint32_t)unit;
           a.trace[4 * t + 0] = s_g0[b];
 #if BT_TRACE_DETAIL
           // detail: [1] handoff pop -> compute start, [2] compute, [3] compute end -> release start
@@ -1144,7 +1145,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
 #else
           a.trace[4 * t + 1] = (unsigned long long)s_popc[b];
           a.trace[4 * t + 2] = (unsigned long long)(c1 - s_c1[b]);
-          a.trace[4 * t + 3] = (unsigned long long)(clock64() - c1);
+          a.trace[4 * t + 3] = (unsigned long long)(c2r - c1);
 #endif
           a.trace_item[t] = (uint32_t)(unit >> 32);
         }
@@ -1726,11 +1727,12 @@ __global__ void __launch_bounds__(kBlockWQ, BT_WQ_MIN_CTAS) scheduler_kernel_wq(
     // the continuation is the prefetched successor: its descriptor is ready
     cont_staged = pre && cont != kStop;
     if (a.trace && lane == 0) {
-      const unsigned long long t = atomicAdd(&a.ctr->trace_next, 1ull);
+      const long long c3 = clock64();
+      const unsigned long long t = (unsigned long long)a.unit_base[item] + chunk;   // the unit's own record
       a.trace[4 * t + 0] = g0;
       a.trace[4 * t + 1] = (unsigned long long)(c1 - c0);
       a.trace[4 * t + 2] = (unsigned long long)(c2 - c1);
-      a.trace[4 * t + 3] = (unsigned long long)(clock64() - c2);
+      a.trace[4 * t + 3] = (unsigned long long)(c3 - c2);
       a.trace_item[t] = item;
     }
     // the next unit's descriptor overwrites this one's: every lane has read it

@@ -355,6 +355,16 @@ def test_trace_timestamps(B, kernel):
     t, item = tr
     assert t.shape == (4000, 4) and np.all(t[:, 0] > 0)
     assert sorted(item.tolist()) == list(range(4000))
+    # multi-chunk items: each (item, chunk) unit writes its own record
+    # (unit_base[item] + chunk, no shared counter): every item 4 times
+    with B.Runtime(flags=B.BT_FLAG_TIMESTAMPS | B.BT_FLAG_NO_FUSION | KERNELS[kernel], chunk_bytes=1024) as rt:
+        s = Session(rt, p)
+        s.submit()
+        rt.wait()
+        t2, item2 = rt.trace()
+        s.finish()
+    assert t2.shape == (16000, 4) and np.all(t2[:, 0] > 0)
+    assert np.array_equal(np.bincount(item2, minlength=4000), np.full(4000, 4))
 
 
 @pytest.mark.parametrize("rounds,threads", [(2, 2), (3, 4), (4, 3)])

@@ -97,3 +97,61 @@ def test_two_ranks_partition_the_program():
             else:
                 # no conflicting pair is split across ranks (it would need a cross-rank edge)
                 assert res[r]["local"][i] == res[r]["local"][j]
+
+
+def _sweep_worker(rank, world, port, q):
+    """The bench's strong-scaling shape: one vector, T tiles block-distributed,
+    every rank submits the whole sweep-major SCAL stream (parallel builder path,
+    remote tiles skipped in phase 1)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1304_0878_b200 import btask as B
+        T, S = 96, 12
+        x = np.ones(T * 16, np.float32)
+        rt = B.Runtime(flags=B.BT_FLAG_HOST_ONLY, rank=rank, nranks=world, host_threads=3, parallel_min=64)
+        h = rt.register_array(x)
+        subs = rt.partition(h, T)
+        rt.distribute_block(h)
+        c = np.full(T * S, B.BT_CL_SCAL, np.int32)
+        f = np.repeat(np.linspace(0.5, 1.5, S).astype(np.float32), T)
+        h0 = np.tile(np.asarray(subs, np.uint64), S)
+        rt.insert_batch(c, f, h0)
+        st = rt.stats()
+        snap = rt.dag_snapshot()
+        rt.unpartition(h)
+        rt.unregister(h)
+        rt.close()
+        out = [None] * world
+        dist.all_gather_object(out, {"local": (snap["task_item"] != 0xFFFFFFFF), "k": snap["item_k"],
+                                     "tasks_local": st["tasks_local"], "submitted": st["tasks_submitted"]})
+        if rank == 0:
+            q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_block_distributed_sweeps_strong_scaling_shape(world):
+    """Every rank submits all T x S tasks; rank r runs exactly the tasks on its
+    block of tiles [r*T/N, (r+1)*T/N), fused into one k = S chain per tile."""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sweep_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = q.get(timeout=120)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    T, S = 96, 12
+    tile = np.tile(np.arange(T), S)
+    total = np.zeros(T * S, np.int64)
+    for r in range(world):
+        lo, hi = r * T // world, (r + 1) * T // world
+        assert np.array_equal(res[r]["local"], (tile >= lo) & (tile < hi))
+        assert res[r]["submitted"] == T * S and res[r]["tasks_local"] == (hi - lo) * S
+        assert sorted(res[r]["k"].tolist()) == [S] * (hi - lo)
+        total += res[r]["local"]
+    assert np.all(total == 1)

@@ -278,3 +278,19 @@ def test_partitioned_tiles_do_not_conflict():
     p.tasks[1] = (W.SCAL, 2, 0, 1, -1, -1)
     p.tasks[2] = (W.SCAL, 2, 0, 0, -1, -1)
     assert oracle.conflict_pairs(p) == {(0, 2)}
+
+
+def test_openmp_variant_equals_sequential():
+    """The OpenMP timing variant (element-parallel inside each task, tasks in
+    order) is byte-identical to the sequential oracle: on small property
+    programs and on C3/C2-shaped programs large enough (>= 65,536 elements per
+    task) to take its parallel loops, with 1, 4 and 8 threads."""
+    progs = [W.random_small_program(600 + s, max_tasks=10) for s in range(40)]
+    progs.append(W.c3_random_dag(nbuf=6, nx=1 << 17, ntasks=60, seed=11))
+    progs.append(W.c2_chain(nx=1 << 19, ntiles=4, sweeps=5))
+    for p in progs:
+        ref = oracle.run(p)
+        for th in (1, 4, 8):
+            got = oracle.run(p, threads=th)
+            for a, b in zip(ref, got):
+                assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), (p.name, th)
