@@ -8,6 +8,9 @@
 // 504-507) and owner-computes rank filtering.
 #include <cuda_runtime.h>
 #include <errno.h>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -60,7 +63,7 @@ constexpr uint32_t kDefaultPipelineMin = 131072;
 constexpr int kEpochRing = 12;                      // epoch buffers in flight (>= rounds + 2)
 constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;   // 20 s
 constexpr uint64_t kQuiesceNs = 50ull * 1000 * 1000;             // stream launch: close after 50 ms without a publication
-constexpr size_t kParallelPack = 4096;              // items above which the pack runs on the pool
+constexpr size_t kParallelPack = 1024;              // items above which the pack runs on the pool
 constexpr uint64_t kWarpUnitMax = 4096;             // units of at most this many elements use "wq"
 constexpr uint64_t kPrefetchBelowK = 32;            // "sw" epochs with shorter average chains prefetch
 constexpr uint64_t kUploadChunk = 64ull << 20;      // registrations >= this upload in chunks on a copy stream
@@ -1724,6 +1727,37 @@ int submit(bt_runtime *rt, int codelet, float scalar, bt_handle h0, bt_handle h1
 // poisoned (-EIO from every later call), never replayed.
 constexpr uint64_t kRemoteKey = 0xFFFFFFFEull;   // phase-1 key (low word) of another rank's SCAL target
 
+// Phase 1 of scal_run_parallel, 8 tasks per step (AVX-512, selected at run
+// time): 1 if all 8 are SCAL tasks whose slot key equals (their handle's
+// generation | low) -- they continue the open run of group low >> 1 --, 2 if
+// all 8 are valid SCALs on another rank's tiles, 0 otherwise (the caller then
+// takes them one by one).  Slot indices are range-checked before the gather.
+#if defined(__x86_64__)
+__attribute__((target("avx512f,avx512vl"))) int block8(const bt_handle *h, const int32_t *c, const uint64_t *kt,
+                                                       uint64_t nslots, uint64_t low) {
+  const __m512i hv = _mm512_loadu_si512(h);
+  const __m256i cv = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(c));
+  const __mmask8 okc = _mm256_cmpeq_epi32_mask(cv, _mm256_set1_epi32(BT_CL_SCAL));
+  const __m512i lo32 = _mm512_set1_epi64(0xFFFFFFFFll);
+  const __m512i s = _mm512_sub_epi64(_mm512_and_si512(hv, lo32), _mm512_set1_epi64(1));
+  const __mmask8 oks = _mm512_cmplt_epu64_mask(s, _mm512_set1_epi64((long long)nslots));
+  if ((__mmask8)(okc & oks) != 0xFF) return 0;
+  const __m512i k = _mm512_i64gather_epi64(s, reinterpret_cast<const long long *>(kt), 8);
+  const __m512i gen = _mm512_andnot_si512(lo32, hv);
+  if (low && _mm512_cmpeq_epi64_mask(k, _mm512_or_si512(gen, _mm512_set1_epi64((long long)low))) == 0xFF) return 1;
+  if (_mm512_cmpeq_epi64_mask(k, _mm512_or_si512(gen, _mm512_set1_epi64((long long)kRemoteKey))) == 0xFF) return 2;
+  return 0;
+}
+bool phase1_simd() {
+  static const bool ok = getenv("BT_NO_SIMD") == nullptr && __builtin_cpu_supports("avx512f") &&
+                         __builtin_cpu_supports("avx512vl");
+  return ok;
+}
+#else
+int block8(const bt_handle *, const int32_t *, const uint64_t *, uint64_t, uint64_t) { return 0; }
+bool phase1_simd() { return false; }
+#endif
+
 int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scalars, const bt_handle *h0, size_t i0,
                       size_t i1) {
   const int P = rt->pool->size();
@@ -1826,31 +1860,27 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
       cur = NONE;
     };
     if (dbg) tloop[c] = now_ms();
-    for (size_t j = lo; j < hi; ++j) {
+    // one task: false if the run must be rejected
+    auto step = [&](size_t j) -> bool {
       const bt_handle h = h0[i0 + j];
       const uint32_t s = (uint32_t)(h & 0xFFFFFFFFull) - 1u;   // handle index 0 wraps to UINT32_MAX
-      if (__builtin_expect(codelets[i0 + j] != BT_CL_SCAL || s >= nslots, 0)) {
-        bad[c] = 1;
-        return;
-      }
+      if (__builtin_expect(codelets[i0 + j] != BT_CL_SCAL || s >= nslots, 0)) return false;
       const uint64_t k = kt[s];
       if (__builtin_expect(((k >> 32) != (h >> 32)) | !(k & 1u), 0)) {
         if (k == ((h & 0xFFFFFFFF00000000ull) | kRemoteKey)) {   // another rank's tile: skipped
           close_run(j);
           ++rem;
-          continue;
+          return true;
         }
         // not a local SCAL target: a stale handle or a bad state (the run
         // fails), or another rank's tile (skipped)
         const SlotHot &sh = hot[s];
         if (sh.gen != (uint32_t)(h >> 32) || (sh.flags & (F_LIVE | F_PARTITIONED | F_BLOCKED)) != F_LIVE ||
-            (!sh.dptr && !host_only) || sh.rank == myrank || sh.rank < 0) {
-          bad[c] = 1;
-          return;
-        }
+            (!sh.dptr && !host_only) || sh.rank == myrank || sh.rank < 0)
+          return false;
         close_run(j);
         ++rem;
-        continue;
+        return true;
       }
       const uint32_t g = (uint32_t)k >> 1;
       if (g != cur) {
@@ -1858,7 +1888,37 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
         cur = g;
         run0 = j;
       }
+      return true;
+    };
+    size_t j = lo;
+    if (phase1_simd()) {
+      // 8 tasks at a time while they continue the open run (or are all
+      // another rank's); any other block of 8 goes through step()
+      for (; j + 8 <= hi;) {
+        const int r = block8(h0 + i0 + j, codelets + i0 + j, kt, nslots,
+                             cur == NONE ? 0ull : ((uint64_t)cur << 1) | 1u);
+        if (r == 1) {
+          j += 8;
+          continue;
+        }
+        if (r == 2) {
+          close_run(j);
+          rem += 8;
+          j += 8;
+          continue;
+        }
+        for (const size_t e = j + 8; j < e; ++j)
+          if (!step(j)) {
+            bad[c] = 1;
+            return;
+          }
+      }
     }
+    for (; j < hi; ++j)
+      if (!step(j)) {
+        bad[c] = 1;
+        return;
+      }
     close_run(hi);
     remote[c] = rem;
     if (dbg) tend[c] = now_ms();
