@@ -54,7 +54,8 @@ extern "C" {
 #endif
 
 #define BT_ABI_VERSION 4   /* 2: bt_stats.kernel_launches, BT_FLAG_KERNEL_*; 3: bt_stats.sched_launches,
-                               BT_FLAG_NO_STREAM; 4: bt_stats.stream_resumes, bt_debug_gate */
+                               BT_FLAG_NO_STREAM; 4: bt_stats.stream_resumes, bt_stats.prio_epochs,
+                               BT_FLAG_PRIORITY, bt_debug_gate */
 
 typedef struct bt_runtime bt_runtime;
 typedef uint64_t bt_handle;
@@ -83,6 +84,9 @@ enum {
   BT_FLAG_SYNC_EPOCH = 1u << 3, /* debugging: synchronise after every epoch launch */
   BT_FLAG_NO_STREAM  = 1u << 4, /* one launch per pipelined round instead of one stream launch per
                                    run ("Stream launches"); for comparisons */
+  BT_FLAG_PRIORITY   = 1u << 5, /* DAG epochs on the CTA-wide "sw" bodies: ready work ordered by upward rank
+                                   (priority levels) instead of FIFO.
+                                   Off by default: measured neutral on C3, slower on smaller DAGs */
   /* testing: force one scheduler variant for every epoch instead of the
    * per-epoch choice (DESIGN.md section "Persistent scheduler kernels"); at
    * most one of the three may be set (-EINVAL otherwise) */
@@ -277,6 +281,7 @@ typedef struct bt_stats {
                                  epoch buffer, or the run failed part-way) */
   uint64_t stream_resumes;    /* stream launches that closed themselves (no publication for 50 ms, e.g.
                                  under a launch-serialising tool) and were finished by their resume launch */
+  uint64_t prio_epochs;       /* epochs run with the priority ready queue (upward-rank levels) */
 } bt_stats;
 int bt_stats_get(bt_runtime *rt, bt_stats *out);
 int bt_stats_reset(bt_runtime *rt);

@@ -22,6 +22,7 @@ BT_ABI_VERSION = 4
 BT_R, BT_W, BT_RW = 1, 2, 3
 BT_CL_SCAL, BT_CL_AXPY, BT_CL_COPY = 1, 2, 3
 BT_FLAG_NO_FUSION, BT_FLAG_HOST_ONLY, BT_FLAG_TIMESTAMPS, BT_FLAG_SYNC_EPOCH, BT_FLAG_NO_STREAM = 1, 2, 4, 8, 16
+BT_FLAG_PRIORITY = 32
 BT_FLAG_KERNEL_SW, BT_FLAG_KERNEL_RW, BT_FLAG_KERNEL_WQ = 1 << 8, 1 << 9, 1 << 10
 
 bt_handle = ctypes.c_uint64
@@ -42,7 +43,7 @@ class bt_stats(ctypes.Structure):
                 ("device_ms", ctypes.c_double), ("device_span_ms", ctypes.c_double), ("grid", ctypes.c_uint32),
                 ("block", ctypes.c_uint32), ("kernel_launches", ctypes.c_uint64),
                 ("sched_launches", ctypes.c_uint64), ("stream_closes", ctypes.c_uint64),
-                ("stream_resumes", ctypes.c_uint64)]
+                ("stream_resumes", ctypes.c_uint64), ("prio_epochs", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

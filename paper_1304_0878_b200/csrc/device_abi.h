@@ -47,6 +47,31 @@ static_assert(sizeof(Counters) == 64, "Counters layout");
 
 enum : uint32_t { ERR_NONE = 0, ERR_BAD_KIND = 1, ERR_WATCHDOG = 2, ERR_BAD_UNIT = 3 };
 
+// ---- priority ready queue (PAPER.md:91-96 HEFT, 1005-1018) --
+// DAG epochs on the "sw" kernel order ready work by the item's upward rank
+// (bytes on the longest path from the item to the end of the epoch, the
+// item's own included): items are dealt to kMaxBuckets levels (DItem::kind
+// bits 16-23, higher = more urgent), and every level is a FIFO of its own.  A
+// level's unit count is known on the host, so a level is a ticket queue like
+// the single FIFO: a CTA holds at most one ticket per level (taken only when
+// the level has unclaimed units, so no CTA waits on an empty level while others
+// have work), runs the most urgent of its published tickets, and leaves when
+// every level is exhausted.  No CAS anywhere.
+// Level b's positions: t < ready -> queue[rbase + t] (initially ready units,
+// uploaded), else queue[U0 + pbase + t - ready] (published at release; the
+// region after the U0 initially ready units is EMPTY at launch).
+constexpr int kMaxBuckets = 8;
+constexpr uint32_t K_BUCKET_SHIFT = 16;
+struct alignas(16) Bucket {
+  unsigned long long head;   // next ticket
+  unsigned long long tail;   // positions reserved by releases (starts at ready)
+  uint32_t total;            // units of this level in the epoch
+  uint32_t ready;            // initially ready units
+  uint32_t rbase;            // first initially ready unit in queue[]
+  uint32_t pbase;            // first published unit in queue[U0 + ...]
+};
+static_assert(sizeof(Bucket) == 32, "Bucket layout");
+
 // A queue slot holds (item << 32) | chunk; EMPTY until published.
 constexpr unsigned long long Q_EMPTY = ~0ull;
 
@@ -63,6 +88,9 @@ struct EpochArgs {
   uint32_t *trace_item;         // item per unit, or null
   const uint32_t *unit_base;    // traced epochs: first trace record of each item (its chunk c
                                 // writes record unit_base[item] + c: no shared counter)
+  Bucket *bk;                   // priority levels (scheduler_kernel_swp), else null
+  uint32_t nbuckets;
+  uint32_t nready;              // U0: initially ready units (queue[0, U0))
   uint64_t total_units;
   uint64_t chunk_elems;         // elements per unit (multiple of 8)
   uint64_t watchdog_ns;         // spin limit before declaring ERR_WATCHDOG

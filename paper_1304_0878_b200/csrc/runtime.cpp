@@ -779,14 +779,22 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     rt->sl.defer = stream_defer();
   }
   bool sub = rt->sl.active;
-  // device layout: ctr | items | pending | succ | factors | unit_base[N] (traced) | queue[U] | chunk_done[N] | trace
+  // priority ready queue (device_abi.h Bucket): DAG epochs on
+  // the "sw" bodies order ready work by upward rank
+  static const int prio_levels = getenv("BT_PRIO_LEVELS") ? std::max(1, std::min(kMaxBuckets, atoi(getenv("BT_PRIO_LEVELS"))))
+                                                          : kMaxBuckets;
+  const int NB = E > 0 && (kernel == 0 || kernel == 3) && !sub && !traced && (rt->cfg.flags & BT_FLAG_PRIORITY)
+                     ? prio_levels : 0;
+  // device layout: ctr | items | pending | succ | factors | unit_base[N] (traced) | buckets[NB] | queue[U] |
+  // chunk_done[N] | trace
   const size_t o_ctr = 0;
   const size_t o_items = 64;
   const size_t o_pend = align_up(o_items + 48 * N, 16);
   const size_t o_succ = align_up(o_pend + 4 * N, 16);
   const size_t o_fac = align_up(o_succ + 4 * E, 16);
   const size_t o_ubase = align_up(o_fac + 4 * F, 16);
-  const size_t o_queue = align_up(o_ubase + (traced ? 4 * N : 0), 16);
+  const size_t o_bk = align_up(o_ubase + (traced ? 4 * N : 0), 32);
+  const size_t o_queue = align_up(o_bk + sizeof(Bucket) * NB, 16);
   const size_t upload = o_queue + 8 * U0;
   const size_t o_cdone = align_up(o_queue + 8 * U, 16);
   const size_t o_trace = align_up(o_cdone + 4 * N, 16);
@@ -912,6 +920,57 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     }
   }
 
+  // priority levels: upward rank = the item's bytes plus the largest rank of
+  // its successors (the longest remaining path, in HBM bytes; HEFT's rank_u on
+  // identical processors), computed in reverse item order
+  // (items are numbered in a topological order: every edge goes from a lower
+  // to a higher id, checked); uniform levels over [0, max rank]
+  int nb_used = 0;
+  if (NB > 0) {
+    bool topo = true;
+    std::vector<uint64_t> rank(N);
+    uint64_t maxr = 0;
+    for (size_t i = N; i-- > 0 && topo;) {
+      const DItem &it = di[i];
+      const uint32_t kd = it.kind & K_MASK;
+      uint64_t best = 0;
+      for (uint32_t j = 0; j < it.nsucc; ++j) {
+        const uint32_t sj = it.nsucc == 1 ? it.succ_off : succ[it.succ_off + j];
+        if (sj <= i || sj >= N) {
+          topo = false;
+          break;
+        }
+        best = std::max(best, rank[sj]);
+      }
+      rank[i] = best + it.n * (kd == K_AXPY ? 12u : 8u);
+      maxr = std::max(maxr, rank[i]);
+    }
+    if (topo) {
+      nb_used = NB;
+      Bucket *bkh = reinterpret_cast<Bucket *>(h + o_bk);
+      uint64_t tot[kMaxBuckets] = {}, rdy[kMaxBuckets] = {};
+      for (size_t i = 0; i < N; ++i) {
+        const uint32_t l = (uint32_t)std::min<uint64_t>(NB - 1, (unsigned __int128)rank[i] * NB / (maxr + 1));
+        di[i].kind |= l << K_BUCKET_SHIFT;
+        tot[l] += di[i].nchunks;
+        if (pend[i] == 0) rdy[l] += di[i].nchunks;
+      }
+      uint64_t rb = 0, pb = 0, cur[kMaxBuckets];
+      for (int l = 0; l < NB; ++l) {
+        bkh[l] = Bucket{0, rdy[l], (uint32_t)tot[l], (uint32_t)rdy[l], (uint32_t)rb, (uint32_t)pb};
+        cur[l] = rb;
+        rb += rdy[l];
+        pb += tot[l] - rdy[l];
+      }
+      for (size_t i = 0; i < N; ++i)   // the initially ready units, grouped by level
+        if (pend[i] == 0) {
+          const uint32_t l = (di[i].kind >> K_BUCKET_SHIFT) & 0xFFu;
+          for (uint32_t c = 0; c < di[i].nchunks; ++c) q[cur[l]++] = ((unsigned long long)i << 32) | c;
+        }
+    }
+  }
+  rt->stats.prio_epochs += nb_used > 0;
+
   char *d = e.dblob;
   const double tC = now_ms();
   if (!e.hctr) {
@@ -931,6 +990,9 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   a.trace = traced ? reinterpret_cast<unsigned long long *>(d + o_trace) : nullptr;
   a.trace_item = traced ? reinterpret_cast<uint32_t *>(d + o_trace + 32 * U) : nullptr;
   a.unit_base = traced ? reinterpret_cast<const uint32_t *>(d + o_ubase) : nullptr;
+  a.bk = nb_used ? reinterpret_cast<Bucket *>(d + o_bk) : nullptr;
+  a.nbuckets = (uint32_t)nb_used;
+  a.nready = (uint32_t)U0;
   a.total_units = U;
   a.chunk_elems = CE;
   a.watchdog_ns = kWatchdogNs;

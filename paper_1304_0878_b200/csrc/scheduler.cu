@@ -297,7 +297,25 @@ __device__ void axpy_range(const float *x, float *y, uint64_t n, float a, int ti
   const float *xv = x + head;
   float *yv = y + head;
   const uint64_t nv = (n - head) >> 3;
-  for (uint64_t i = tid; i < nv; i += C) {
+  uint64_t i = tid;
+  // two vectors of x and y per step: 128 bytes of loads in flight per thread
+  // (the accesses are asm volatile: the compiler does not overlap iterations);
+  // CTA-wide bodies only (the warp-wide "wq" bodies stay within 64 registers)
+  if constexpr (C >= 128)
+  for (; i + C < nv; i += 2 * C) {
+    float xr[2][8], yr[2][8];
+    ld8(xv + 8 * i, xr[0]);
+    ld8(xv + 8 * (i + C), xr[1]);
+    ld8(yv + 8 * i, yr[0]);
+    ld8(yv + 8 * (i + C), yr[1]);
+#pragma unroll
+    for (int v = 0; v < 2; ++v)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) yr[v][q] = axpy1(a, xr[v][q], yr[v][q]);
+    st8(yv + 8 * i, yr[0]);
+    st8(yv + 8 * (i + C), yr[1]);
+  }
+  for (; i < nv; i += C) {
     float xr[8], yr[8];
     ld8(xv + 8 * i, xr);
     ld8(yv + 8 * i, yr);
@@ -321,6 +339,19 @@ __device__ void copy_range(const float *x, float *y, uint64_t n, int tid) {
   float *yv = y + head;
   const uint64_t nv = (n - head) >> 3;
   uint64_t i = tid;
+  // four vectors per step: 128 bytes of loads in flight per thread (CTA-wide bodies)
+  if constexpr (C >= 128)
+  for (; i + 3 * C < nv; i += 4 * C) {
+    float a[8], b[8], c[8], d[8];
+    ld8(xv + 8 * i, a);
+    ld8(xv + 8 * (i + C), b);
+    ld8(xv + 8 * (i + 2 * C), c);
+    ld8(xv + 8 * (i + 3 * C), d);
+    st8(yv + 8 * i, a);
+    st8(yv + 8 * (i + C), b);
+    st8(yv + 8 * (i + 2 * C), c);
+    st8(yv + 8 * (i + 3 * C), d);
+  }
   for (; i + C < nv; i += 2 * C) {
     float a[8], b[8];
     ld8(xv + 8 * i, a);
@@ -496,10 +527,17 @@ __device__ __forceinline__ void release_unit(const EpochArgs &a, uint32_t item, 
       const uint32_t nc = i == 0 ? m.s0nc : ldro<NC>(&a.items[s].nchunks);
       if (nc == 1 && mailbox_put(mb, (unsigned long long)s << 32, i == 0 && m.s0stage, m.i0, m.i1, m.i2))
         continue;   // run it here
-      const unsigned long long pos = atomicAdd(&a.ctr->tail, (unsigned long long)nc);
+      unsigned long long *qd;
+      if (a.bk) {   // priority level of the successor (device_abi.h Bucket)
+        Bucket *bk = a.bk + ((skind >> K_BUCKET_SHIFT) & 0xFFu);
+        const unsigned long long pos = atomicAdd(&bk->tail, (unsigned long long)nc);
+        qd = a.queue + a.nready + __ldcg(&bk->pbase) + (pos - __ldcg(&bk->ready));
+      } else {
+        qd = a.queue + atomicAdd(&a.ctr->tail, (unsigned long long)nc);
+      }
       fence_acq_rel_gpu();   // one release fence covers the nc relaxed publications
 #pragma unroll 1
-      for (uint32_t c = 0; c < nc; ++c) st_relaxed_u64(&a.queue[pos + c], ((unsigned long long)s << 32) | c);
+      for (uint32_t c = 0; c < nc; ++c) st_relaxed_u64(qd + c, ((unsigned long long)s << 32) | c);
     }
   }
   atomicAdd(&a.ctr->done, 1ull);
@@ -1270,6 +1308,113 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_sw(Epoch
   report_exit(a);
 }
 
+// "swp": "sw" with the priority ready queue (device_abi.h Bucket; SURVEY
+// NEXT-3): lane 0 of the scheduler warp holds at most one ticket per level,
+// takes a ticket on a level only while it has unclaimed units, and pops the
+// most urgent published one; a CTA leaves when every level is exhausted for it.
+template <bool PF>
+__global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_swp(EpochArgs a) {
+  constexpr int kCompute = kComputeSW;
+  __shared__ unsigned long long s_unit[2];
+  __shared__ DItem s_item[2];
+  __shared__ __align__(8) uint64_t s_empty[2];
+  __shared__ __align__(16) float s_fac[2][kMaxFactors];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = (int)a.nbuckets;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_empty[0], kCompute / 32);
+    mbar_init(&s_empty[1], kCompute / 32);
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // warp-cooperative pop: lane l < nb serves level l (its ticket, its
+    // exhaustion); lane 0 releases (slots, as in "sw")
+    SlotState st[2];
+    for (int b = 0; b < 2; ++b) {
+      st[b].unit = kStop;
+      st[b].parity = 0;
+      st[b].unreleased = false;
+    }
+    const bool mine = lane < nb;
+    Bucket *const bk = a.bk + (mine ? lane : 0);
+    const uint32_t l_total = mine ? __ldcg(&bk->total) : 0, l_ready = mine ? __ldcg(&bk->ready) : 0;
+    const uint32_t l_rbase = mine ? __ldcg(&bk->rbase) : 0, l_pbase = mine ? __ldcg(&bk->pbase) : 0;
+    unsigned long long held = ~0ull;   // this lane's ticket on its level
+    bool exhausted = !mine;
+    for (unsigned u = 0;; ++u) {
+      const int b = u & 1;
+      if (lane == 0) drain_slot(a, st[b], &s_empty[b]);   // slot b's previous unit (u-2)
+      __syncwarp();
+      unsigned long long unit = kStop;
+      const uint64_t start = globaltimer();
+      for (unsigned spin = 0;; ++spin) {
+        // 1) a ticket on each level with unclaimed units (no wait on a drained level)
+        if (held == ~0ull && !exhausted &&
+            ld_relaxed_u64(&bk->tail) > ld_relaxed_u64(&bk->head)) {
+          const unsigned long long t = atomicAdd(&bk->head, 1ull);
+          if (t >= l_total) exhausted = true;
+          else held = t;
+        }
+        // 2) the most urgent level whose held ticket is published
+        unsigned long long *q = nullptr, v = Q_EMPTY;
+        if (held != ~0ull) {
+          q = held < l_ready ? a.queue + l_rbase + held : a.queue + a.nready + l_pbase + (held - l_ready);
+          v = ld_relaxed_u64(q);
+        }
+        const unsigned pubm = __ballot_sync(0xffffffffu, v != Q_EMPTY);
+        if (pubm) {
+          const int top = 31 - __clz((int)pubm);
+          if (lane == top) {
+            v = ld_acquire_u64(q);   // slots are written once: same value, now acquired
+            held = ~0ull;
+          }
+          unit = __shfl_sync(0xffffffffu, v, top);
+          break;
+        }
+        // 3) leave: every level exhausted with nothing held, or every unit done
+        //    (tickets taken past the last publication of a level stay unfilled)
+        if (__all_sync(0xffffffffu, exhausted && held == ~0ull)) break;
+        int stop = 0;
+        if (lane == 0) {
+          if ((spin & 15) == 15 && ld_relaxed_u64(&a.ctr->done) == a.total_units) stop = 1;
+          poll_slot(a, st[b ^ 1], &s_empty[b ^ 1]);
+          if ((spin & 63) == 63) {
+            if (ld_relaxed_u32(&a.ctr->abort)) stop = 1;
+            else if (globaltimer() - start > a.watchdog_ns) {
+              raise_error(a, ERR_WATCHDOG);
+              stop = 1;
+            }
+          }
+        }
+        if (__shfl_sync(0xffffffffu, stop, 0)) break;
+        __nanosleep(spin < 64 ? 32 : 256);
+      }
+      if (lane == 0) {
+        if (unit != kStop && (unit >> 32) >= a.nitems) {
+          raise_error(a, ERR_BAD_UNIT);
+          unit = kStop;
+        }
+        st[b].unit = unit;
+        st[b].unreleased = unit != kStop;
+      }
+      unit = __shfl_sync(0xffffffffu, unit, 0);
+      __syncwarp();   // memory order: the acquiring lane's load before the other lanes' descriptor loads
+      stage_unit(a, unit, &s_item[b], s_fac[b], lane);
+      if (lane == 0) s_unit[b] = unit;
+      __syncwarp();
+      bar_arrive(kBarFull + b, 32 + kCompute);
+      if (unit == kStop) {
+        if (lane == 0) drain_slot(a, st[b ^ 1], &s_empty[b ^ 1]);   // unit u-1 still in flight
+        break;
+      }
+    }
+  } else {
+    compute_loop<kCompute, kSlotsSW, PF>(a, nullptr, s_unit, s_item, s_fac, s_empty, lane);
+  }
+  report_exit(a);
+}
+
 // "sw" as a stream launch (StreamCtl, device_abi.h): the
 // pipelined rounds of one SCAL run are sub-epochs of this single launch, built
 // and published by the host while the kernel already runs the earlier ones.
@@ -1804,6 +1949,11 @@ cudaError_t launch_direct(const DirectArgs &args, unsigned grid_x, cudaStream_t 
 // kernel: 0 = sw, 1 = rw, 2 = wq, 3 = sw with prefetching SCAL bodies (short
 // chains); grid in CTAs of that kernel's block size.
 cudaError_t launch_epoch(const EpochArgs &args, int grid, cudaStream_t stream, int kernel) {
+  if (args.bk) {   // priority ready queue ("sw" bodies)
+    if (kernel == 3) scheduler_kernel_swp<true><<<grid, kBlock, 0, stream>>>(args);
+    else scheduler_kernel_swp<false><<<grid, kBlock, 0, stream>>>(args);
+    return cudaGetLastError();
+  }
   if (kernel == 2) scheduler_kernel_wq<<<grid, kBlockWQ, 0, stream>>>(args);
   else if (kernel == 1) scheduler_kernel_rw<<<grid, kBlock, 0, stream>>>(args);
   else if (kernel == 3) scheduler_kernel_sw<true><<<grid, kBlock, 0, stream>>>(args);
@@ -1823,6 +1973,10 @@ cudaError_t scheduler_occupancy(int *blocks_per_sm, int *block) {
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, scheduler_kernel_sw<false>, kBlock, 0);
   int c = 0;
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, scheduler_kernel_sw<true>, kBlock, 0);
+  if (c < b) b = c;
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, scheduler_kernel_swp<false>, kBlock, 0);
+  if (c < b) b = c;
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, scheduler_kernel_swp<true>, kBlock, 0);
   if (c < b) b = c;
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, scheduler_kernel_sws<false>, kBlock, 0);
   if (c < b) b = c;

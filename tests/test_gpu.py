@@ -225,6 +225,22 @@ def test_c2b_unpartitioned_chain(B):
     compare_program(p)
 
 
+@pytest.mark.parametrize("chunk_bytes", [0, 96, 4096])
+def test_priority_ready_queue(B, chunk_bytes):
+    """DAG epochs on the "sw" bodies use the upward-rank priority levels
+    (BT_FLAG_PRIORITY, scheduler_kernel_swp): bit-exact on
+    random programs and a reduced C3, with multi-chunk items; the default FIFO agrees."""
+    progs = [W.random_small_program(7100 + s, max_tasks=10, max_elems=2000) for s in range(30)]
+    progs.append(W.c3_random_dag(nbuf=12, nx=40000, ntasks=500, seed=99))
+    n_prio = 0
+    for p in progs:
+        st = compare_program(p, flags=KERNELS["sw"] | B.BT_FLAG_PRIORITY, chunk_bytes=chunk_bytes)
+        n_prio += st["prio_epochs"]
+        st2 = compare_program(p, flags=KERNELS["sw"], chunk_bytes=chunk_bytes)
+        assert st2["prio_epochs"] == 0
+    assert n_prio >= 15
+
+
 def test_c3_reduced(B):
     p = W.c3_random_dag(nbuf=64, nx=1 << 12, ntasks=10000)
     stats = compare_program(p, chunk_bytes=4096)
