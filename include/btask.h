@@ -282,6 +282,8 @@ typedef struct bt_stats {
   uint64_t stream_resumes;    /* stream launches that closed themselves (no publication for 50 ms, e.g.
                                  under a launch-serialising tool) and were finished by their resume launch */
   uint64_t prio_epochs;       /* epochs run with the priority ready queue (upward-rank levels) */
+  uint64_t h2d_data_bytes;    /* host-homed data uploaded (first reads; bt_data_release of an RW acquire) */
+  uint64_t d2h_data_bytes;    /* host-homed data written back (eager write-backs, dirty ranges) */
 } bt_stats;
 int bt_stats_get(bt_runtime *rt, bt_stats *out);
 int bt_stats_reset(bt_runtime *rt);

@@ -133,14 +133,16 @@ struct EpochBuf {
 
 // Host <-> device coherence of one host-homed registered vector (PAPER.md:
 // 97-99 "transferring data between main memory and GPUs as needed").
-//  * register uploads large vectors in chunks on a copy stream; an epoch
-//    waits only for the chunks its tasks touch, so the first tasks start
-//    while the rest is still in flight;
+//  * lazy upload ("W-first accesses skip upload"): nothing is
+//    copied at registration; the first epoch that READS a range uploads it
+//    (in 64 MiB pieces on a copy stream, each with an event the epoch waits
+//    for), while a range whose first access is write-only (a COPY
+//    destination) becomes valid on the device without any upload;
 //  * write-back: when an epoch writes a range of the vector for the first
 //    time since registration, that range is copied back to the host buffer
 //    right after the epoch (on a second copy stream), so unregister finds the
-//    host copy current.  A range written twice marks the vector dirty and
-//    unregister copies the whole vector back after everything else.
+//    host copy current.  A range written again is marked dirty; acquire /
+//    unregister copy back exactly the dirty ranges they need.
 struct UploadChunk {
   uint64_t lo, hi;            // device byte range
   cudaEvent_t ev;             // recorded after its H2D copy
@@ -169,13 +171,41 @@ struct RangeSet {
     }
     m.emplace(lo, hi);
   }
+  bool empty() const { return m.empty(); }
+  // the parts of [lo, hi) in the set, appended to out; removed from the set if take
+  void pieces(uint64_t lo, uint64_t hi, std::vector<std::pair<uint64_t, uint64_t>> &out, bool take) {
+    auto it = m.upper_bound(lo);
+    if (it != m.begin() && std::prev(it)->second > lo) --it;
+    while (it != m.end() && it->first < hi) {
+      const uint64_t rlo = it->first, rhi = it->second;
+      const uint64_t a = std::max(lo, rlo), b = std::min(hi, rhi);
+      out.emplace_back(a, b);
+      if (!take) {
+        ++it;
+        continue;
+      }
+      it = m.erase(it);
+      if (rlo < a) m.emplace(rlo, a);   // keys below `it`: the iterator stays valid
+      if (b < rhi) {                    // b == hi: the last overlapping range
+        m.emplace(b, rhi);
+        break;
+      }
+    }
+  }
+  void remove(uint64_t lo, uint64_t hi) {
+    std::vector<std::pair<uint64_t, uint64_t>> tmp;
+    pieces(lo, hi, tmp, true);
+  }
 };
 
 struct RootCache {
   uint64_t dlo = 0, dhi = 0;  // device byte range of the replica
-  std::vector<UploadChunk> uploads;
+  std::vector<UploadChunk> uploads;   // issued host -> device copies (events), until the next wait
+  RangeSet pending;           // device bytes whose replica is not valid yet: the host holds the data
+                              // (uploaded on the first read; a write-only first access skips it)
   RangeSet written;           // device byte ranges written by epochs
-  bool dirty = false;         // a write not covered by an eager write-back
+  RangeSet dirty;             // written again after their eager write-back: copied back at acquire/unregister
+  RangeSet ewrite;            // scratch: ranges the epoch being flushed writes
   bool wb = false;            // eager write-backs issued
 };
 
@@ -506,6 +536,88 @@ int retire(bt_runtime *rt, EpochBuf &e) {
     const uint32_t *ti = reinterpret_cast<const uint32_t *>(e.hblob + e.trace_off_h + 32 * e.units);
     rt->trace_item.assign(ti, ti + e.units);
   }
+  return 0;
+}
+
+// Upload device byte range [lo, hi) of host-homed root `root` from the
+// registered host buffer on the H2D copy stream, in pieces of at most
+// kUploadChunk, each with an event that epochs reading it wait for
+// (RootCache::uploads).
+int upload_range(bt_runtime *rt, uint32_t root, RootCache &c, uint64_t lo, uint64_t hi) {
+  const char *host = static_cast<const char *>(rt->slots[root].hptr);
+  for (uint64_t a = lo; a < hi; a += kUploadChunk) {
+    const uint64_t len = std::min<uint64_t>(kUploadChunk, hi - a);
+    CUDA_TRY(rt, cudaMemcpyAsync(reinterpret_cast<void *>(a), host + (a - c.dlo), len, cudaMemcpyHostToDevice, rt->h2d));
+    UploadChunk u{a, a + len, rt->get_event()};
+    CUDA_TRY(rt, cudaEventRecord(u.ev, rt->h2d));
+    c.uploads.push_back(u);
+    rt->stats.h2d_data_bytes += len;
+  }
+  return 0;
+}
+
+// Make device bytes [lo, hi) of a host-homed root valid: upload the parts still pending.
+int ensure_device(bt_runtime *rt, uint32_t root, RootCache &c, uint64_t lo, uint64_t hi) {
+  if (c.pending.empty()) return 0;
+  std::vector<std::pair<uint64_t, uint64_t>> ps;
+  c.pending.pieces(lo, hi, ps, true);
+  for (const auto &pc : ps)
+    if (int e = upload_range(rt, root, c, pc.first, pc.second)) return e;
+  return 0;
+}
+
+// Host <-> device coherence of the epoch about to launch (items in topological
+// order): every range an item reads is uploaded if still pending; a range whose
+// first access is a COPY destination (write-only) just stops being pending;
+// the ranges the epoch writes are collected per root (RootCache::ewrite) for
+// the write-back after it.
+int epoch_coherence(bt_runtime *rt) {
+  struct Ref {
+    uint64_t lo, hi;
+    uint32_t root;
+    RootCache *c;
+  };
+  std::vector<Ref> refs;
+  for (auto &kv : rt->caches) {
+    kv.second.ewrite.m.clear();
+    refs.push_back(Ref{kv.second.dlo, kv.second.dhi, kv.first, &kv.second});
+  }
+  std::sort(refs.begin(), refs.end(), [](const Ref &a, const Ref &b) { return a.lo < b.lo; });
+  auto find = [&](uint64_t a) -> Ref * {
+    auto it = std::upper_bound(refs.begin(), refs.end(), a, [](uint64_t v, const Ref &r) { return v < r.lo; });
+    if (it == refs.begin()) return nullptr;
+    --it;
+    return a < it->hi ? &*it : nullptr;
+  };
+  // ranges read while pending are collected (merged) and uploaded once, in
+  // large copies, before the epoch; a write-only first access removes its range
+  std::vector<RangeSet> load(refs.size());
+  std::vector<std::pair<uint64_t, uint64_t>> ps;
+  for (const HItem &it : rt->builder.items) {
+    const uint64_t bytes = 4 * it.n;
+    auto rd = [&](uint64_t a) {
+      Ref *r = find(a);
+      if (!r || r->c->pending.empty()) return;
+      ps.clear();
+      r->c->pending.pieces(a, a + bytes, ps, true);
+      for (const auto &pc : ps) load[r - refs.data()].add(pc.first, pc.second);
+    };
+    auto wr = [&](uint64_t a, bool reads) {
+      Ref *r = find(a);
+      if (!r) return;
+      if (reads) rd(a);
+      else if (!r->c->pending.empty()) r->c->pending.remove(a, a + bytes);   // write-only first: no upload (R7)
+      r->c->ewrite.add(a, a + bytes);
+    };
+    switch (it.kind) {
+      case K_SCAL: wr(it.x, true); break;
+      case K_AXPY: rd(it.x); wr(it.y, true); break;
+      default: rd(it.x); wr(it.y, it.x == it.y); break;   // COPY x -> x reads x
+    }
+  }
+  for (size_t i = 0; i < refs.size(); ++i)
+    for (const auto &rg : load[i].m)
+      if (int e = upload_range(rt, refs[i].root, *refs[i].c, rg.first, rg.second)) return e;
   return 0;
 }
 
@@ -1103,6 +1215,10 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
 
   const int grid = (int)std::min<uint64_t>((uint64_t)rt->grid_max, U);
 
+  // host-homed data: upload what this epoch reads first, skip write-only
+  // first accesses, collect what it writes
+  if (!rt->caches.empty())
+    if (int r = epoch_coherence(rt)) return r;
   // host-homed data this epoch touches must have arrived (chunked uploads)
   for (auto &kv2 : rt->caches) {
     RootCache &c = kv2.second;
@@ -1151,24 +1267,34 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   }
   CUDA_TRY(rt, cudaEventRecord(e.end, stream));
   // write-back of host-homed ranges written for the first time since registration
+  // (the parts written before are marked dirty instead: copied back at
+  // acquire / unregister, after everything that writes them)
   bool wb_waited = false;
   for (auto &kv2 : rt->caches) {
     RootCache &c = kv2.second;
-    const uint64_t lo = std::max(tot.wlo, c.dlo), hi = std::min(tot.whi, c.dhi);
-    if (lo >= hi) continue;
-    const bool again = c.written.overlaps(lo, hi);
-    c.written.add(lo, hi);
-    if (again || c.dirty) {
-      c.dirty = true;
-      continue;
+    for (const auto &w : c.ewrite.m) {
+      std::vector<std::pair<uint64_t, uint64_t>> old;
+      c.written.pieces(w.first, w.second, old, false);
+      for (const auto &o : old) c.dirty.add(o.first, o.second);
+      uint64_t a = w.first;
+      old.emplace_back(w.second, w.second);
+      for (const auto &o : old) {   // the gaps between old pieces: first writes
+        if (a < o.first) {
+          if (!wb_waited) {
+            CUDA_TRY(rt, cudaStreamWaitEvent(rt->d2h, e.end, 0));
+            wb_waited = true;
+          }
+          char *host = static_cast<char *>(rt->slots[kv2.first].hptr) + (a - c.dlo);
+          CUDA_TRY(rt, cudaMemcpyAsync(host, reinterpret_cast<const void *>(a), o.first - a, cudaMemcpyDeviceToHost,
+                                       rt->d2h));
+          rt->stats.d2h_data_bytes += o.first - a;
+          c.wb = true;
+        }
+        a = std::max(a, o.second);
+      }
+      c.written.add(w.first, w.second);
     }
-    if (!wb_waited) {
-      CUDA_TRY(rt, cudaStreamWaitEvent(rt->d2h, e.end, 0));
-      wb_waited = true;
-    }
-    char *host = static_cast<char *>(rt->slots[kv2.first].hptr) + (lo - c.dlo);
-    CUDA_TRY(rt, cudaMemcpyAsync(host, reinterpret_cast<const void *>(lo), hi - lo, cudaMemcpyDeviceToHost, rt->d2h));
-    c.wb = true;
+    c.ewrite.m.clear();
   }
   if (traced) CUDA_TRY(rt, cudaMemcpyAsync(h + o_trace_h, d + o_trace, 36 * U, cudaMemcpyDeviceToHost, stream));
   CUDA_TRY(rt, cudaEventRecord(e.done, stream));
@@ -1462,14 +1588,6 @@ int bt_vector_data_register(bt_runtime *rt, bt_handle *out, int home_node, void 
         return fail(rt, -ENOMEM, "cannot allocate the device replica (%zu bytes)", nx * 4);
       }
       owns = true;
-      if (nx * 4 < kUploadChunk) {
-        e = cudaMemcpyAsync(dptr, ptr, nx * 4, cudaMemcpyHostToDevice, rt->stream);
-        if (e != cudaSuccess) {
-          if (rt->comm) cudaFree(dptr);
-          else cudaFreeAsync(dptr, rt->stream);
-          return cuda_fail(rt, e, "register upload");
-        }
-      }
     }
   }
   const uint32_t s = alloc_slots(rt, 1);
@@ -1489,25 +1607,16 @@ int bt_vector_data_register(bt_runtime *rt, bt_handle *out, int home_node, void 
     rt->ranges[lo] = {hi, s};
     rt->by_ptr[lo] = s;
   }
-  if (owns) {   // host-homed replica: coherence state, chunked upload of large vectors
+  if (owns) {   // host-homed replica: coherence state; the data stays on the host until first read
     RootCache &c = rt->caches[s];
     c = RootCache();
     c.dlo = reinterpret_cast<uint64_t>(dptr);
     c.dhi = c.dlo + nx * 4;
-    if (nx * 4 >= kUploadChunk) {
-      cudaEvent_t ev_alloc = rt->get_event();
-      CUDA_TRY(rt, cudaEventRecord(ev_alloc, rt->stream));        // after cudaMallocAsync
-      CUDA_TRY(rt, cudaStreamWaitEvent(rt->h2d, ev_alloc, 0));
-      rt->put_event(ev_alloc);
-      for (uint64_t off = 0; off < nx * 4; off += kUploadChunk) {
-        const uint64_t len = std::min<uint64_t>(kUploadChunk, nx * 4 - off);
-        CUDA_TRY(rt, cudaMemcpyAsync(reinterpret_cast<char *>(dptr) + off, static_cast<const char *>(ptr) + off, len,
-                                     cudaMemcpyHostToDevice, rt->h2d));
-        UploadChunk u{c.dlo + off, c.dlo + off + len, rt->get_event()};
-        CUDA_TRY(rt, cudaEventRecord(u.ev, rt->h2d));
-        c.uploads.push_back(u);
-      }
-    }
+    c.pending.add(c.dlo, c.dhi);
+    cudaEvent_t ev_alloc = rt->get_event();
+    CUDA_TRY(rt, cudaEventRecord(ev_alloc, rt->stream));        // uploads follow the (stream-ordered) allocation
+    CUDA_TRY(rt, cudaStreamWaitEvent(rt->h2d, ev_alloc, 0));
+    rt->put_event(ev_alloc);
   }
   ++rt->live_roots;
   *out = make_handle(rt, s);
@@ -1540,7 +1649,8 @@ int bt_data_partition(bt_runtime *rt, bt_handle h, uint32_t nparts) {
   uint32_t rounds = (uint32_t)rt->rounds_default;
   {
     auto it = rt->caches.find(p.root);
-    if (it != rt->caches.end() && !it->second.uploads.empty() && rounds > 1) rounds = (uint32_t)rt->nrounds;
+    if (it != rt->caches.end() && (!it->second.uploads.empty() || !it->second.pending.empty()) && rounds > 1)
+      rounds = (uint32_t)rt->nrounds;
   }
   for (uint32_t t = 0; t < nparts; ++t) {
     rt->key_dirty = true;
@@ -1704,6 +1814,14 @@ int cross_rank_read(bt_runtime *rt, uint32_t x, int peer, bool send) {
   float *const dptr = rt->hot[x].dptr;
   const uint64_t bytes = rt->hot[x].nx * 4;
   const uint64_t lo = reinterpret_cast<uint64_t>(dptr);
+  auto ci = rt->caches.find(root);
+  if (ci != rt->caches.end()) {
+    if (send) {   // the peer reads this range of our replica: valid on the device first
+      if (int r = ensure_device(rt, root, ci->second, lo, lo + bytes)) return r;
+    } else {      // overwritten by the copy (a non-owner's replica holds the last value received)
+      ci->second.pending.remove(lo, lo + bytes);
+    }
+  }
   if (int r = wait_uploads(rt, rt->stream, lo, lo + bytes)) return r;   // initial data in the replica
   std::string err;
   const int r = send ? rt->comm->send(rt->stream, peer, rt->slots[root].reg_key, rt->hot[root].dptr,
@@ -2297,9 +2415,13 @@ int sync_to_host(bt_runtime *rt, uint32_t root, uint64_t lo, uint64_t hi) {
   if (it == rt->caches.end()) return 0;
   RootCache &c = it->second;
   const bool touched = c.written.overlaps(lo, hi);
-  if (touched && c.dirty) {
-    char *host = static_cast<char *>(rt->slots[root].hptr) + (lo - c.dlo);
-    CUDA_TRY(rt, cudaMemcpyAsync(host, reinterpret_cast<const void *>(lo), hi - lo, cudaMemcpyDeviceToHost, rt->d2h));
+  std::vector<std::pair<uint64_t, uint64_t>> ps;
+  c.dirty.pieces(lo, hi, ps, true);   // written again since their eager write-back
+  for (const auto &pc : ps) {
+    char *host = static_cast<char *>(rt->slots[root].hptr) + (pc.first - c.dlo);
+    CUDA_TRY(rt, cudaMemcpyAsync(host, reinterpret_cast<const void *>(pc.first), pc.second - pc.first,
+                                 cudaMemcpyDeviceToHost, rt->d2h));
+    rt->stats.d2h_data_bytes += pc.second - pc.first;
   }
   if (touched || c.wb) CUDA_TRY(rt, cudaStreamSynchronize(rt->d2h));
   return 0;
@@ -2341,6 +2463,13 @@ int bt_data_release(bt_runtime *rt, bt_handle h) {
     cudaSetDevice(rt->device);
     CUDA_TRY(rt, cudaMemcpyAsync(sh.dptr, static_cast<float *>(root.hptr) + sl.offset, sh.nx * 4,
                                  cudaMemcpyHostToDevice, rt->stream));
+    rt->stats.h2d_data_bytes += sh.nx * 4;
+    auto it = rt->caches.find(sl.root);
+    if (it != rt->caches.end()) {
+      const uint64_t lo = reinterpret_cast<uint64_t>(sh.dptr);
+      it->second.pending.remove(lo, lo + sh.nx * 4);
+      it->second.dirty.remove(lo, lo + sh.nx * 4);   // the device copy now equals the host's
+    }
     // host writes under RW acquire: later tasks see them (stream order)
     CUDA_TRY(rt, cudaStreamSynchronize(rt->stream));
   }

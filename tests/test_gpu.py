@@ -691,6 +691,66 @@ def test_large_host_buffer_untouched_and_axpy(B):
     assert_bits_equal(b, (np.float32(0.5) * a0 + b0).astype(np.float32), "axpy")
 
 
+def test_write_first_copy_skips_upload(B):
+    """NEXT-4 (reading R7 "W": prior contents not read): a host
+    buffer whose first access is a COPY destination is never uploaded -- its
+    initial contents (here NaN garbage) cannot matter -- while a buffer read
+    first is uploaded once.  Bytes counted by bt_stats.h2d_data_bytes; the
+    results are the oracle's; unregister writes every result back."""
+    rng = np.random.default_rng(W.SEED_BASE + 96)
+    n = 1 << 20
+    x0 = W.unit_interval_floats(rng, n)
+    y0 = np.full(n, np.nan, np.float32)          # write-only first: never read
+    z0 = np.full(n, np.nan, np.float32)
+    rows = [(W.COPY, 0.0, 0, -1, 1, -1), (W.SCAL, np.float32(2.5), 1, -1, -1, -1),
+            (W.COPY, 0.0, 1, -1, 2, -1), (W.AXPY, np.float32(0.25), 0, -1, 2, -1)]
+    p = W.Program([x0, y0, z0], [0, 0, 0], W._tasks(len(rows)), name="W-first")
+    for i, r in enumerate(rows):
+        p.tasks[i] = r
+    exp = oracle.run(p)
+    bufs = p.copy_buffers()
+    with B.Runtime() as rt:
+        from paper_1304_0878_b200.programs import Session
+        sess = Session(rt, p, host_buffers=bufs)
+        sess.submit(batch=False)
+        rt.wait()
+        st = rt.stats()
+        sess.finish()
+    for b in range(3):
+        assert_bits_equal(bufs[b], exp[b], f"W-first buffer {b}")
+    assert st["h2d_data_bytes"] == 4 * n, st          # x only
+    assert st["d2h_data_bytes"] == 2 * 4 * n, st      # y and z written back, x untouched
+
+
+def test_partial_write_first_tiles(B):
+    """Per-range coherence: tiles 1 and 2 of a partitioned host buffer are COPY
+    destinations first (no upload), tiles 0 and 3 are scaled (uploaded); tile 2
+    is then written again (dirty: copied back at unregister)."""
+    rng = np.random.default_rng(W.SEED_BASE + 97)
+    nt, tile = 4, 1 << 18
+    x0 = W.unit_interval_floats(rng, nt * tile)
+    x0[tile:3 * tile] = np.nan
+    src = W.unit_interval_floats(rng, nt * tile)
+    rows = [(W.COPY, 0.0, 1, 1, 0, 1), (W.COPY, 0.0, 1, 2, 0, 2), (W.SCAL, np.float32(0.5), 0, 0, -1, -1),
+            (W.SCAL, np.float32(3.0), 0, 3, -1, -1), (W.SCAL, np.float32(1.5), 0, 2, -1, -1)]
+    p = W.Program([x0, src], [nt, nt], W._tasks(len(rows)), name="partial W-first")
+    for i, r in enumerate(rows):
+        p.tasks[i] = r
+    exp = oracle.run(p)
+    bufs = p.copy_buffers()
+    with B.Runtime() as rt:
+        from paper_1304_0878_b200.programs import Session
+        sess = Session(rt, p, host_buffers=bufs)
+        sess.submit(batch=False)
+        rt.wait()
+        st = rt.stats()
+        sess.finish()
+    for b in range(2):
+        assert_bits_equal(bufs[b], exp[b], f"partial W-first buffer {b}")
+    # x: tiles 0 and 3 uploaded; src: tiles 1 and 2 read
+    assert st["h2d_data_bytes"] == 4 * 4 * tile, st
+
+
 def test_stress_random_configurations(B):
     """Random programs under random runtime configurations (work-unit size,
     fusion, builder threads, pipelining thresholds, epoch auto-flush): every

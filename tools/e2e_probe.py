@@ -5,7 +5,7 @@ from paper_1304_0878_b200 import btask as B
 import workloads as W
 elems = 1 << 30; T = 16384
 f = W.sweep_factors(np.random.default_rng(1), 64)
-for threads in (16, 1):
+for threads in (14,):
     rt = B.Runtime(device=0, host_threads=threads)
     addr, host = B.pinned_empty(elems * 4)
     host[:] = 1.5
