@@ -16,6 +16,9 @@
 
 namespace bt {
 
+cudaError_t launch_flag_wait(const uint32_t *addr, uint32_t value, uint64_t watchdog_ns, cudaStream_t stream);
+cudaError_t launch_flag_write(uint32_t *addr, uint32_t value, cudaStream_t stream);
+
 namespace {
 
 constexpr int kMaxRanks = 16;
@@ -29,6 +32,7 @@ struct ShmExport {
   uint64_t key;                  // registration ordinal of the root
   uint64_t offset;               // bytes from the allocation base to the root
   uint64_t bytes;
+  uint64_t ptr;                  // the root's device address in the owner (same-process peers use it as is)
   cudaIpcMemHandle_t mem;        // handle of the allocation holding the root
 };
 
@@ -37,6 +41,9 @@ struct ShmRank {
   std::atomic<uint32_t> nexports;
   cudaIpcEventHandle_t ev_ready[kMaxRanks];
   cudaIpcEventHandle_t ev_done[kMaxRanks];
+  cudaIpcMemHandle_t flag_mem;   // the rank's flag page (device protocol)
+  uint64_t flag_ptr;             // ... its device address (same-process peers use it as is)
+  int32_t pid;                   // ranks in one process (threads, one runtime each) share addresses
   ShmExport exports[kMaxExports];
 };
 
@@ -85,7 +92,42 @@ int alloc_base(const void *p, uint64_t *base) {
   return 0;
 }
 
+// Stream memory operations through the runtime's driver entry points.
+// CUresult cuStreamWaitValue32(CUstream, CUdeviceptr, cuuint32_t, unsigned) (GEQ = 0);
+// CUresult cuStreamWriteValue32(CUstream, CUdeviceptr, cuuint32_t, unsigned) (0 = fence before the write).
+typedef int (*StreamValueFn)(cudaStream_t, unsigned long long, uint32_t, unsigned);
+StreamValueFn driver_fn(const char *name) {
+  if (getenv("BT_COMM_FLAG_KERNELS")) return nullptr;   // tests: the kernel fallback
+  void *sym = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &sym, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return reinterpret_cast<StreamValueFn>(sym);
+}
+
 }  // namespace
+
+int Comm::flag_wait(cudaStream_t stream, const uint32_t *addr, uint32_t value, std::string *err) {
+  static const StreamValueFn fn = driver_fn("cuStreamWaitValue32");
+  if (fn && fn(stream, reinterpret_cast<unsigned long long>(addr), value, 0u) == 0) return 0;
+  if (launch_flag_wait(addr, value, (uint64_t)(kTimeoutS * 1e9), stream) != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(err, -EIO, "cross-rank flag wait failed");
+  }
+  return 0;
+}
+
+int Comm::flag_write(cudaStream_t stream, uint32_t *addr, uint32_t value, std::string *err) {
+  static const StreamValueFn fn = driver_fn("cuStreamWriteValue32");
+  if (fn && fn(stream, reinterpret_cast<unsigned long long>(addr), value, 0u) == 0) return 0;
+  if (launch_flag_write(addr, value, stream) != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(err, -EIO, "cross-rank flag write failed");
+  }
+  return 0;
+}
 
 int Comm::create(const char *name, int rank, int nranks, int device, Comm **out, std::string *err) {
   *out = nullptr;
@@ -148,9 +190,18 @@ int Comm::create(const char *name, int rank, int nranks, int device, Comm **out,
       return set_err(err, -EINVAL, "ranks disagree on nranks (%s)", name);
     }
   }
-  // this rank's interprocess events, published for the peers
+  // this rank's interprocess events and flag page, published for the peers
   cudaSetDevice(device);
   ShmRank &me = c->seg_->ranks[rank];
+  c->dev_ = getenv("BT_COMM_HOST") == nullptr;
+  if (c->dev_) {
+    if (cudaMalloc((void **)&c->flags_, 256) != cudaSuccess || cudaMemset(c->flags_, 0, 256) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess || cudaIpcGetMemHandle(&me.flag_mem, c->flags_) != cudaSuccess) {
+      cudaGetLastError();
+      delete c;
+      return set_err(err, -EIO, "cannot create the cross-rank flag page");
+    }
+  }
   for (int p = 0; p < nranks; ++p) {
     if (p == rank) continue;
     if (cudaEventCreateWithFlags(&c->ev_ready_[p], cudaEventDisableTiming | cudaEventInterprocess) != cudaSuccess ||
@@ -162,6 +213,8 @@ int Comm::create(const char *name, int rank, int nranks, int device, Comm **out,
       return set_err(err, -EIO, "cannot create interprocess events");
     }
   }
+  me.flag_ptr = reinterpret_cast<uint64_t>(c->flags_);
+  me.pid = (int32_t)getpid();
   me.attached.store(1, std::memory_order_release);
   for (int p = 0; p < nranks; ++p)   // collective: every rank has published its events
     while (c->seg_->ranks[p].attached.load(std::memory_order_acquire) != 1) {
@@ -171,12 +224,31 @@ int Comm::create(const char *name, int rank, int nranks, int device, Comm **out,
       }
       std::this_thread::sleep_for(std::chrono::microseconds(100));
     }
+  if (c->dev_)
+    for (int p = 0; p < nranks; ++p) {
+      if (p == rank) continue;
+      void *fp = nullptr;
+      if (c->seg_->ranks[p].pid == (int32_t)getpid()) {   // a rank in this process: same address space
+        c->peer_flags_[p] = reinterpret_cast<uint32_t *>(c->seg_->ranks[p].flag_ptr);
+        c->peer_local_[p] = true;
+        continue;
+      }
+      if (cudaIpcOpenMemHandle(&fp, c->seg_->ranks[p].flag_mem, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        delete c;
+        return set_err(err, -EIO, "cannot map a peer's flag page");
+      }
+      c->peer_flags_[p] = static_cast<uint32_t *>(fp);
+    }
   *out = c;
   return 0;
 }
 
 Comm::~Comm() {
   for (auto &kv : alloc_opened_) cudaIpcCloseMemHandle(kv.second);
+  for (int p = 0; p < 16; ++p)
+    if (peer_flags_[p] && !peer_local_[p]) cudaIpcCloseMemHandle(peer_flags_[p]);
+  if (flags_) cudaFree(flags_);
   for (int p = 0; p < 16; ++p) {
     if (ev_ready_[p]) cudaEventDestroy(ev_ready_[p]);
     if (ev_done_[p]) cudaEventDestroy(ev_done_[p]);
@@ -227,6 +299,7 @@ int Comm::export_root(uint64_t key, const void *root, uint64_t bytes, std::strin
                    "register it after bt_comm_init, or pass cudaMalloc'ed device memory");
   }
   x.key = key;
+  x.ptr = reinterpret_cast<uint64_t>(root);
   x.offset = reinterpret_cast<uint64_t>(root) - base;
   x.bytes = bytes;
   x.valid.store(1, std::memory_order_release);
@@ -241,12 +314,29 @@ int Comm::open_root(int peer, uint64_t key, char **out, std::string *err) {
     *out = it->second;
     return 0;
   }
+  // device protocol: the owner exports a root the first time it sends it,
+  // possibly after we got here: wait for it (once per root and peer)
+  const double t0 = seconds();
+  for (;;) {
+    const ShmRank &pr = seg_->ranks[peer];
+    const uint32_t n = pr.nexports.load(std::memory_order_acquire);
+    bool found = false;
+    for (uint32_t i = 0; i < n && !found; ++i)
+      found = pr.exports[i].valid.load(std::memory_order_acquire) == 1 && pr.exports[i].key == key;
+    if (found || !dev_) break;
+    if (seconds() - t0 > kTimeoutS) return set_err(err, -ETIMEDOUT, "the owner rank never exported the buffer");
+    std::this_thread::yield();
+  }
   // the owner exported the root before it published the rendezvous we waited for
   const ShmRank &pr = seg_->ranks[peer];
   const uint32_t n = pr.nexports.load(std::memory_order_acquire);
   for (uint32_t i = 0; i < n; ++i) {
     const ShmExport &x = pr.exports[i];
     if (x.valid.load(std::memory_order_acquire) != 1 || x.key != key) continue;
+    if (pr.pid == (int32_t)getpid()) {   // a rank in this process: its address as is
+      *out = opened_[{peer, key}] = reinterpret_cast<char *>(x.ptr);
+      return 0;
+    }
     std::string hk(reinterpret_cast<const char *>(&x.mem), sizeof x.mem);
     char *base = nullptr;
     auto a = alloc_opened_.find({peer, hk});
@@ -269,6 +359,14 @@ int Comm::open_root(int peer, uint64_t key, char **out, std::string *err) {
 
 int Comm::send(cudaStream_t stream, int peer, uint64_t key, const void *root, uint64_t root_bytes, std::string *err) {
   if (int r = export_root(key, root, root_bytes, err)) return r;
+  if (dev_) {
+    const uint32_t k = (uint32_t)++sent_[peer];
+    if (int r = flag_write(stream, peer_flags_[peer] + rank_, k, err)) return r;        // peer's ready[me] = k
+#ifndef BT_COMM_MUTANT_NO_WAR   // test-sensitivity check only: drop the WAR ordering
+    if (int r = flag_wait(stream, flags_ + 16 + peer, k, err)) return r;                // my done[peer] >= k
+#endif
+    return 0;
+  }
   if (cudaEventRecord(ev_ready_[peer], stream) != cudaSuccess) return set_err(err, -EIO, "event record failed");
   seg_->ready[rank_][peer].fetch_add(1, std::memory_order_acq_rel);
   // WAR across ranks: later work here (a writer of the data) waits for the
@@ -287,6 +385,19 @@ int Comm::send(cudaStream_t stream, int peer, uint64_t key, const void *root, ui
 
 int Comm::recv(cudaStream_t stream, int peer, uint64_t key, uint64_t off, void *dst, uint64_t bytes,
                std::string *err) {
+  if (dev_) {
+    const uint32_t k = (uint32_t)++recvd_[peer];
+#ifndef BT_COMM_MUTANT_NO_RAW   // test-sensitivity check only: drop the RAW ordering
+    if (int r = flag_wait(stream, flags_ + peer, k, err)) return r;                     // my ready[peer] >= k
+#endif
+    char *src = nullptr;
+    if (int r = open_root(peer, key, &src, err)) return r;
+    if (bytes && cudaMemcpyAsync(dst, src + off, bytes, cudaMemcpyDeviceToDevice, stream) != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(err, -EIO, "peer copy failed");
+    }
+    return flag_write(stream, peer_flags_[peer] + 16 + rank_, k, err);                  // peer's done[me] = k
+  }
   const uint64_t want = ++recvd_[peer];
   if (int r = wait_seq(&seg_->ready[peer][rank_], want, "reader waits for the owner", err)) return r;
   cudaEvent_t ev;

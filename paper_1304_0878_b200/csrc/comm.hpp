@@ -15,11 +15,25 @@
 //             copy over NVLink between GPUs) into b's own replica of it;
 //             record DONE[b<-a]; signal a; the task then reads the replica.
 //
-// Host signalling goes through a POSIX shared-memory segment (sequence
-// counters per ordered rank pair, exported IPC handles); device ordering
-// through interprocess CUDA events.  No kernel ever waits for another rank:
-// only streams wait for events, so two ranks may also share one GPU (the
-// tests do).  Internal to libbtask.so.
+// Device protocol (default): no host waits at all.  Every rank owns a flag
+// page in device memory (ready[16], done[16]: per-peer sequence numbers),
+// mapped into every peer by CUDA IPC at bt_comm_init.  The k-th rendezvous of
+// the ordered pair (a, b) -- both sides count it alike, in submission order --
+// is, on the GPUs' streams:
+//   owner a:  WRITE b.ready[a] = k  (a stream memory write into b's page, after
+//             a's earlier work: a's writers of the data)
+//             WAIT  a.done[b] >= k  (a's later work, e.g. the next writer of the
+//             data, waits until b has copied it: WAR across ranks)
+//   reader b: WAIT  b.ready[a] >= k (RAW across ranks); copy the range from a's
+//             memory (IPC mapping; a peer copy over NVLink between GPUs);
+//             WRITE a.done[b] = k
+// Stream memory operations (cuStreamWaitValue32 / cuStreamWriteValue32, which
+// fence before the write) when the driver has them, else one-thread flag
+// kernels.  Host protocol (BT_COMM_HOST=1, the first implementation):
+// sequence counters in a POSIX shared-memory segment and interprocess events
+// (the owner's host waits until the reader has enqueued its copy).
+// Either way only streams wait, never a kernel for another rank's kernel, so
+// two ranks may also share one GPU (the tests do).  Internal to libbtask.so.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -47,6 +61,7 @@ class Comm {
   // dst, ordered on `stream`.
   int recv(cudaStream_t stream, int peer, uint64_t key, uint64_t off, void *dst, uint64_t bytes, std::string *err);
 
+  bool device_protocol() const { return dev_; }
   int rank() const { return rank_; }
   int nranks() const { return nranks_; }
 
@@ -67,6 +82,12 @@ class Comm {
   cudaEvent_t peer_ready_[16] = {};   // opened: peer p's READY[p->me]
   cudaEvent_t peer_done_[16] = {};    // opened: peer p's DONE[p<-me]
   uint64_t sent_[16] = {}, recvd_[16] = {};
+  bool dev_ = true;                   // device protocol (flag pages); false: host protocol
+  uint32_t *flags_ = nullptr;         // this rank's flag page: ready[16] | done[16]
+  uint32_t *peer_flags_[16] = {};     // the peers' pages, mapped here
+  bool peer_local_[16] = {};          // the peer is a rank of this process (no IPC mapping)
+  int flag_wait(cudaStream_t stream, const uint32_t *addr, uint32_t value, std::string *err);
+  int flag_write(cudaStream_t stream, uint32_t *addr, uint32_t value, std::string *err);
   std::map<uint64_t, int> exported_;                   // key -> export slot
   std::map<std::pair<int, uint64_t>, char *> opened_;  // (peer, key) -> root address here
   std::map<std::pair<int, std::string>, char *> alloc_opened_;   // (peer, IPC handle bytes) -> mapping

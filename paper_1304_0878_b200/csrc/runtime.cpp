@@ -1808,7 +1808,12 @@ int wait_uploads(bt_runtime *rt, cudaStream_t stream, uint64_t lo, uint64_t hi) 
 // Everything submitted earlier is flushed first, so the copy is ordered after
 // the owner's earlier writers and the reader's earlier readers of the replica.
 int cross_rank_read(bt_runtime *rt, uint32_t x, int peer, bool send) {
-  if (int r = flush_epoch(rt)) return r;
+  // the device protocol's stream operations are ordered after everything
+  // already enqueued: flush the pending epoch only if it touches x (owner: x's
+  // writers must precede the signal; reader: the replica's readers must
+  // precede the copy).  Later work follows in stream order either way.
+  if (!rt->comm->device_protocol() || rt->deps[x].epoch == rt->builder.epoch)
+    if (int r = flush_epoch(rt)) return r;
   const Slot &xs = rt->slots[x];
   const uint32_t root = xs.root;
   float *const dptr = rt->hot[x].dptr;

@@ -1691,6 +1691,32 @@ cudaError_t launch_gate(const volatile unsigned *flag_dev, uint64_t watchdog_ns,
   return cudaGetLastError();
 }
 
+// Cross-rank flags (comm.hpp, device protocol) when the driver has no stream
+// memory operations: one thread waits until *addr >= value (a peer's write
+// into this GPU's flag page), or writes *addr = value after a system-wide
+// fence (into a peer's page, after this stream's earlier work).
+__global__ void flag_wait_kernel(const uint32_t *addr, uint32_t value, uint64_t watchdog_ns) {
+  const uint64_t t0 = globaltimer();
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(addr) : "memory");
+    if ((int32_t)(v - value) >= 0 || globaltimer() - t0 > watchdog_ns) break;
+    __nanosleep(500);
+  }
+}
+__global__ void flag_write_kernel(uint32_t *addr, uint32_t value) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(addr), "r"(value) : "memory");
+}
+cudaError_t launch_flag_wait(const uint32_t *addr, uint32_t value, uint64_t watchdog_ns, cudaStream_t stream) {
+  flag_wait_kernel<<<1, 1, 0, stream>>>(addr, value, watchdog_ns);
+  return cudaGetLastError();
+}
+cudaError_t launch_flag_write(uint32_t *addr, uint32_t value, cudaStream_t stream) {
+  flag_write_kernel<<<1, 1, 0, stream>>>(addr, value);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // "wq": every warp is an independent worker (pop, body, release), for epochs of
 // small units (<= 16 KiB): a CTA-wide unit of 4 KiB leaves most threads idle

@@ -855,6 +855,27 @@ def test_cross_rank_reads_random_programs(B, batch):
         _check_owned(p, results, owners)
 
 
+@pytest.mark.parametrize("protocol", ["host", "flag_kernels"])
+def test_cross_rank_other_protocols(B, protocol):
+    """The same random cross-rank programs with the host protocol (shared-memory
+    counters + interprocess events, BT_COMM_HOST=1) and with the device
+    protocol's one-thread flag kernels instead of stream memory operations."""
+    import os
+    from tests import xrank
+    var = {"host": "BT_COMM_HOST", "flag_kernels": "BT_COMM_FLAG_KERNELS"}[protocol]
+    os.environ[var] = "1"
+    try:
+        for seed in range(3):
+            p = W.random_small_program(3100 + seed, max_tasks=12, max_elems=4096)
+            results, stats, owners = xrank.run(p, nranks=2, seed=seed)
+            _check_owned(p, results, owners)
+        p = _gated_program()
+        results, stats, owners = xrank.run(p, nranks=2, owners=[0, 1], gate=(0, 0.3), batch=False)
+        _check_owned(p, results, owners)
+    finally:
+        del os.environ[var]
+
+
 def test_cross_rank_c3_dag_and_sharded_sweeps(B):
     """C3-shaped random DAG (AXPY/COPY across owners -> many rendezvous) and a
     C5-shaped owner-computes sweep (tile halves per rank; each rank's local
