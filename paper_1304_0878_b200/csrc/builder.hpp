@@ -102,6 +102,12 @@ struct RunRec {
   uint32_t len;
 };
 
+// A handle's run in a direct round (Builder::lane_count): its tasks' factors
+// are fpool[start, start + m), split into `items` chained items.
+struct RunH {
+  uint32_t slot, start, m, items;
+};
+
 struct alignas(64) Lane {
   vec<LaneEntry> gather;              // the lane's entries of one round, gathered from the runs
   vec<uint32_t> gtask;                // their task indices (record_tasks only)
@@ -114,6 +120,12 @@ struct alignas(64) Lane {
   std::vector<uint32_t> relocated;    // global items whose factors moved to fpool
   std::vector<uint64_t> recorded;     // (task << 32) | tagged item (record_tasks)
   uint64_t fused = 0;
+  // direct rounds (lane_count / lane_write): the lane's handle runs, its
+  // totals, and its bases in the epoch's arrays
+  vec<RunH> hr;
+  vec<uint8_t> reuse;                 // per item with > 1 factor: 1 = same list as the lane's previous one
+  uint64_t d_items = 0, d_elems = 0, d_work = 0, d_fac = 0;
+  uint64_t ibase = 0, fbase = 0;
   char pad_[64];                      // keep neighbouring lanes off this cache line
   void clear() {
     items.clear();
@@ -238,6 +250,21 @@ class Builder {
   void merge(std::vector<Lane> &lanes, size_t nlanes, DepState *deps, Par &&par, int nworkers);
 
   const float *factors(const HItem &it) const { return &fpool[it.fofs]; }
+
+  // ---- direct rounds ---------------------------------------------------
+  // A round of a pipelined SCAL run is its own epoch, flushed right after it
+  // is built: every handle's tasks form one chain that starts ready (the
+  // earlier epochs precede it in stream order) and no two handles interact.
+  // Such a round skips the item / edge / merge / pack pipeline: lane_count
+  // sorts the lane's tasks by handle (stable) and counts items, elements and
+  // distinct factor lists; the runtime lays the epoch out from the lanes'
+  // totals; lane_write then writes the device descriptors themselves (item
+  // ids = the lane's base + position; a chain's successor is the next id,
+  // stored inline).  Same items, same factor order as lane_runs would build.
+  template <class Loc, class SlotOf, class Geom>
+  void lane_count(Lane &L, uint32_t nlocal, Loc &&loc, SlotOf &&slot_of, Geom &&geom);
+  template <class Geom, class Item>
+  void lane_write(Lane &L, uint64_t chunk_elems, float *fac, int32_t *pend, Geom &&geom, Item &&item);
 
  private:
   void fresh(DepState &st) {
@@ -487,6 +514,92 @@ void Builder::lane_runs(Lane &L, const LaneEntry *const *chunks, const uint32_t 
     st.ext = NONE;
     if (prev & TAG) L.touched.push_back(s);
     b = e_;
+  }
+}
+
+// ------------------------------------------------------- direct rounds --
+template <class Loc, class SlotOf, class Geom>
+void Builder::lane_count(Lane &L, uint32_t nlocal, Loc &&loc, SlotOf &&slot_of, Geom &&geom) {
+  L.hr.clear();
+  L.reuse.clear();
+  L.d_items = L.d_elems = L.d_work = L.d_fac = 0;
+  const size_t n = L.gather.size();
+  if (n == 0) return;
+  L.cnt.assign(nlocal + 1, 0);
+  uint32_t *cnt = L.cnt.data();
+  const LaneEntry *ge = L.gather.data();
+  for (size_t j = 0; j < n; ++j) ++cnt[loc(ge[j].slot) + 1];
+  for (uint32_t l = 1; l <= nlocal; ++l) cnt[l] += cnt[l - 1];
+  L.fpool.resize(n);
+  float *fs = L.fpool.data();
+  for (size_t j = 0; j < n; ++j) memcpy(fs + cnt[loc(ge[j].slot)]++, &ge[j].fbits, 4);
+  const uint32_t step = fusion ? max_fused : 1u;
+  const float *pf = nullptr;   // the lane's previous list of > 1 factors
+  uint32_t pk = 0;
+  uint32_t b = 0;
+  for (uint32_t l = 0; l < nlocal; ++l) {
+    const uint32_t e = cnt[l];
+    if (e == b) continue;
+    const uint32_t m = e - b, s = slot_of(l);
+    const uint32_t items = (m + step - 1) / step;
+    L.hr.push_back(RunH{s, b, m, items});
+    const uint64_t nx = geom(s).second;
+    L.d_items += items;
+    L.d_elems += (uint64_t)items * nx;
+    L.d_work += (uint64_t)m * nx;
+    for (uint32_t q = 0; q < items && step > 1; ++q) {
+      const uint32_t take = std::min(step, m - q * step);
+      if (take == 1) continue;
+      const float *f = fs + b + q * step;
+      const bool same = pf && pk == take && memcmp(pf, f, 4ull * take) == 0;
+      L.reuse.push_back(same ? 1 : 0);
+      if (!same) {
+        L.d_fac += take;
+        pf = f;
+        pk = take;
+      }
+    }
+    b = e;
+  }
+}
+
+// item(id) -> DItem& of the epoch; ids are L.ibase + position; factor lists
+// go to fac[L.fbase ...]; pend[id] = unfinished predecessors.
+template <class Geom, class Item>
+void Builder::lane_write(Lane &L, uint64_t chunk_elems, float *fac, int32_t *pend, Geom &&geom, Item &&item) {
+  const uint32_t step = fusion ? max_fused : 1u;
+  const float *fs = L.fpool.data();
+  uint32_t id = (uint32_t)L.ibase;
+  uint32_t fo = (uint32_t)L.fbase, pfo = 0;
+  size_t ri = 0;
+  for (const RunH &h : L.hr) {
+    const auto g = geom(h.slot);
+    const uint32_t nc = (uint32_t)((g.second + chunk_elems - 1) / chunk_elems);
+    for (uint32_t q = 0; q < h.items; ++q, ++id) {
+      const uint32_t take = std::min(step, h.m - q * step);
+      const float *f = fs + h.start + q * step;
+      auto &d = item(id);
+      d.x = g.first;
+      d.y = 0;
+      d.n = g.second;
+      d.kind = 1u | (q ? (1u << 8) : 0u);   // K_SCAL | K_SINGLE_PRED (device_abi.h)
+      d.k = take;
+      if (take == 1) {
+        memcpy(&d.arg, f, 4);
+      } else {
+        if (!L.reuse[ri++]) {
+          memcpy(fac + fo, f, 4ull * take);
+          pfo = fo;
+          fo += take;
+        }
+        d.arg = pfo;
+      }
+      d.nchunks = nc;
+      const bool more = q + 1 < h.items;
+      d.succ_off = more ? id + 1 : 0u;   // single successor inline
+      d.nsucc = more ? 1u : 0u;
+      pend[id] = q ? 1 : 0;
+    }
   }
 }
 

@@ -745,9 +745,17 @@ uint32_t round_of(uint64_t t, uint64_t n, uint32_t rounds, int geo) {
   return (uint32_t)(t * rounds / n);
 }
 
-int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
+// A round of a pipelined SCAL run built by Builder::lane_count (direct
+// rounds, builder.hpp): the lanes' handle runs in item order and the totals.
+struct DirectRound {
+  Lane *const *lanes;
+  size_t nlanes;
+  uint64_t N, E, F, elems, work, tasks;
+};
+
+int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound *dr = nullptr) {
   Builder &B = rt->builder;
-  if (B.items.empty()) {
+  if (dr ? dr->N == 0 : B.items.empty()) {
     B.next_epoch();
     return 0;
   }
@@ -772,19 +780,28 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
          (unsigned long long)e.seq, (int)e.inflight);
   if (int r = retire(rt, e)) return r;
 
-  const size_t N = B.items.size();
-  const size_t E = B.edges.size();
-  const bool big = N >= kParallelPack && rt->pool->size() > 1;
+  const size_t N = dr ? dr->N : B.items.size();
+  const size_t E = dr ? dr->E : B.edges.size();
+  const bool big = !dr && N >= kParallelPack && rt->pool->size() > 1;
   const int P = big ? rt->pool->size() : 1;
 
-  // work-unit size from the epoch's total elements (sampled for huge epochs)
-  const size_t stride = std::max<size_t>(1, N / 4096);
-  uint64_t sampled = 0, cnt = 0, sampled_work = 0;
-  for (size_t i = 0; i < N; i += stride, ++cnt) {
-    sampled += B.items[i].n;
-    sampled_work += B.items[i].n * std::max<uint32_t>(1, B.items[i].kind == K_SCAL ? B.items[i].k : 1);
+  // work-unit size from the epoch's total elements (sampled for huge epochs;
+  // exact for a direct round)
+  uint64_t tot_elems = 0, tot_work = 0;
+  if (dr) {
+    tot_elems = dr->elems;
+    tot_work = dr->work;
+  } else {
+    const size_t stride = std::max<size_t>(1, N / 4096);
+    uint64_t sampled = 0, cnt = 0, sampled_work = 0;
+    for (size_t i = 0; i < N; i += stride, ++cnt) {
+      sampled += B.items[i].n;
+      sampled_work += B.items[i].n * std::max<uint32_t>(1, B.items[i].kind == K_SCAL ? B.items[i].k : 1);
+    }
+    tot_elems = sampled / cnt * N;
+    tot_work = sampled_work / cnt * N;
   }
-  uint64_t est = sampled / cnt * N;
+  uint64_t est = tot_elems;
   // a stream launch's sub-epoch: units sized for the whole run (the launch
   // has no per-round tail to balance), equal in every sub-epoch
   if ((rt->sl.want || rt->sl.active) && rt->sl.cur_tasks) est = est * rt->sl.run_tasks / rt->sl.cur_tasks;
@@ -838,8 +855,22 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     }
     acc[p] = a;
   };
-  if (big) rt->par(passA);
-  else passA(0);
+  if (dr) {   // a direct round: units from the lanes' handle runs (every chain starts ready)
+    RangeAcc a;
+    for (size_t i = 0; i < dr->nlanes; ++i)
+      for (const RunH &h : dr->lanes[i]->hr) {
+        const uint64_t nc = (rt->hot[h.slot].nx + CE - 1) / CE;
+        a.units += nc * h.items;
+        a.ready += nc;
+      }
+    a.succ = E;
+    a.fac = dr->F;
+    acc[0] = a;
+  } else if (big) {
+    rt->par(passA);
+  } else {
+    passA(0);
+  }
   const double tA = now_ms();
   std::vector<RangeAcc> base(P);
   RangeAcc tot;
@@ -861,9 +892,9 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   // scheduler variant ("Persistent scheduler kernels")
   static const char *kv = getenv("BT_KERNEL");   // "sw" / "rw" / "wq": experiments only
   // work per unit = elements x chained multiplies
-  const uint64_t avg_work = (sampled_work / cnt * N) / std::max<uint64_t>(1, U);
+  const uint64_t avg_work = tot_work / std::max<uint64_t>(1, U);
   // units of at most 16 KiB: one warp per unit ("wq", many units in flight)
-  const uint64_t avg_elems = (sampled / cnt * N) / std::max<uint64_t>(1, U);
+  const uint64_t avg_elems = tot_elems / std::max<uint64_t>(1, U);
   // ... when the epoch is wide: a narrow one (few initially ready units, e.g.
   // a 1-wide dependency chain) is latency-bound, and the CTA-wide "rw" kernel
   // runs chains in its slots with the shortest dependency latency
@@ -895,7 +926,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   // the "sw" bodies order ready work by upward rank
   static const int prio_levels = getenv("BT_PRIO_LEVELS") ? std::max(1, std::min(kMaxBuckets, atoi(getenv("BT_PRIO_LEVELS"))))
                                                           : kMaxBuckets;
-  const int NB = E > 0 && (kernel == 0 || kernel == 3) && !sub && !traced && (rt->cfg.flags & BT_FLAG_PRIORITY)
+  const int NB = !dr && E > 0 && (kernel == 0 || kernel == 3) && !sub && !traced && (rt->cfg.flags & BT_FLAG_PRIORITY)
                      ? prio_levels : 0;
   // device layout: ctr | items | pending | succ | factors | unit_base[N] (traced) | buckets[NB] | queue[U] |
   // chunk_done[N] | trace
@@ -1001,14 +1032,37 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
         for (uint64_t c = 0; c < nc; ++c) q[qi++] = ((unsigned long long)i << 32) | c;
     }
   };
-  if (big) rt->par(passB);
-  else passB(0);
+  if (dr) {
+    // direct round: the ready queue (every chain's first item, in item order),
+    // then the lanes write their descriptors in parallel
+    uint64_t qi = 0, id = 0;
+    for (size_t i = 0; i < dr->nlanes; ++i)
+      for (const RunH &h : dr->lanes[i]->hr) {
+        const uint64_t nc = (rt->hot[h.slot].nx + CE - 1) / CE;
+        for (uint64_t c = 0; c < nc; ++c) q[qi++] = (id << 32) | c;
+        id += h.items;
+      }
+    const SlotHot *hot = rt->hot.data();
+    rt->par([&](int l) {
+      for (size_t i = (size_t)l; i < dr->nlanes; i += (size_t)rt->pool->size())
+        B.lane_write(
+            *dr->lanes[i], CE, fac, pend,
+            [hot](uint32_t sl) { return std::pair<uint64_t, uint64_t>(reinterpret_cast<uint64_t>(hot[sl].dptr), hot[sl].nx); },
+            [di](uint32_t id2) -> DItem & { return di[id2]; });
+    });
+  } else if (big) {
+    rt->par(passB);
+  } else {
+    passB(0);
+  }
   const double tB = now_ms();
   // CSR scatter (successor order within a list: edge creation order when
   // sequential; any order is valid).  An item with a single successor holds
   // the successor's id itself in DItem::succ_off (one dependent load less on
   // the device's release path: chains).
-  if (big) {
+  if (dr) {
+    // chains only: every successor is stored inline (lane_write)
+  } else if (big) {
     uint32_t *cur = rt->succ_off.data();
     rt->par([&](int p) {
       size_t lo, hi;
@@ -1121,7 +1175,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
     rt->stats.units += U;
     rt->stats.epochs += 1;
     rt->stats.upload_bytes += upload;
-    rt->stats.fused_tasks += B.fused;
+    rt->stats.fused_tasks += dr ? dr->tasks - N : B.fused;
     B.next_epoch();
     rt->stats.host_build_ms += now_ms() - t0;
   };
@@ -1180,7 +1234,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr) {
   // a tiny epoch of independent items: one direct launch, no blob (DirectArgs)
   static const bool no_direct = getenv("BT_NO_DIRECT") != nullptr;   // comparisons
   uint64_t max_n = 0;
-  bool direct = E == 0 && N <= (size_t)kDirectItems && !traced && !no_direct &&
+  bool direct = !dr && E == 0 && N <= (size_t)kDirectItems && !traced && !no_direct &&
                 !(rt->cfg.flags & (BT_FLAG_KERNEL_SW | BT_FLAG_KERNEL_RW | BT_FLAG_KERNEL_WQ));
   // distinct factor lists (consecutive equal lists shared, as in pass B)
   uint64_t dfac = 0;
@@ -2230,12 +2284,79 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
     rt->sl.nsub = nsub;
     rt->sl.run_tasks = local;
   }
+  // direct rounds (Builder::lane_count / lane_write): pipelined rounds of
+  // device-resident data go from the sorted tasks straight to the device
+  // descriptors (no items, edges, merge or pack pass); BT_NO_DIRECT_ROUNDS=1
+  // builds them through lane_runs as before (comparisons)
+  static const bool no_direct_rounds = getenv("BT_NO_DIRECT_ROUNDS") != nullptr;
+  const bool direct_rounds = pipelined && !no_direct_rounds && rt->caches.empty() && !record &&
+                             !(rt->cfg.flags & BT_FLAG_TIMESTAMPS);
+  std::vector<Lane *> dlanes;
   for (int rr = 0; rr < launches; ++rr) {
     const int rlo = bound[rr], rhi = bound[rr + 1];
     size_t sz = 0;
     for (int r = rlo; r < rhi; ++r) sz += round_size[r];
     if (pipelined && sz == 0) continue;
     const double ta = now_ms();
+    if (direct_rounds) {
+      rt->par([&](int l) {
+        for (int r = rlo; r < rhi; ++r) {
+          const uint32_t g = (uint32_t)(r * P + l);
+          Lane &L = rt->lanes[(size_t)(r - rlo) * P + l];
+          size_t m = 0;
+          for (int c = 0; c < P; ++c) m += rt->run_tasks[(size_t)c * G + g];
+          L.gather.resize(m);
+          LaneEntry *ge = L.gather.data();
+          size_t qd = 0;
+          for (int c = 0; c < P; ++c)
+            for (const RunRec &run : rt->runs[(size_t)c * G + g]) {
+              const bt_handle *hh = h0 + i0 + run.start;
+              const float *ff = scalars + i0 + run.start;
+              for (uint32_t j = 0; j < run.len; ++j) {
+                ge[qd + j].slot = (uint32_t)(hh[j] & 0xFFFFFFFFull) - 1u;
+                memcpy(&ge[qd + j].fbits, &ff[j], 4);
+              }
+              qd += run.len;
+            }
+          B.lane_count(
+              L, nlocal, [bl = blk_local.data()](uint32_t s) { return bl[s >> 6] + (s & 63); },
+              [up = (uint32_t)P, ul = (uint32_t)l](uint32_t loc) { return ((loc >> 6) * up + ul) * 64 + (loc & 63); },
+              [hot](uint32_t s) {
+                return std::pair<uint64_t, uint64_t>(reinterpret_cast<uint64_t>(hot[s].dptr), hot[s].nx);
+              });
+        }
+      });
+      const double tb = now_ms();
+      // item order: round, then lane; each lane object's bases
+      dlanes.clear();
+      DirectRound dr{nullptr, 0, 0, 0, 0, 0, 0, 0};
+      for (int r = rlo; r < rhi; ++r)
+        for (int l = 0; l < P; ++l) {
+          Lane *L = &rt->lanes[(size_t)(r - rlo) * P + l];
+          if (L->hr.empty()) continue;
+          L->ibase = dr.N;
+          L->fbase = dr.F;
+          dr.N += L->d_items;
+          dr.E += L->d_items - L->hr.size();
+          dr.F += L->d_fac;
+          dr.elems += L->d_elems;
+          dr.work += L->d_work;
+          dr.tasks += L->gather.size();
+          dlanes.push_back(L);
+        }
+      dr.lanes = dlanes.data();
+      dr.nlanes = dlanes.size();
+      B.ntasks = tbase + n;   // the round's epoch accounts the run
+      rt->sl.cur_tasks = sz;
+      cudaStream_t st = rt->rstream[rr & 1];
+      const double tc = now_ms();
+      if (int e = flush_epoch(rt, st, &dr)) return e;
+      CUDA_TRY(rt, cudaEventRecord(rt->ev_round[rr & 1], st));
+      if (dbg) t_launch.push_back(now_ms() - tp0);
+      t_p2 += tb - ta;
+      t_flush += now_ms() - tc;
+      continue;
+    }
     rt->par([&](int l) {
       // this lane builds its groups of every round of the launch in one go
       for (int r = rlo; r < rhi; ++r) {
