@@ -37,6 +37,8 @@
 #include <utility>
 #include <vector>
 
+#include "device_abi.h"
+
 namespace bt {
 
 // std::allocator that default-initialises (no zero fill on resize): the
@@ -124,7 +126,7 @@ struct alignas(64) Lane {
   // totals, and its bases in the epoch's arrays
   vec<RunH> hr;
   vec<uint8_t> reuse;                 // per item with > 1 factor: 1 = same list as the lane's previous one
-  uint64_t d_items = 0, d_elems = 0, d_work = 0, d_fac = 0;
+  uint64_t d_items = 0, d_elems = 0, d_work = 0, d_fac = 0, d_tasks = 0;
   uint64_t ibase = 0, fbase = 0;
   char pad_[64];                      // keep neighbouring lanes off this cache line
   void clear() {
@@ -261,10 +263,10 @@ class Builder {
   // totals; lane_write then writes the device descriptors themselves (item
   // ids = the lane's base + position; a chain's successor is the next id,
   // stored inline).  Same items, same factor order as lane_runs would build.
-  template <class Loc, class SlotOf, class Geom>
-  void lane_count(Lane &L, uint32_t nlocal, Loc &&loc, SlotOf &&slot_of, Geom &&geom);
+  template <class Src, class Loc, class SlotOf, class Geom>
+  void lane_count(Lane &L, Src &&src, uint32_t nlocal, Loc &&loc, SlotOf &&slot_of, Geom &&geom);
   template <class Geom, class Item>
-  void lane_write(Lane &L, uint64_t chunk_elems, float *fac, int32_t *pend, Geom &&geom, Item &&item);
+  void lane_write(Lane &L, float *fac, Geom &&geom, Item &&item);
 
  private:
   void fresh(DepState &st) {
@@ -518,21 +520,24 @@ void Builder::lane_runs(Lane &L, const LaneEntry *const *chunks, const uint32_t 
 }
 
 // ------------------------------------------------------- direct rounds --
-template <class Loc, class SlotOf, class Geom>
-void Builder::lane_count(Lane &L, uint32_t nlocal, Loc &&loc, SlotOf &&slot_of, Geom &&geom) {
+template <class Src, class Loc, class SlotOf, class Geom>
+void Builder::lane_count(Lane &L, Src &&src, uint32_t nlocal, Loc &&loc, SlotOf &&slot_of, Geom &&geom) {
   L.hr.clear();
   L.reuse.clear();
   L.d_items = L.d_elems = L.d_work = L.d_fac = 0;
-  const size_t n = L.gather.size();
-  if (n == 0) return;
+  L.d_tasks = 0;
+  // src(visit): visit(slot, fbits) for each of the lane's tasks in stream
+  // order (twice: a counting pass, then the scatter of the factors)
   L.cnt.assign(nlocal + 1, 0);
   uint32_t *cnt = L.cnt.data();
-  const LaneEntry *ge = L.gather.data();
-  for (size_t j = 0; j < n; ++j) ++cnt[loc(ge[j].slot) + 1];
+  src([&](uint32_t s, uint32_t) { ++cnt[loc(s) + 1]; });
   for (uint32_t l = 1; l <= nlocal; ++l) cnt[l] += cnt[l - 1];
+  const size_t n = cnt[nlocal];
+  L.d_tasks = n;
+  if (n == 0) return;
   L.fpool.resize(n);
   float *fs = L.fpool.data();
-  for (size_t j = 0; j < n; ++j) memcpy(fs + cnt[loc(ge[j].slot)]++, &ge[j].fbits, 4);
+  src([&](uint32_t s, uint32_t fb) { memcpy(fs + cnt[loc(s)]++, &fb, 4); });
   const uint32_t step = fusion ? max_fused : 1u;
   const float *pf = nullptr;   // the lane's previous list of > 1 factors
   uint32_t pk = 0;
@@ -564,9 +569,9 @@ void Builder::lane_count(Lane &L, uint32_t nlocal, Loc &&loc, SlotOf &&slot_of, 
 }
 
 // item(id) -> DItem& of the epoch; ids are L.ibase + position; factor lists
-// go to fac[L.fbase ...]; pend[id] = unfinished predecessors.
+// go to fac[L.fbase ...].
 template <class Geom, class Item>
-void Builder::lane_write(Lane &L, uint64_t chunk_elems, float *fac, int32_t *pend, Geom &&geom, Item &&item) {
+void Builder::lane_write(Lane &L, float *fac, Geom &&geom, Item &&item) {
   const uint32_t step = fusion ? max_fused : 1u;
   const float *fs = L.fpool.data();
   uint32_t id = (uint32_t)L.ibase;
@@ -574,16 +579,15 @@ void Builder::lane_write(Lane &L, uint64_t chunk_elems, float *fac, int32_t *pen
   size_t ri = 0;
   for (const RunH &h : L.hr) {
     const auto g = geom(h.slot);
-    const uint32_t nc = (uint32_t)((g.second + chunk_elems - 1) / chunk_elems);
     for (uint32_t q = 0; q < h.items; ++q, ++id) {
       const uint32_t take = std::min(step, h.m - q * step);
       const float *f = fs + h.start + q * step;
+      const bool more = q + 1 < h.items;
       auto &d = item(id);
       d.x = g.first;
       d.y = 0;
-      d.n = g.second;
-      d.kind = 1u | (q ? (1u << 8) : 0u);   // K_SCAL | K_SINGLE_PRED (device_abi.h)
-      d.k = take;
+      d.n = (uint32_t)g.second;
+      d.meta = make_meta(K_SCAL, q > 0, take, more ? 1 : 0);
       if (take == 1) {
         memcpy(&d.arg, f, 4);
       } else {
@@ -594,11 +598,9 @@ void Builder::lane_write(Lane &L, uint64_t chunk_elems, float *fac, int32_t *pen
         }
         d.arg = pfo;
       }
-      d.nchunks = nc;
-      const bool more = q + 1 < h.items;
-      d.succ_off = more ? id + 1 : 0u;   // single successor inline
-      d.nsucc = more ? 1u : 0u;
-      pend[id] = q ? 1 : 0;
+      d.succ = more ? id + 1 : 0u;   // single successor inline
+      // (pend[id] is not written: a chain item has one predecessor
+      // (K_SINGLE_PRED), released without its counter)
     }
   }
 }

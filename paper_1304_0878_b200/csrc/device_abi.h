@@ -6,30 +6,51 @@
 
 namespace bt {
 
+#if defined(__CUDACC__)
+#define BT_HD __host__ __device__
+#else
+#define BT_HD
+#endif
+
 // Work-item kinds (equal to the public BT_CL_* codelet ids).
 enum : uint32_t { K_SCAL = 1, K_AXPY = 2, K_COPY = 3 };
-// DItem::kind bit: the item has exactly one predecessor, so the completion of
-// that predecessor makes it ready without touching its pending counter.
-constexpr uint32_t K_SINGLE_PRED = 1u << 8;
-constexpr uint32_t K_MASK = 0xFFu;
+
+// DItem::meta: kind (bits 0-3) | K_SINGLE_PRED (bit 4) | priority level
+// (bits 5-7, device_abi Bucket) | k (bits 8-18) | successor count (bits 19-31).
+constexpr uint32_t K_MASK = 0xFu;
+// the item has exactly one predecessor, so the completion of that
+// predecessor makes it ready without touching its pending counter
+constexpr uint32_t K_SINGLE_PRED = 1u << 4;
+constexpr uint32_t K_LEVEL_SHIFT = 5, K_LEVEL_MASK = 0x7u;
+constexpr uint32_t K_K_SHIFT = 8, K_K_MASK = 0x7FFu;            // chained factors, 1..2047
+constexpr uint32_t K_NSUCC_SHIFT = 19, K_NSUCC_ESC = 0x1FFFu;   // 8191: the count is succ[succ], the list follows
 
 // One work item of an epoch: a task, or a fused chain of SCAL tasks on the
-// same (sub)handle.  48 bytes, read-only during the kernel.
+// same (sub)handle.  32 bytes (two 16-byte words), read-only during the kernel:
+//   word 0: x, y            word 1: n, meta, arg, succ
+// Units per item = ceil(n / EpochArgs::chunk_elems) (computed, not stored).
 struct alignas(16) DItem {
   uint64_t x;         // device address of operand 0 (float*)
   uint64_t y;         // device address of operand 1 (AXPY/COPY), else 0
-  uint64_t n;         // elements of each operand
-  uint32_t kind;      // K_* | K_SINGLE_PRED
-  uint32_t k;         // SCAL: number of chained factors (>= 1); else 1
+  uint32_t n;         // elements of each operand (< 2^32: bt_vector_data_register)
+  uint32_t meta;      // see above
   uint32_t arg;       // SCAL: k == 1: float bits of the factor; k > 1: offset of
-                      // the k factors in EpochArgs::factors;
-                      // AXPY: float bits of a
-  uint32_t nchunks;   // work units of this item = ceil(n / chunk_elems)
-  uint32_t succ_off;  // successors: succ[succ_off .. succ_off + nsucc); with
-                      // nsucc == 1 the successor's item id itself
-  uint32_t nsucc;
+                      // the k factors in EpochArgs::factors; AXPY: float bits of a
+  uint32_t succ;      // one successor: its item id; more: offset of their ids in
+                      // EpochArgs::succ (escaped count: succ[succ] = count, ids after)
+  BT_HD uint32_t kind() const { return meta & K_MASK; }
+  BT_HD uint32_t k() const { return (meta >> K_K_SHIFT) & K_K_MASK; }
+  BT_HD uint32_t nsucc_field() const { return meta >> K_NSUCC_SHIFT; }
+  BT_HD bool single_pred() const { return (meta & K_SINGLE_PRED) != 0; }
 };
-static_assert(sizeof(DItem) == 48, "DItem layout");
+static_assert(sizeof(DItem) == 32, "DItem layout");
+BT_HD inline uint32_t make_meta(uint32_t kind, bool single_pred, uint32_t k, uint64_t nsucc) {
+  return kind | (single_pred ? K_SINGLE_PRED : 0u) | (k << K_K_SHIFT) |
+         ((uint32_t)(nsucc < K_NSUCC_ESC ? nsucc : K_NSUCC_ESC) << K_NSUCC_SHIFT);
+}
+BT_HD inline uint32_t units_of(uint32_t n, uint64_t chunk_elems) {
+  return (uint32_t)(((uint64_t)n + chunk_elems - 1) / chunk_elems);
+}
 
 // Epoch counters, in device memory, initialised by the host upload.
 struct alignas(64) Counters {
@@ -50,8 +71,8 @@ enum : uint32_t { ERR_NONE = 0, ERR_BAD_KIND = 1, ERR_WATCHDOG = 2, ERR_BAD_UNIT
 // ---- priority ready queue (PAPER.md:91-96 HEFT, 1005-1018) --
 // DAG epochs on the "sw" kernel order ready work by the item's upward rank
 // (bytes on the longest path from the item to the end of the epoch, the
-// item's own included): items are dealt to kMaxBuckets levels (DItem::kind
-// bits 16-23, higher = more urgent), and every level is a FIFO of its own.  A
+// item's own included): items are dealt to kMaxBuckets levels (DItem::meta
+// level bits, higher = more urgent), and every level is a FIFO of its own.  A
 // level's unit count is known on the host, so a level is a ticket queue like
 // the single FIFO: a CTA holds at most one ticket per level (taken only when
 // the level has unclaimed units, so no CTA waits on an empty level while others
@@ -60,8 +81,7 @@ enum : uint32_t { ERR_NONE = 0, ERR_BAD_KIND = 1, ERR_WATCHDOG = 2, ERR_BAD_UNIT
 // Level b's positions: t < ready -> queue[rbase + t] (initially ready units,
 // uploaded), else queue[U0 + pbase + t - ready] (published at release; the
 // region after the U0 initially ready units is EMPTY at launch).
-constexpr int kMaxBuckets = 8;
-constexpr uint32_t K_BUCKET_SHIFT = 16;
+constexpr int kMaxBuckets = 8;   // DItem::meta level bits
 struct alignas(16) Bucket {
   unsigned long long head;   // next ticket
   unsigned long long tail;   // positions reserved by releases (starts at ready)

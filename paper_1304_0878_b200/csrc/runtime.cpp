@@ -819,7 +819,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
   // Pass A (per range): units, initially ready units, successors, factors
   // (a SCAL item whose factor list equals the previous item's reuses it).
   struct RangeAcc {
-    uint64_t units = 0, ready = 0, succ = 0, fac = 0;
+    uint64_t units = 0, ready = 0, succ = 0, fac = 0, esc = 0;
     uint64_t wlo = ~0ull, whi = 0, alo = ~0ull, ahi = 0;   // written / all operand byte ranges
   };
   std::vector<RangeAcc> acc(P);
@@ -834,7 +834,8 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
       const uint64_t nc = (it.n + CE - 1) / CE;
       a.units += nc;
       if (it.npred == 0) a.ready += nc;
-      a.succ += it.nsucc;
+      a.succ += it.nsucc + (it.nsucc >= K_NSUCC_ESC ? 1u : 0u);   // an escaped count precedes its list
+      a.esc += it.nsucc >= K_NSUCC_ESC;
       const uint64_t bytes = 4 * it.n;
       const uint64_t w = it.kind == K_SCAL ? it.x : it.y;
       a.wlo = std::min(a.wlo, w);
@@ -879,6 +880,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
     tot.units += acc[p].units;
     tot.ready += acc[p].ready;
     tot.succ += acc[p].succ;
+    tot.esc += acc[p].esc;
     tot.fac += acc[p].fac;
     tot.wlo = std::min(tot.wlo, acc[p].wlo);
     tot.whi = std::max(tot.whi, acc[p].whi);
@@ -887,7 +889,8 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
   }
   const uint64_t U = tot.units, U0 = tot.ready, F = tot.fac;
   const bool traced = (rt->cfg.flags & BT_FLAG_TIMESTAMPS) != 0;
-  if (tot.succ != E) return fail(rt, -EIO, "internal: successor count mismatch");
+  if (tot.succ != E + tot.esc) return fail(rt, -EIO, "internal: successor count mismatch");
+  const uint64_t SL = tot.succ;   // successor-list words (edges + escaped counts)
 
   // scheduler variant ("Persistent scheduler kernels")
   static const char *kv = getenv("BT_KERNEL");   // "sw" / "rw" / "wq": experiments only
@@ -932,9 +935,9 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
   // chunk_done[N] | trace
   const size_t o_ctr = 0;
   const size_t o_items = 64;
-  const size_t o_pend = align_up(o_items + 48 * N, 16);
+  const size_t o_pend = align_up(o_items + sizeof(DItem) * N, 16);
   const size_t o_succ = align_up(o_pend + 4 * N, 16);
-  const size_t o_fac = align_up(o_succ + 4 * E, 16);
+  const size_t o_fac = align_up(o_succ + 4 * SL, 16);
   const size_t o_ubase = align_up(o_fac + 4 * F, 16);
   const size_t o_bk = align_up(o_ubase + (traced ? 4 * N : 0), 32);
   const size_t o_queue = align_up(o_bk + sizeof(Bucket) * NB, 16);
@@ -1002,9 +1005,8 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
       DItem &d = di[i];
       d.x = it.x;
       d.y = it.y;
-      d.n = it.n;
-      d.kind = it.kind | (it.npred == 1 ? K_SINGLE_PRED : 0u);
-      d.k = it.k;
+      d.n = (uint32_t)it.n;
+      d.meta = make_meta(it.kind, it.npred == 1, it.k, it.nsucc);
       if (it.kind == K_SCAL && it.k == 1) {
         memcpy(&d.arg, B.factors(it), 4);
       } else if (it.kind == K_SCAL) {
@@ -1018,13 +1020,15 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
         d.arg = it.arg;
       }
       const uint64_t nc = (it.n + CE - 1) / CE;
-      d.nchunks = (uint32_t)nc;
       if (ubase) {
         ubase[i] = (uint32_t)ub;
         ub += nc;
       }
-      d.succ_off = (uint32_t)so;
-      d.nsucc = it.nsucc;
+      d.succ = (uint32_t)so;
+      if (it.nsucc >= K_NSUCC_ESC) {   // the count in front of the list
+        succ[so] = it.nsucc;
+        ++so;
+      }
       rt->succ_off[i] = (uint32_t)so;
       so += it.nsucc;
       pend[i] = (int32_t)it.npred;
@@ -1046,7 +1050,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
     rt->par([&](int l) {
       for (size_t i = (size_t)l; i < dr->nlanes; i += (size_t)rt->pool->size())
         B.lane_write(
-            *dr->lanes[i], CE, fac, pend,
+            *dr->lanes[i], fac,
             [hot](uint32_t sl) { return std::pair<uint64_t, uint64_t>(reinterpret_cast<uint64_t>(hot[sl].dptr), hot[sl].nx); },
             [di](uint32_t id2) -> DItem & { return di[id2]; });
     });
@@ -1070,8 +1074,8 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
       for (size_t j = lo; j < hi; ++j) {
         const uint64_t ed = B.edges[j];
         const uint32_t src = (uint32_t)(ed >> 32);
-        if (di[src].nsucc == 1) {
-          di[src].succ_off = (uint32_t)ed;
+        if (di[src].nsucc_field() == 1) {
+          di[src].succ = (uint32_t)ed;
           continue;
         }
         const uint32_t pos = __atomic_fetch_add(&cur[src], 1u, __ATOMIC_RELAXED);
@@ -1081,7 +1085,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
   } else {
     for (uint64_t ed : B.edges) {
       const uint32_t src = (uint32_t)(ed >> 32);
-      if (di[src].nsucc == 1) di[src].succ_off = (uint32_t)ed;
+      if (di[src].nsucc_field() == 1) di[src].succ = (uint32_t)ed;
       else succ[rt->succ_off[src]++] = (uint32_t)ed;
     }
   }
@@ -1098,10 +1102,12 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
     uint64_t maxr = 0;
     for (size_t i = N; i-- > 0 && topo;) {
       const DItem &it = di[i];
-      const uint32_t kd = it.kind & K_MASK;
+      const uint32_t kd = it.kind();
       uint64_t best = 0;
-      for (uint32_t j = 0; j < it.nsucc; ++j) {
-        const uint32_t sj = it.nsucc == 1 ? it.succ_off : succ[it.succ_off + j];
+      const uint32_t f = it.nsucc_field();
+      const uint32_t ns = f == K_NSUCC_ESC ? succ[it.succ] : f, off = f == K_NSUCC_ESC ? it.succ + 1 : it.succ;
+      for (uint32_t j = 0; j < ns; ++j) {
+        const uint32_t sj = ns == 1 ? off : succ[off + j];
         if (sj <= i || sj >= N) {
           topo = false;
           break;
@@ -1117,9 +1123,10 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
       uint64_t tot[kMaxBuckets] = {}, rdy[kMaxBuckets] = {};
       for (size_t i = 0; i < N; ++i) {
         const uint32_t l = (uint32_t)std::min<uint64_t>(NB - 1, (unsigned __int128)rank[i] * NB / (maxr + 1));
-        di[i].kind |= l << K_BUCKET_SHIFT;
-        tot[l] += di[i].nchunks;
-        if (pend[i] == 0) rdy[l] += di[i].nchunks;
+        di[i].meta |= l << K_LEVEL_SHIFT;
+        const uint32_t nci = units_of(di[i].n, CE);
+        tot[l] += nci;
+        if (pend[i] == 0) rdy[l] += nci;
       }
       uint64_t rb = 0, pb = 0, cur[kMaxBuckets];
       for (int l = 0; l < NB; ++l) {
@@ -1130,8 +1137,9 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
       }
       for (size_t i = 0; i < N; ++i)   // the initially ready units, grouped by level
         if (pend[i] == 0) {
-          const uint32_t l = (di[i].kind >> K_BUCKET_SHIFT) & 0xFFu;
-          for (uint32_t c = 0; c < di[i].nchunks; ++c) q[cur[l]++] = ((unsigned long long)i << 32) | c;
+          const uint32_t l = (di[i].meta >> K_LEVEL_SHIFT) & K_LEVEL_MASK;
+          const uint32_t nci = units_of(di[i].n, CE);
+          for (uint32_t c = 0; c < nci; ++c) q[cur[l]++] = ((unsigned long long)i << 32) | c;
         }
     }
   }
@@ -1606,6 +1614,7 @@ int bt_vector_data_register(bt_runtime *rt, bt_handle *out, int home_node, void 
   if (!out) return fail(rt, -EINVAL, "null output handle");
   *out = 0;
   if (nx == 0 || elemsize != 4) return fail(rt, -EINVAL, "only float32 vectors (elemsize 4, nx > 0) are supported");
+  if (nx > 0xFFFFFFFFull) return fail(rt, -EINVAL, "at most 2^32 - 1 elements per vector (16 GiB)");
   if (home_node != 0 && home_node != 1) return fail(rt, -EINVAL, "home_node must be 0 (host) or 1 (device)");
   if (home_node == 1 && !ptr) return fail(rt, -EINVAL, "device-homed data needs a pointer");
   if (home_node == 1 && rt->host_only) return fail(rt, -ENODEV, "host-only runtime");
@@ -2303,23 +2312,17 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
         for (int r = rlo; r < rhi; ++r) {
           const uint32_t g = (uint32_t)(r * P + l);
           Lane &L = rt->lanes[(size_t)(r - rlo) * P + l];
-          size_t m = 0;
-          for (int c = 0; c < P; ++c) m += rt->run_tasks[(size_t)c * G + g];
-          L.gather.resize(m);
-          LaneEntry *ge = L.gather.data();
-          size_t qd = 0;
-          for (int c = 0; c < P; ++c)
-            for (const RunRec &run : rt->runs[(size_t)c * G + g]) {
-              const bt_handle *hh = h0 + i0 + run.start;
-              const float *ff = scalars + i0 + run.start;
-              for (uint32_t j = 0; j < run.len; ++j) {
-                ge[qd + j].slot = (uint32_t)(hh[j] & 0xFFFFFFFFull) - 1u;
-                memcpy(&ge[qd + j].fbits, &ff[j], 4);
+          // the lane's tasks, straight from the caller's arrays (the run records of phase 1)
+          auto src = [&](auto &&visit) {
+            for (int c = 0; c < P; ++c)
+              for (const RunRec &run : rt->runs[(size_t)c * G + g]) {
+                const bt_handle *hh = h0 + i0 + run.start;
+                const uint32_t *ff = reinterpret_cast<const uint32_t *>(scalars + i0 + run.start);
+                for (uint32_t j = 0; j < run.len; ++j) visit((uint32_t)(hh[j] & 0xFFFFFFFFull) - 1u, ff[j]);
               }
-              qd += run.len;
-            }
+          };
           B.lane_count(
-              L, nlocal, [bl = blk_local.data()](uint32_t s) { return bl[s >> 6] + (s & 63); },
+              L, src, nlocal, [bl = blk_local.data()](uint32_t s) { return bl[s >> 6] + (s & 63); },
               [up = (uint32_t)P, ul = (uint32_t)l](uint32_t loc) { return ((loc >> 6) * up + ul) * 64 + (loc & 63); },
               [hot](uint32_t s) {
                 return std::pair<uint64_t, uint64_t>(reinterpret_cast<uint64_t>(hot[s].dptr), hot[s].nx);
@@ -2341,7 +2344,7 @@ int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scal
           dr.F += L->d_fac;
           dr.elems += L->d_elems;
           dr.work += L->d_work;
-          dr.tasks += L->gather.size();
+          dr.tasks += L->d_tasks;
           dlanes.push_back(L);
         }
       dr.lanes = dlanes.data();

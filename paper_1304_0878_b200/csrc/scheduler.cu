@@ -439,19 +439,18 @@ __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_re
 struct Mailbox {
   unsigned long long *unit;
   unsigned *state;
-  uint4 *item;        // 3 x 16 bytes: the staged DItem
+  uint4 *item;        // 2 x 16 bytes: the staged DItem
   unsigned *staged;   // 1: *item holds the unit's descriptor
   uint64_t *bar;      // mbarrier (count 1): one phase per put, wakes a pop warp in try_wait
 };
 
 __device__ __forceinline__ bool mailbox_put(const Mailbox &mb, unsigned long long unit, bool stage = false,
-                                            uint4 i0 = uint4{}, uint4 i1 = uint4{}, uint4 i2 = uint4{}) {
+                                            uint4 i0 = uint4{}, uint4 i1 = uint4{}) {
   if (!mb.unit || atomicCAS(mb.state, 0u, 2u) != 0u) return false;
   *reinterpret_cast<volatile unsigned long long *>(mb.unit) = unit;
   if (stage) {
     mb.item[0] = i0;
     mb.item[1] = i1;
-    mb.item[2] = i2;
   }
   *reinterpret_cast<volatile unsigned *>(mb.staged) = stage ? 1u : 0u;
   __threadfence_block();
@@ -466,39 +465,56 @@ __device__ __forceinline__ bool mailbox_put(const Mailbox &mb, unsigned long lon
 // Release metadata of a unit: read-only descriptors, so the release warp
 // loads them while the unit is still being computed (off the critical path).
 struct RelMeta {
-  uint32_t nchunks, nsucc, off;
-  uint32_t s0, s0kind, s0nc;   // first successor (valid if nsucc > 0)
-  uint4 i0, i1, i2;            // its descriptor (DItem as 3 x 16 bytes)
-  bool s0stage;                // a continuation candidate that needs no factor list
+  uint32_t nchunks, nsucc, off;   // off: the successor list (or the single successor's id)
+  uint32_t s0, s0kind, s0nc;      // first successor (valid if nsucc > 0); s0kind = its meta
+  uint4 i0, i1;                   // its descriptor (DItem as 2 x 16 bytes)
+  bool s0stage;                   // a continuation candidate that needs no factor list
 };
+
+// Successors of an item: count and where the list starts (device_abi.h
+// DItem::succ; an escaped count is stored in front of the list).
+template <bool NC>
+__device__ __forceinline__ void succ_list(const EpochArgs &a, uint32_t field, uint32_t succ, uint32_t &n,
+                                          uint32_t &off) {
+  if (field == K_NSUCC_ESC) {
+    n = ldro<NC>(&a.succ[succ]);
+    off = succ + 1;
+  } else {
+    n = field;
+    off = succ;
+  }
+}
 // self: the item's descriptor already staged in shared memory, or null.
 template <bool NC = true>
 __device__ __forceinline__ RelMeta release_meta(const EpochArgs &a, uint32_t item, const DItem *self = nullptr) {
   RelMeta m;
+  uint32_t n, meta, succ;
   if (self) {
-    m.nchunks = self->nchunks;
-    m.nsucc = self->nsucc;
-    m.off = self->succ_off;
+    n = self->n;
+    meta = self->meta;
+    succ = self->succ;
   } else {
     const DItem &it = a.items[item];
-    m.nchunks = ldro<NC>(&it.nchunks);
-    m.nsucc = ldro<NC>(&it.nsucc);
-    m.off = ldro<NC>(&it.succ_off);
+    n = ldro<NC>(&it.n);
+    meta = ldro<NC>(&it.meta);
+    succ = ldro<NC>(&it.succ);
   }
+  m.nchunks = units_of(n, a.chunk_elems);
+  succ_list<NC>(a, meta >> K_NSUCC_SHIFT, succ, m.nsucc, m.off);
   m.s0 = m.s0kind = m.s0nc = 0;
   m.s0stage = false;
-  m.i0 = m.i1 = m.i2 = uint4{};
+  m.i0 = m.i1 = uint4{};
   if (m.nsucc) {
     m.s0 = m.nsucc == 1 ? m.off : ldro<NC>(&a.succ[m.off]);   // a single successor is stored inline
     const uint4 *src = reinterpret_cast<const uint4 *>(a.items + m.s0);
-    m.i0 = ldro<NC>(src);
-    m.i1 = ldro<NC>(src + 1);   // n (x, y), kind (z), k (w)
-    m.i2 = ldro<NC>(src + 2);   // arg (x), nchunks (y), succ_off (z), nsucc (w)
-    static_assert(offsetof(DItem, kind) == 24 && offsetof(DItem, k) == 28 && offsetof(DItem, nchunks) == 36,
+    m.i0 = ldro<NC>(src);       // x, y
+    m.i1 = ldro<NC>(src + 1);   // n (x), meta (y), arg (z), succ (w)
+    static_assert(offsetof(DItem, n) == 16 && offsetof(DItem, meta) == 20 && offsetof(DItem, arg) == 24,
                   "DItem layout");
-    m.s0kind = m.i1.z;
-    m.s0nc = m.i2.y;
-    m.s0stage = (m.s0kind & K_SINGLE_PRED) && m.s0nc == 1 && ((m.s0kind & K_MASK) != K_SCAL || m.i1.w == 1);
+    m.s0kind = m.i1.y;
+    m.s0nc = units_of(m.i1.x, a.chunk_elems);
+    m.s0stage = (m.s0kind & K_SINGLE_PRED) && m.s0nc == 1 &&
+                ((m.s0kind & K_MASK) != K_SCAL || ((m.s0kind >> K_K_SHIFT) & K_K_MASK) == 1);
   }
   return m;
 }
@@ -517,19 +533,21 @@ __device__ __forceinline__ void release_unit(const EpochArgs &a, uint32_t item, 
   }
   for (uint32_t i = 0; i < nsucc; ++i) {
     const uint32_t s = i == 0 ? m.s0 : ldro<NC>(&a.succ[off + i]);
-    const uint32_t skind = i == 0 ? m.s0kind : ldro<NC>(&a.items[s].kind);
+    const uint32_t skind = i == 0 ? m.s0kind : ldro<NC>(&a.items[s].meta);
     // a single-predecessor successor is ready now (no counter); with more
     // predecessors the acq_rel RMW both releases ours and acquires theirs
-    const bool ready = mb.unit && (skind & K_SINGLE_PRED)
+    // (the publication below is a release either way: fence.acq_rel, then the
+    // relaxed slot stores the consumer reads with ld.acquire)
+    const bool ready = (skind & K_SINGLE_PRED)
                            ? true
                            : atom_add_acq_rel(reinterpret_cast<unsigned *>(&a.pending[s]), 0xFFFFFFFFu) == 1u;
     if (ready) {
-      const uint32_t nc = i == 0 ? m.s0nc : ldro<NC>(&a.items[s].nchunks);
-      if (nc == 1 && mailbox_put(mb, (unsigned long long)s << 32, i == 0 && m.s0stage, m.i0, m.i1, m.i2))
+      const uint32_t nc = i == 0 ? m.s0nc : units_of(ldro<NC>(&a.items[s].n), a.chunk_elems);
+      if (nc == 1 && mailbox_put(mb, (unsigned long long)s << 32, i == 0 && m.s0stage, m.i0, m.i1))
         continue;   // run it here
       unsigned long long *qd;
       if (a.bk) {   // priority level of the successor (device_abi.h Bucket)
-        Bucket *bk = a.bk + ((skind >> K_BUCKET_SHIFT) & 0xFFu);
+        Bucket *bk = a.bk + ((skind >> K_LEVEL_SHIFT) & K_LEVEL_MASK);
         const unsigned long long pos = atomicAdd(&bk->tail, (unsigned long long)nc);
         qd = a.queue + a.nready + __ldcg(&bk->pbase) + (pos - __ldcg(&bk->ready));
       } else {
@@ -774,20 +792,21 @@ __device__ __forceinline__ void compute_loop(const EpochArgs &a0, const EpochArg
     const uint32_t chunk = (uint32_t)unit;
     const DItem it = s_item[b];                  // staged by the pop warp
     const uint64_t lo = (uint64_t)chunk * a.chunk_elems;
-    const uint64_t hi = min(it.n, lo + a.chunk_elems);
-    switch (it.kind & K_MASK) {
+    const uint64_t hi = min((uint64_t)it.n, lo + a.chunk_elems);
+    const uint32_t kk = it.k();
+    switch (it.kind()) {
       case K_SCAL:
 #if BT_BULK
         if (s_bulk) {
           float *xs = reinterpret_cast<float *>(it.x) + lo;
           const uint64_t n = hi - lo;
           const uint64_t head = head_elems(xs, n);
-          for (uint64_t i = tid; i < head; i += C) __stcg(xs + i, chain_scalar(__ldcg(xs + i), s_fac[b], it.k));
+          for (uint64_t i = tid; i < head; i += C) __stcg(xs + i, chain_scalar(__ldcg(xs + i), s_fac[b], kk));
           const uint64_t nv = (n - head) >> 3;
-          scal_bulk<C / 32>(xs + head, nv, s_fac[b], it.k, cw, lane, s_bulk + cw * 2 * kSB, s_bulk_bar + 2 * cw,
+          scal_bulk<C / 32>(xs + head, nv, s_fac[b], kk, cw, lane, s_bulk + cw * 2 * kSB, s_bulk_bar + 2 * cw,
                             bulk_ph);
           for (uint64_t t = head + 8 * nv + tid; t < n; t += C)
-            __stcg(xs + t, chain_scalar(__ldcg(xs + t), s_fac[b], it.k));
+            __stcg(xs + t, chain_scalar(__ldcg(xs + t), s_fac[b], kk));
           break;
         }
 #endif
@@ -796,9 +815,9 @@ __device__ __forceinline__ void compute_loop(const EpochArgs &a0, const EpochArg
         // wider step without prefetch is faster (C5 2.07 vs 2.08 ms).  One
         // body per kernel instance (both inlined would spill).
         if (PF)
-          scal_range_pf<2, C>(reinterpret_cast<float *>(it.x) + lo, hi - lo, s_fac[b], it.k, tid);
+          scal_range_pf<2, C>(reinterpret_cast<float *>(it.x) + lo, hi - lo, s_fac[b], kk, tid);
         else
-          scal_range<4, C>(reinterpret_cast<float *>(it.x) + lo, hi - lo, s_fac[b], it.k, tid);
+          scal_range<4, C>(reinterpret_cast<float *>(it.x) + lo, hi - lo, s_fac[b], kk, tid);
         break;
       case K_AXPY:
         axpy_range<C>(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, hi - lo,
@@ -856,22 +875,22 @@ __device__ __forceinline__ void compute_loop_rw(const EpochArgs &a, const unsign
     unsigned par = 0, extra = 0;
     for (;;) {
       // may this unit continue in the slot?  (uniform: every thread sees it)
-      const bool maybe = BT_INSLOT && !a.trace && it.nchunks == 1 && it.nsucc == 1;
+      const bool maybe = BT_INSLOT && !a.trace && units_of(it.n, a.chunk_elems) == 1 && it.nsucc_field() == 1;
       if (maybe && tid == 0) {   // the successor's descriptor, copied to shared memory under the body
         const unsigned dst = (unsigned)__cvta_generic_to_shared(&s_nitem[b][par]);
-        const DItem *src = a.items + it.succ_off;
+        const DItem *src = a.items + it.succ;
 #pragma unroll
-        for (int q = 0; q < 3; ++q)
+        for (int q = 0; q < 2; ++q)
           asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst + 16 * q), "l"(reinterpret_cast<const char *>(src) + 16 * q)
                        : "memory");
         asm volatile("cp.async.commit_group;" ::: "memory");
       }
       const uint32_t chunk = (uint32_t)unit;
       const uint64_t lo = (uint64_t)chunk * a.chunk_elems;
-      const uint64_t hi = min(it.n, lo + a.chunk_elems);
-      switch (it.kind & K_MASK) {
+      const uint64_t hi = min((uint64_t)it.n, lo + a.chunk_elems);
+      switch (it.kind()) {
         case K_SCAL:   // small units (the rw kernel's domain): 2 x 8 elements per thread and step
-          scal_range<2, C>(reinterpret_cast<float *>(it.x) + lo, hi - lo, fac, it.k, tid);
+          scal_range<2, C>(reinterpret_cast<float *>(it.x) + lo, hi - lo, fac, it.k(), tid);
           break;
         case K_AXPY:
           axpy_range<C>(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, hi - lo,
@@ -889,7 +908,7 @@ __device__ __forceinline__ void compute_loop_rw(const EpochArgs &a, const unsign
       if (tid == 0) {
         asm volatile("cp.async.wait_all;" ::: "memory");
         const DItem &n = s_nitem[b][par];
-        const unsigned go = (n.kind & K_SINGLE_PRED) && n.nchunks == 1 && ((n.kind & K_MASK) != K_SCAL || n.k == 1)
+        const unsigned go = n.single_pred() && units_of(n.n, a.chunk_elems) == 1 && (n.kind() != K_SCAL || n.k() == 1)
                                 ? 1u : 0u;
         if (go) s_nfac[b][par] = __uint_as_float(n.arg);   // a single factor travels in arg
         s_go[b][par] = go;
@@ -899,7 +918,7 @@ __device__ __forceinline__ void compute_loop_rw(const EpochArgs &a, const unsign
       // still read this step's while thread 0 fills the next
       bar_sync_n<kBarCompute>(C);
       if (!s_go[b][par]) break;
-      unit = (unsigned long long)it.succ_off << 32;   // nsucc == 1: succ_off is the successor's id
+      unit = (unsigned long long)it.succ << 32;   // one successor: succ is its id
       it = s_nitem[b][par];
       fac = &s_nfac[b][par];
       par ^= 1u;
@@ -951,9 +970,10 @@ __device__ __forceinline__ void stage_unit(const EpochArgs &a, unsigned long lon
                                            float *fac_dst, int lane) {
   if (unit == kStop) return;
   const DItem *it = a.items + (uint32_t)(unit >> 32);
-  if (lane < 3) reinterpret_cast<uint4 *>(item_dst)[lane] = ldro<NC>(reinterpret_cast<const uint4 *>(it) + lane);
-  if ((ldro<NC>(&it->kind) & K_MASK) == K_SCAL) {
-    const uint32_t k = ldro<NC>(&it->k), arg = ldro<NC>(&it->arg);
+  if (lane < 2) reinterpret_cast<uint4 *>(item_dst)[lane] = ldro<NC>(reinterpret_cast<const uint4 *>(it) + lane);
+  const uint32_t meta = ldro<NC>(&it->meta);
+  if ((meta & K_MASK) == K_SCAL) {
+    const uint32_t k = (meta >> K_K_SHIFT) & K_K_MASK, arg = ldro<NC>(&it->arg);
     if (k == 1) {   // a single factor travels inline in arg: no dependent load
       if (lane == 0) fac_dst[0] = __uint_as_float(arg);
     } else {
@@ -1004,7 +1024,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
   __shared__ unsigned s_popped, s_released, s_mb_state, s_mb_staged, s_mb_expect;
   __shared__ __align__(8) uint64_t s_mb_bar;
   __shared__ unsigned long long s_mb_unit;
-  __shared__ uint4 s_mb_item[3];
+  __shared__ uint4 s_mb_item[2];
   __shared__ unsigned long long s_g0[kSlots];
   __shared__ long long s_popc[kSlots], s_c1[kSlots];
 #if BT_TRACE_DETAIL
@@ -1051,7 +1071,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
             if (staged) {   // copy the descriptor out before the mailbox is reused
               const volatile uint4 *src = s_mb_item;
               uint4 *dst = reinterpret_cast<uint4 *>(&s_item[b]);
-              for (int q = 0; q < 3; ++q) {
+              for (int q = 0; q < 2; ++q) {
                 const uint4 w = {src[q].x, src[q].y, src[q].z, src[q].w};
                 dst[q] = w;
               }
@@ -1122,7 +1142,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
       __syncwarp();   // memory order: lane 0's ld.acquire of the unit before the other lanes' descriptor loads
       if (!staged) {
         stage_unit(a, unit, &s_item[b], s_fac[b], lane);
-      } else if (lane == 0 && (s_item[b].kind & K_MASK) == K_SCAL) {
+      } else if (lane == 0 && s_item[b].kind() == K_SCAL) {
         s_fac[b][0] = __uint_as_float(s_item[b].arg);   // staged SCAL continuations have k == 1
       }
       if (lane == 0) s_unit[b] = unit;
@@ -1744,21 +1764,24 @@ constexpr unsigned kDoneBatch = 16;                  // completions per RMW on c
 // (nsucc == 1), else ignored.  The unit's completion is counted by the caller.
 __device__ __forceinline__ unsigned long long release_wq(const EpochArgs &a, uint32_t item, const DItem &it,
                                                          uint32_t s0kind, uint32_t s0nc, bool pre) {
-  if (it.nchunks > 1) {
+  const uint32_t nchunks = units_of(it.n, a.chunk_elems);
+  if (nchunks > 1) {
     const unsigned c = atom_add_acq_rel(&a.chunk_done[item], 1u);
-    if (c + 1 != it.nchunks) return kStop;
+    if (c + 1 != nchunks) return kStop;
   }
   unsigned long long cont = kStop;
-  for (uint32_t i = 0; i < it.nsucc; ++i) {
-    const uint32_t s = it.nsucc == 1 ? it.succ_off : __ldg(&a.succ[it.succ_off + i]);   // single successor inline
-    const uint32_t skind = pre ? s0kind : __ldg(&a.items[s].kind);
+  uint32_t nsucc, off;
+  succ_list<true>(a, it.nsucc_field(), it.succ, nsucc, off);
+  for (uint32_t i = 0; i < nsucc; ++i) {
+    const uint32_t s = nsucc == 1 ? off : __ldg(&a.succ[off + i]);   // single successor inline
+    const uint32_t skind = pre ? s0kind : __ldg(&a.items[s].meta);
     // a single-predecessor successor is ready now; with more predecessors
     // the acq_rel RMW both releases ours and acquires theirs
     const bool ready = (skind & K_SINGLE_PRED)
                            ? true
                            : atom_add_acq_rel(reinterpret_cast<unsigned *>(&a.pending[s]), 0xFFFFFFFFu) == 1u;
     if (!ready) continue;
-    const uint32_t nc = pre ? s0nc : __ldg(&a.items[s].nchunks);
+    const uint32_t nc = pre ? s0nc : units_of(__ldg(&a.items[s].n), a.chunk_elems);
     if (cont == kStop && nc == 1) {   // run it here next
       cont = (unsigned long long)s << 32;
       continue;
@@ -1844,29 +1867,30 @@ __global__ void __launch_bounds__(kBlockWQ, BT_WQ_MIN_CTAS) scheduler_kernel_wq(
     // stage the descriptor (lanes 0-2, 16 bytes each; a continuation's was
     // prefetched) and the factor list
     const uint32_t item = (uint32_t)(unit >> 32);
-    if (!cont_staged && lane < 3)
+    if (!cont_staged && lane < 2)
       reinterpret_cast<uint4 *>(my)[lane] = __ldg(reinterpret_cast<const uint4 *>(a.items + item) + lane);
     __syncwarp();
     const DItem it = *my;
-    // prefetch the single successor's descriptor under the body (lanes 0-2)
-    const bool pre = it.nsucc == 1 && it.nchunks == 1;
+    const uint32_t kk = it.k();
+    // prefetch the single successor's descriptor under the body (lanes 0-1)
+    const bool pre = it.nsucc_field() == 1 && units_of(it.n, a.chunk_elems) == 1;
     uint4 nd = {};
-    if (pre && lane < 3) nd = __ldg(reinterpret_cast<const uint4 *>(a.items + it.succ_off) + lane);
-    if ((it.kind & K_MASK) == K_SCAL) {
-      if (it.k == 1) {
+    if (pre && lane < 2) nd = __ldg(reinterpret_cast<const uint4 *>(a.items + it.succ) + lane);
+    if (it.kind() == K_SCAL) {
+      if (kk == 1) {
         if (lane == 0) fac[0] = __uint_as_float(it.arg);   // a single factor travels inline
       } else {
-        for (uint32_t j = lane; j < it.k; j += 32) fac[j] = __ldg(a.factors + it.arg + j);
+        for (uint32_t j = lane; j < kk; j += 32) fac[j] = __ldg(a.factors + it.arg + j);
       }
       __syncwarp();
     }
     if (a.trace) c1 = clock64();
     const uint32_t chunk = (uint32_t)unit;
     const uint64_t lo = (uint64_t)chunk * a.chunk_elems;
-    const uint64_t hi = min(it.n, lo + a.chunk_elems);
-    switch (it.kind & K_MASK) {
+    const uint64_t hi = min((uint64_t)it.n, lo + a.chunk_elems);
+    switch (it.kind()) {
       case K_SCAL:
-        scal_range<BT_WQ_U, 32>(reinterpret_cast<float *>(it.x) + lo, hi - lo, fac, it.k, lane);
+        scal_range<BT_WQ_U, 32>(reinterpret_cast<float *>(it.x) + lo, hi - lo, fac, kk, lane);
         break;
       case K_AXPY:
         axpy_range<32>(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, hi - lo,
@@ -1884,8 +1908,8 @@ __global__ void __launch_bounds__(kBlockWQ, BT_WQ_MIN_CTAS) scheduler_kernel_wq(
     // among the warp's lanes; lane 0's acq_rel operations are cumulative)
     __syncwarp();
     if (a.trace) c2 = clock64();
-    const uint32_t s0kind = __shfl_sync(0xffffffffu, nd.z, 1);   // word 1: n (x, y), kind (z), k (w)
-    const uint32_t s0nc = __shfl_sync(0xffffffffu, nd.y, 2);     // word 2: arg (x), nchunks (y)
+    const uint32_t s0kind = __shfl_sync(0xffffffffu, nd.y, 1);                          // word 1: n, meta, arg, succ
+    const uint32_t s0nc = units_of(__shfl_sync(0xffffffffu, nd.x, 1), a.chunk_elems);
     if (lane == 0) {
       cont = release_wq(a, item, it, s0kind, s0nc, pre);
       chained |= cont != kStop;
@@ -1908,7 +1932,7 @@ __global__ void __launch_bounds__(kBlockWQ, BT_WQ_MIN_CTAS) scheduler_kernel_wq(
     }
     // the next unit's descriptor overwrites this one's: every lane has read it
     __syncwarp();
-    if (cont_staged && lane < 3) reinterpret_cast<uint4 *>(my)[lane] = nd;
+    if (cont_staged && lane < 2) reinterpret_cast<uint4 *>(my)[lane] = nd;
   }
   report_exit(a);
 }
