@@ -126,8 +126,8 @@ struct alignas(64) Lane {
   // totals, and its bases in the epoch's arrays
   vec<RunH> hr;
   vec<uint8_t> reuse;                 // per item with > 1 factor: 1 = same list as the lane's previous one
-  uint64_t d_items = 0, d_elems = 0, d_work = 0, d_fac = 0, d_tasks = 0;
-  uint64_t ibase = 0, fbase = 0;
+  uint64_t d_items = 0, d_elems = 0, d_work = 0, d_fac = 0, d_tasks = 0, d_units = 0, d_ready = 0;
+  uint64_t ibase = 0, fbase = 0, qbase = 0;
   char pad_[64];                      // keep neighbouring lanes off this cache line
   void clear() {
     items.clear();
@@ -266,7 +266,7 @@ class Builder {
   template <class Src, class Loc, class SlotOf, class Geom>
   void lane_count(Lane &L, Src &&src, uint32_t nlocal, Loc &&loc, SlotOf &&slot_of, Geom &&geom);
   template <class Geom, class Item>
-  void lane_write(Lane &L, float *fac, Geom &&geom, Item &&item);
+  void lane_write(Lane &L, uint64_t chunk_elems, float *fac, unsigned long long *queue, Geom &&geom, Item &&item);
 
  private:
   void fresh(DepState &st) {
@@ -569,16 +569,21 @@ void Builder::lane_count(Lane &L, Src &&src, uint32_t nlocal, Loc &&loc, SlotOf 
 }
 
 // item(id) -> DItem& of the epoch; ids are L.ibase + position; factor lists
-// go to fac[L.fbase ...].
+// go to fac[L.fbase ...], the initially ready units to queue[L.qbase ...].
 template <class Geom, class Item>
-void Builder::lane_write(Lane &L, float *fac, Geom &&geom, Item &&item) {
+void Builder::lane_write(Lane &L, uint64_t chunk_elems, float *fac, unsigned long long *queue, Geom &&geom,
+                         Item &&item) {
   const uint32_t step = fusion ? max_fused : 1u;
   const float *fs = L.fpool.data();
   uint32_t id = (uint32_t)L.ibase;
   uint32_t fo = (uint32_t)L.fbase, pfo = 0;
+  uint64_t qi = L.qbase;
   size_t ri = 0;
   for (const RunH &h : L.hr) {
     const auto g = geom(h.slot);
+    // the chain's first item starts ready: its units join the initial queue
+    const uint32_t nc = units_of((uint32_t)g.second, chunk_elems);
+    for (uint32_t c = 0; c < nc; ++c) queue[qi++] = ((unsigned long long)id << 32) | c;
     for (uint32_t q = 0; q < h.items; ++q, ++id) {
       const uint32_t take = std::min(step, h.m - q * step);
       const float *f = fs + h.start + q * step;

@@ -49,7 +49,8 @@ BT_HD inline uint32_t make_meta(uint32_t kind, bool single_pred, uint32_t k, uin
          ((uint32_t)(nsucc < K_NSUCC_ESC ? nsucc : K_NSUCC_ESC) << K_NSUCC_SHIFT);
 }
 BT_HD inline uint32_t units_of(uint32_t n, uint64_t chunk_elems) {
-  return (uint32_t)(((uint64_t)n + chunk_elems - 1) / chunk_elems);
+  // (the common single-unit case without a division: chains of small items)
+  return n <= chunk_elems ? 1u : (uint32_t)(((uint64_t)n + chunk_elems - 1) / chunk_elems);
 }
 
 // Epoch counters, in device memory, initialised by the host upload.

@@ -857,13 +857,26 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
     acc[p] = a;
   };
   if (dr) {   // a direct round: units from the lanes' handle runs (every chain starts ready)
-    RangeAcc a;
-    for (size_t i = 0; i < dr->nlanes; ++i)
-      for (const RunH &h : dr->lanes[i]->hr) {
-        const uint64_t nc = (rt->hot[h.slot].nx + CE - 1) / CE;
-        a.units += nc * h.items;
-        a.ready += nc;
+    const SlotHot *hot = rt->hot.data();
+    rt->par([&](int l) {
+      for (size_t i = (size_t)l; i < dr->nlanes; i += (size_t)rt->pool->size()) {
+        Lane &L = *dr->lanes[i];
+        uint64_t u = 0, r = 0;
+        for (const RunH &h : L.hr) {
+          const uint64_t nc = units_of((uint32_t)hot[h.slot].nx, CE);
+          u += nc * h.items;
+          r += nc;
+        }
+        L.d_units = u;
+        L.d_ready = r;
       }
+    });
+    RangeAcc a;
+    for (size_t i = 0; i < dr->nlanes; ++i) {
+      dr->lanes[i]->qbase = a.ready;
+      a.units += dr->lanes[i]->d_units;
+      a.ready += dr->lanes[i]->d_ready;
+    }
     a.succ = E;
     a.fac = dr->F;
     acc[0] = a;
@@ -1037,20 +1050,13 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
     }
   };
   if (dr) {
-    // direct round: the ready queue (every chain's first item, in item order),
-    // then the lanes write their descriptors in parallel
-    uint64_t qi = 0, id = 0;
-    for (size_t i = 0; i < dr->nlanes; ++i)
-      for (const RunH &h : dr->lanes[i]->hr) {
-        const uint64_t nc = (rt->hot[h.slot].nx + CE - 1) / CE;
-        for (uint64_t c = 0; c < nc; ++c) q[qi++] = (id << 32) | c;
-        id += h.items;
-      }
+    // direct round: the lanes write their descriptors and initially ready
+    // units (every chain's first item) in parallel
     const SlotHot *hot = rt->hot.data();
     rt->par([&](int l) {
       for (size_t i = (size_t)l; i < dr->nlanes; i += (size_t)rt->pool->size())
         B.lane_write(
-            *dr->lanes[i], fac,
+            *dr->lanes[i], CE, fac, q,
             [hot](uint32_t sl) { return std::pair<uint64_t, uint64_t>(reinterpret_cast<uint64_t>(hot[sl].dptr), hot[sl].nx); },
             [di](uint32_t id2) -> DItem & { return di[id2]; });
     });

@@ -875,7 +875,7 @@ __device__ __forceinline__ void compute_loop_rw(const EpochArgs &a, const unsign
     unsigned par = 0, extra = 0;
     for (;;) {
       // may this unit continue in the slot?  (uniform: every thread sees it)
-      const bool maybe = BT_INSLOT && !a.trace && units_of(it.n, a.chunk_elems) == 1 && it.nsucc_field() == 1;
+      const bool maybe = BT_INSLOT && !a.trace && (uint64_t)it.n <= a.chunk_elems && it.nsucc_field() == 1;
       if (maybe && tid == 0) {   // the successor's descriptor, copied to shared memory under the body
         const unsigned dst = (unsigned)__cvta_generic_to_shared(&s_nitem[b][par]);
         const DItem *src = a.items + it.succ;
@@ -908,7 +908,7 @@ __device__ __forceinline__ void compute_loop_rw(const EpochArgs &a, const unsign
       if (tid == 0) {
         asm volatile("cp.async.wait_all;" ::: "memory");
         const DItem &n = s_nitem[b][par];
-        const unsigned go = n.single_pred() && units_of(n.n, a.chunk_elems) == 1 && (n.kind() != K_SCAL || n.k() == 1)
+        const unsigned go = n.single_pred() && (uint64_t)n.n <= a.chunk_elems && (n.kind() != K_SCAL || n.k() == 1)
                                 ? 1u : 0u;
         if (go) s_nfac[b][par] = __uint_as_float(n.arg);   // a single factor travels in arg
         s_go[b][par] = go;
@@ -1873,7 +1873,7 @@ __global__ void __launch_bounds__(kBlockWQ, BT_WQ_MIN_CTAS) scheduler_kernel_wq(
     const DItem it = *my;
     const uint32_t kk = it.k();
     // prefetch the single successor's descriptor under the body (lanes 0-1)
-    const bool pre = it.nsucc_field() == 1 && units_of(it.n, a.chunk_elems) == 1;
+    const bool pre = it.nsucc_field() == 1 && (uint64_t)it.n <= a.chunk_elems;
     uint4 nd = {};
     if (pre && lane < 2) nd = __ldg(reinterpret_cast<const uint4 *>(a.items + it.succ) + lane);
     if (it.kind() == K_SCAL) {
