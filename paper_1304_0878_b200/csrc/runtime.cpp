@@ -648,8 +648,12 @@ bool stream_defer() {
   static const bool d = [] {
     const char *lb = getenv("CUDA_LAUNCH_BLOCKING");
     if (getenv("BT_STREAM_NODEFER")) return false;   // tests: exercise the close + resume path
+    // Nsight Compute's target environment (checked on the box: ncu 2025.2
+    // sets NV_NSIGHT_INJECTION_* and NV_COMPUTE_PROFILER_PERFWORKS_DIR);
+    // CUDA_INJECTION64_PATH: injection-based tools in general
     return getenv("BT_STREAM_DEFER") != nullptr || getenv("CUDA_INJECTION64_PATH") != nullptr ||
-           (lb && lb[0] == '1');
+           getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr ||
+           getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR") != nullptr || (lb && lb[0] == '1');
   }();
   return d;
 }
