@@ -989,6 +989,26 @@ def test_long_chain_max_fused(B, kernel, max_fused):
     assert stats["items"] == -(-1000 // max_fused)
 
 
+@pytest.mark.parametrize("kernel", ["auto", "sw", "rw", "wq"])
+def test_item_with_many_successors(B, kernel):
+    """An item with more successors than the descriptor's count field holds
+    (8,191: the escaped count precedes the successor list, device_abi.h DItem):
+    X is scaled, read by 9,000 AXPYs into the tiles of Y (RAW fan-out), then
+    scaled again (WAR fan-in of 9,000 predecessors)."""
+    rng = np.random.default_rng(W.SEED_BASE + 98)
+    n, nt = 256, 9000
+    x = W.unit_interval_floats(rng, n)
+    y = W.unit_interval_floats(rng, n * nt)
+    rows = [(W.SCAL, np.float32(1.5), 0, -1, -1, -1)]
+    rows += [(W.AXPY, np.float32(0.25), 0, -1, 1, t) for t in range(nt)]
+    rows += [(W.SCAL, np.float32(0.5), 0, -1, -1, -1)]
+    p = W.Program([x, y], [0, nt], W._tasks(len(rows)), name="fan-out 9,000")
+    for i, r in enumerate(rows):
+        p.tasks[i] = r
+    stats = compare_program(p, flags=KERNELS[kernel])
+    assert stats["edges"] >= 2 * nt, stats
+
+
 def test_one_element_tiles(B):
     """Degenerate partitions: 1-element tiles (nparts = nx) and 3-element tiles
     (every 256-bit vector path falls back to the scalar head/tail), with
