@@ -61,7 +61,8 @@ def make(seed, device=False):
                       sweeps=int(rng.integers(1, 40)), seed=seed,
                       order="sweep" if rng.random() < 0.5 else "tile")
     kw = dict(chunk_bytes=int(rng.choice([0, 0, 32, 96, 4096, 65536])),
-              flags=(0 if rng.random() < 0.6 else B.BT_FLAG_NO_FUSION) | int(rng.choice(KERNELS)),
+              flags=(0 if rng.random() < 0.6 else B.BT_FLAG_NO_FUSION) | int(rng.choice(KERNELS)) |
+              (B.BT_FLAG_PRIORITY if rng.random() < 0.3 else 0),
               host_threads=int(rng.integers(1, 6)), parallel_min=int(rng.integers(1, 64)),
               pipeline_min=int(rng.integers(1, 64)), pipeline_rounds=int(rng.integers(1, 5)),
               max_fused=int(rng.choice([0, 1, 3, 7, 64, 1024])),
