@@ -378,5 +378,41 @@ def test_library_contains_every_kernel(B):
     launch and the set-up kernel."""
     out = subprocess.check_output(["cuobjdump", "--list-text", B.LIB_PATH], text=True)
     for k in ("scheduler_kernel_sw", "scheduler_kernel_sws", "scheduler_kernel_rw", "scheduler_kernel_wq",
-              "direct_kernel", "stage_kernel"):
+              "scheduler_kernel_swp", "direct_kernel", "stage_kernel", "flag_wait_kernel", "flag_write_kernel",
+              "gate_kernel"):
         assert k in out, k
+
+
+def test_descriptor_packing(tmp_path):
+    """The 32-byte work-item descriptor (device_abi.h DItem): the packed meta
+    word round-trips kind, single-predecessor bit, k up to 2047 and successor
+    counts, escaping at 8,191; single-unit test without division."""
+    src = tmp_path / "meta.cpp"
+    src.write_text(
+        '#include <cstdio>\n#include <initializer_list>\n#include "device_abi.h"\nusing namespace bt;\n'
+        'int main() { int bad = 0; DItem d{};\n'
+        ' for (unsigned kind = 1; kind <= 3; ++kind) for (int sp = 0; sp < 2; ++sp)\n'
+        '  for (unsigned k : {1u, 2u, 64u, 1024u, 2047u}) for (unsigned long ns : {0ul, 1ul, 2ul, 8190ul, 8191ul, 9000ul, 1ul << 20}) {\n'
+        '   d.meta = make_meta(kind, sp, k, ns);\n'
+        '   unsigned f = d.nsucc_field();\n'
+        '   bad += d.kind() != kind || d.single_pred() != (bool)sp || d.k() != k ||\n'
+        '          f != (ns < K_NSUCC_ESC ? ns : K_NSUCC_ESC); }\n'
+        ' bad += units_of(1, 16384) != 1 || units_of(16384, 16384) != 1 || units_of(16385, 16384) != 2 ||\n'
+        '        units_of(100, 24) != 5 || units_of(0xFFFFFFFFu, 8) != 0x20000000u;\n'
+        ' printf("%d %zu\\n", bad, sizeof(DItem)); return 0; }\n')
+    exe = tmp_path / "meta"
+    subprocess.check_call(["g++", "-std=c++17", "-I", os.path.join(ROOT, "paper_1304_0878_b200", "csrc"), str(src),
+                           "-o", str(exe)])
+    bad, size = map(int, subprocess.check_output([str(exe)], text=True).split())
+    assert bad == 0 and size == 32
+
+
+def test_register_rejects_vectors_of_2_32_elements(B):
+    """Descriptors hold 32-bit lengths (reading R22): 2^32 elements -> -EINVAL."""
+    rt = B.Runtime(flags=B.BT_FLAG_HOST_ONLY)
+    h = B.bt_handle()
+    rc = B.bt_vector_data_register(rt.rt, ctypes.byref(h), 0, None, 1 << 32, 4)
+    assert rc == -errno.EINVAL and "2^32" in rt.last_error()
+    assert B.bt_vector_data_register(rt.rt, ctypes.byref(h), 0, None, (1 << 32) - 1, 4) == 0
+    assert B.bt_data_unregister(rt.rt, h.value) == 0
+    rt.close()
