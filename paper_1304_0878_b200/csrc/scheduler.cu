@@ -1961,7 +1961,9 @@ __global__ void __launch_bounds__(256) direct_kernel(const __grid_constant__ Arg
     case K_SCAL:
       for (uint32_t j = tid; j < it.k; j += blockDim.x) sf[j] = p.factors[it.arg + j];
       __syncthreads();
-      scal_range<4, 256>(reinterpret_cast<float *>(it.x) + lo, n, sf, it.k, tid);
+      // short chains are HBM-bound: keep the next step's loads in flight (as "sws")
+      if (it.k < 32) scal_range_pf<2, 256>(reinterpret_cast<float *>(it.x) + lo, n, sf, it.k, tid);
+      else scal_range<4, 256>(reinterpret_cast<float *>(it.x) + lo, n, sf, it.k, tid);
       break;
     case K_AXPY:
       axpy_range<256>(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, n,
