@@ -189,6 +189,12 @@ int bt_data_distribute_block(bt_runtime *rt, bt_handle h);
  * runs on b; other ranks skip it.  Every rank must register x (with local
  * storage) and partition it alike.  A non-owner's replica of x holds the last
  * value it received; only owners' data is defined after the program.
+ * A reader keeps what it received as a shared copy: a later read of the same
+ * range by the same rank skips the transfer (on both ranks) while no task has
+ * written the data since -- every rank sees every task, so both decide alike.
+ * Host writes to data other ranks read (bt_data_acquire BT_RW + release) must
+ * then be collective: every rank calls bt_data_release at the same point of
+ * the task stream (a release invalidates the shared copies).
  * Returns 0, -EINVAL (nranks < 2, bad name, ranks disagree), -ENODEV
  * (host-only runtime), -EBUSY (already initialised), -ETIMEDOUT (a rank did
  * not join within 60 s), -EIO.  A rendezvous that times out (60 s) returns
@@ -284,6 +290,8 @@ typedef struct bt_stats {
   uint64_t prio_epochs;       /* epochs run with the priority ready queue (upward-rank levels) */
   uint64_t h2d_data_bytes;    /* host-homed data uploaded (first reads; bt_data_release of an RW acquire) */
   uint64_t d2h_data_bytes;    /* host-homed data written back (eager write-backs, dirty ranges) */
+  uint64_t cross_rank_copies; /* cross-rank reads that copied their operand (bt_comm_init) */
+  uint64_t cross_rank_skips;  /* ... that found the pair's previous copy still current (no write since) */
 } bt_stats;
 int bt_stats_get(bt_runtime *rt, bt_stats *out);
 int bt_stats_reset(bt_runtime *rt);

@@ -44,7 +44,8 @@ class bt_stats(ctypes.Structure):
                 ("block", ctypes.c_uint32), ("kernel_launches", ctypes.c_uint64),
                 ("sched_launches", ctypes.c_uint64), ("stream_closes", ctypes.c_uint64),
                 ("stream_resumes", ctypes.c_uint64), ("prio_epochs", ctypes.c_uint64),
-                ("h2d_data_bytes", ctypes.c_uint64), ("d2h_data_bytes", ctypes.c_uint64)]
+                ("h2d_data_bytes", ctypes.c_uint64), ("d2h_data_bytes", ctypes.c_uint64),
+                ("cross_rank_copies", ctypes.c_uint64), ("cross_rank_skips", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -20,6 +20,7 @@
 #include <chrono>
 #include <map>
 #include <memory>
+#include <tuple>
 #include <string>
 #include <thread>
 #include <unordered_map>
@@ -299,6 +300,17 @@ struct bt_runtime {
   void put_event(cudaEvent_t e) { ev_free.push_back(e); }
   bt_stats stats{};
   std::unique_ptr<Comm> comm;   // cross-rank reads (bt_comm_init)
+  // Shared copies across ranks (NEXT-4, "lazy MSI across ranks"): every rank
+  // sees every task in submission order, so every rank can tell alike whether
+  // data a reader copied before has been written since.  wver[root] counts
+  // the tasks writing a part of the root (local or not); gver is bumped by
+  // everything coarser (a parallel SCAL run, registration, partitioning, rank
+  // changes, a host RW release -- collective calls under bt_comm_init).  A
+  // cross-rank read whose (wver, gver) equal those of the pair's last transfer
+  // of the same range skips the rendezvous on both sides.
+  std::vector<uint64_t> wver;
+  uint64_t gver = 1;
+  std::map<std::tuple<uint64_t, uint64_t, uint64_t, int>, std::pair<uint64_t, uint64_t>> xcache;
   uint64_t reg_seq = 0;         // registrations so far (Slot::reg_key)
 
   // host-only snapshot storage
@@ -1707,6 +1719,7 @@ int bt_data_lookup(bt_runtime *rt, const void *ptr, bt_handle *out) {
 
 int bt_data_partition(bt_runtime *rt, bt_handle h, uint32_t nparts) {
   if (int r = check_live(rt)) return r;
+  ++rt->gver;
   uint32_t s = resolve(rt, h);
   if (s == NONE) return fail(rt, -ENOENT, "attempt to use unregistered pointer");
   if (rt->slots[s].nparts) return fail(rt, -EBUSY, "handle already partitioned");
@@ -1786,6 +1799,7 @@ int bt_data_get_children(bt_runtime *rt, bt_handle h, bt_handle *out, uint32_t n
 
 int bt_data_unpartition(bt_runtime *rt, bt_handle h) {
   if (int r = check_live(rt)) return r;
+  ++rt->gver;
   uint32_t s = resolve(rt, h);
   if (s == NONE) return fail(rt, -ENOENT, "attempt to use unregistered pointer");
   Slot &p = rt->slots[s];
@@ -1806,6 +1820,7 @@ int bt_data_unpartition(bt_runtime *rt, bt_handle h) {
 
 int bt_data_set_rank(bt_runtime *rt, bt_handle h, int rank) {
   if (int r = check_live(rt)) return r;
+  ++rt->gver;
   uint32_t s = resolve(rt, h);
   if (s == NONE) return fail(rt, -ENOENT, "attempt to use unregistered pointer");
   if (rank < 0 || rank >= rt->cfg.nranks) return fail(rt, -EINVAL, "rank %d out of range", rank);
@@ -1913,10 +1928,19 @@ int cross_rank_read(bt_runtime *rt, uint32_t x, int peer, bool send) {
   return 0;
 }
 
+// A task writes a part of slot s's root (every rank, local task or not).
+inline void note_write(bt_runtime *rt, uint32_t s) {
+  if (!rt->comm) return;
+  const uint32_t r = rt->slots[s].root;
+  if (rt->wver.size() <= r) rt->wver.resize(r + 1, 0);
+  ++rt->wver[r];
+}
+
 int submit(bt_runtime *rt, int codelet, float scalar, bt_handle h0, bt_handle h1) {
   if (rt->poisoned) return fail(rt, rt->poisoned, "runtime poisoned by an earlier device error");
   int64_t s0 = operand(rt, codelet, h0);
   if (s0 < 0) return (int)s0;
+  if (codelet == BT_CL_SCAL) note_write(rt, (uint32_t)s0);
   if (codelet == BT_CL_SCAL) {
     const SlotHot &x = rt->hot[s0];
     if (x.rank != rt->cfg.rank) {
@@ -1944,9 +1968,24 @@ int submit(bt_runtime *rt, int codelet, float scalar, bt_handle h0, bt_handle h1
       const int me = rt->cfg.rank;
       if (me == x.rank || me == y.rank) {
         if (!x.dptr || (me == y.rank && !y.dptr)) return insert_fail(rt, codelet, -EINVAL, "no local storage");
-        if (int r = cross_rank_read(rt, (uint32_t)s0, me == x.rank ? y.rank : x.rank, me == x.rank)) return r;
+        // the pair's last transfer of this range is still current: skip (both sides)
+        const Slot &xs = rt->slots[s0];
+        const uint32_t root = xs.root;
+        const int reader = y.rank;
+        const auto key = std::make_tuple(rt->slots[root].reg_key, (uint64_t)(xs.offset - rt->slots[root].offset),
+                                         (uint64_t)x.nx, reader);
+        const std::pair<uint64_t, uint64_t> ver(root < rt->wver.size() ? rt->wver[root] : (uint64_t)0, rt->gver);
+        auto it = rt->xcache.find(key);
+        if (it != rt->xcache.end() && it->second == ver) {
+          ++rt->stats.cross_rank_skips;
+        } else {
+          if (int r = cross_rank_read(rt, (uint32_t)s0, me == x.rank ? y.rank : x.rank, me == x.rank)) return r;
+          rt->xcache[key] = ver;
+          ++rt->stats.cross_rank_copies;
+        }
       }
     }
+    note_write(rt, (uint32_t)s1);
     if (y.rank != rt->cfg.rank) {
       if (y.rank < 0) return insert_fail(rt, codelet, -EINVAL, "data has no home rank");
       rt->builder.add_remote();
@@ -2018,6 +2057,7 @@ bool phase1_simd() { return false; }
 
 int scal_run_parallel(bt_runtime *rt, const int32_t *codelets, const float *scalars, const bt_handle *h0, size_t i0,
                       size_t i1) {
+  ++rt->gver;   // the run writes many roots: every shared copy across ranks is invalid
   const int P = rt->pool->size();
   const size_t n = i1 - i0;
   Builder &B = rt->builder;
@@ -2592,6 +2632,7 @@ int bt_data_acquire(bt_runtime *rt, bt_handle h, int mode) {
 
 int bt_data_release(bt_runtime *rt, bt_handle h) {
   if (int r = check_live(rt)) return r;
+  ++rt->gver;   // host writes (RW): collective under bt_comm_init (btask.h)
   uint32_t s = resolve(rt, h);
   if (s == NONE) return fail(rt, -ENOENT, "attempt to use unregistered pointer");
   Slot &sl = rt->slots[s];
@@ -2619,6 +2660,7 @@ int bt_data_release(bt_runtime *rt, bt_handle h) {
 
 int bt_data_unregister(bt_runtime *rt, bt_handle h) {
   if (int r = check_live(rt)) return r;
+  ++rt->gver;
   uint32_t s = resolve(rt, h);
   if (s == NONE) return fail(rt, -ENOENT, "attempt to use unregistered pointer");
   Slot &sl = rt->slots[s];

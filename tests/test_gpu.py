@@ -855,6 +855,31 @@ def test_cross_rank_reads_random_programs(B, batch):
         _check_owned(p, results, owners)
 
 
+def test_cross_rank_shared_copies(B):
+    """Shared copies across ranks (NEXT-4, "lazy MSI across ranks"): rank 1
+    reads X (rank 0's) into five of its buffers with no write of X in between
+    -- one transfer, four skipped on both ranks --, then rank 0 scales X and
+    rank 1 reads it again (a new transfer), and a tile of a partitioned
+    buffer is read twice; every owner's data is the oracle's."""
+    from tests import xrank
+    n = 1 << 16
+    rng = np.random.default_rng(W.SEED_BASE + 99)
+    bufs = [W.unit_interval_floats(rng, n) for _ in range(7)] + [W.unit_interval_floats(rng, 4 * n)]
+    rows = [(W.COPY, 0.0, 0, -1, 1 + i, -1) for i in range(5)]          # 1 transfer + 4 skips
+    rows += [(W.SCAL, np.float32(1.25), 0, -1, -1, -1),                  # X written on rank 0
+             (W.AXPY, np.float32(0.5), 0, -1, 6, -1),                    # new transfer
+             (W.AXPY, np.float32(0.25), 0, -1, 6, -1),                   # skip
+             (W.COPY, 0.0, 7, 1, 1, -1), (W.COPY, 0.0, 7, 1, 2, -1)]     # tile 1 of buffer 7: transfer + skip
+    p = W.Program(bufs, [0] * 7 + [4], W._tasks(len(rows)), name="shared copies across ranks")
+    for i, r in enumerate(rows):
+        p.tasks[i] = r
+    owners = [0, 1, 1, 1, 1, 1, 1, [0, 0, 1, 1]]
+    results, stats, owners = xrank.run(p, nranks=2, owners=owners, batch=False)
+    _check_owned(p, results, owners)
+    for st in stats:
+        assert st["cross_rank_copies"] == 3 and st["cross_rank_skips"] == 4 + 1 + 1, st
+
+
 @pytest.mark.parametrize("protocol", ["host", "flag_kernels"])
 def test_cross_rank_other_protocols(B, protocol):
     """The same random cross-rank programs with the host protocol (shared-memory
