@@ -80,7 +80,7 @@ def main():
     ap.add_argument("--count", type=int, default=0, help="stop after this many programs (0: --minutes only)")
     ap.add_argument("--extra-flags", type=int, default=0, help="OR-ed into every configuration's flags")
     args = ap.parse_args()
-    streams = 0
+    streams = resumes = 0
     t_end = time.time() + 60 * args.minutes
     seed, n, tasks = args.seed0, 0, 0
     while time.time() < t_end and (not args.count or n < args.count):
@@ -101,6 +101,7 @@ def main():
                                   "config": {k: int(v) for k, v in kw.items()}}), flush=True)
                 return 1
             streams += st["sched_launches"] < st["epochs"]
+            resumes += st.get("stream_resumes", 0)
             p = W.Program(p.buffers, p.nparts, np.concatenate([p.tasks] * reps), name=p.name)
         else:
             out, st = run_program(p, device=0, **kw)
@@ -118,7 +119,8 @@ def main():
                   flush=True)
         seed += 1
     print(json.dumps({"ok": True, "programs": n, "tasks": tasks, "seeds": [args.seed0, seed - 1],
-                      "device_homed": args.device, "with_stream_launch": streams}), flush=True)
+                      "device_homed": args.device, "with_stream_launch": streams, "stream_resumes": resumes,
+                      "env": {k: v for k, v in os.environ.items() if k.startswith("BT_")}}), flush=True)
     return 0
 
 
