@@ -66,6 +66,7 @@ using vec = std::vector<T, NoInitAlloc<T>>;
 
 constexpr uint32_t NONE = 0xFFFFFFFFu;
 constexpr uint32_t TAG = 0x80000000u;     // lane-local item id / lane-local factor offset
+constexpr uint32_t STAMP_NONE = 0x7FFFFFFFu;   // HItem::stamp of no task
 
 // Per leaf (sub)handle.  12 bytes; multi-writer / reader sets live in exts.
 struct DepState {
@@ -89,7 +90,11 @@ struct HItem {
   uint32_t fcap;       // SCAL: reserved factors at fofs
   uint32_t npred;
   uint32_t nsucc;      // updated atomically by lanes for shared predecessors
-  uint32_t stamp;      // dedupe marker (sequential path)
+  uint32_t stamp : 31; // dedupe marker (sequential path; item ids < 2^31)
+  // 1: some predecessor reached this item through ANOTHER (sub)handle (a
+  // partition's parent / parts): its element ranges may not line up with this
+  // item's, so every predecessor counts as a whole (no chunk-wise release)
+  uint32_t item_deps : 1;
 };
 
 struct LaneEntry {
@@ -204,7 +209,7 @@ class Builder {
     it.fcap = 4;
     fpool.resize(fpool.size() + 4);
     memcpy(&fpool[it.fofs], &fbits, 4);
-    collect(st, t, 3u);
+    collect(st, t, 3u, s);
     st.writer = t;
     st.ext = NONE;
   }
@@ -218,11 +223,11 @@ class Builder {
     const uint32_t t = new_item(kind, s0, s1, x, y, n, arg);
     if (st1 == st0) {  // same handle twice: modes OR-ed (reading R6)
       const uint32_t m = m0 | m1;
-      collect(*st0, t, m);
+      collect(*st0, t, m, s0);
       update(*st0, t, m);
     } else {
-      collect(*st0, t, m0);
-      collect(*st1, t, m1);
+      collect(*st0, t, m0, s0);
+      collect(*st1, t, m1, s1);
       update(*st0, t, m0);
       update(*st1, t, m1);
     }
@@ -300,7 +305,7 @@ class Builder {
 
   uint32_t new_item(uint32_t kind, uint32_t s0, uint32_t s1, uint64_t x, uint64_t y, uint64_t n, uint32_t arg) {
     const uint32_t t = (uint32_t)items.size();
-    items.push_back(HItem{kind, 1, s0, s1, x, y, n, arg, 0, 0, 0, 0, NONE});
+    items.push_back(HItem{kind, 1, s0, s1, x, y, n, arg, 0, 0, 0, 0, STAMP_NONE, 0});
     record(t, 0);
     return t;
   }
@@ -314,13 +319,22 @@ class Builder {
     edges.push_back(((uint64_t)p << 32) | t);
   }
 
-  void collect(DepState &st, uint32_t t, uint32_t mode) {
-    if (st.writer != NONE) edge(st.writer, t);
+  // The predecessors in the state of (sub)handle `slot`, which item t accesses.
+  // A predecessor that accessed the same slot touched the same elements at
+  // the same offsets (chunk c of both covers the same elements); one found
+  // through partition-inherited state did not (item_deps).
+  void collect(DepState &st, uint32_t t, uint32_t mode, uint32_t slot) {
+    auto add = [&](uint32_t p) {
+      const HItem &pi = items[p];
+      if (pi.slot0 != slot && pi.slot1 != slot) items[t].item_deps = 1;
+      edge(p, t);
+    };
+    if (st.writer != NONE) add(st.writer);
     if (st.ext != NONE) {
       const DepExt &e = exts[st.ext];
-      for (uint32_t w : e.writers) edge(w, t);
+      for (uint32_t w : e.writers) add(w);
       if (mode & 2u)
-        for (uint32_t r : e.readers) edge(r, t);
+        for (uint32_t r : e.readers) add(r);
     }
   }
 
@@ -459,7 +473,7 @@ void Builder::lane_runs(Lane &L, const LaneEntry *const *chunks, const uint32_t 
         const uint32_t take = std::min(m - i, step);
         const uint32_t t = TAG | (uint32_t)li;
         IT[li] = HItem{1, take, s, NONE, g.first, 0, g.second, 0, TAG | (b + i), take, 1, q + 1 < cnt_items ? 1u : 0u,
-                       NONE};
+                       STAMP_NONE, 0};
         ED[le] = ((uint64_t)prev << 32) | t;
         if (record_tasks)
           for (uint32_t r = 0; r < take; ++r) {
@@ -476,11 +490,13 @@ void Builder::lane_runs(Lane &L, const LaneEntry *const *chunks, const uint32_t 
       const uint32_t take = fusion ? std::min(m - i, max_fused) : 1u;
       const uint32_t local = (uint32_t)L.items.size();
       const uint32_t t = TAG | local;
-      L.items.push_back(HItem{1, take, s, NONE, g.first, 0, g.second, 0, TAG | (b + i), take, 0, 0, NONE});
+      L.items.push_back(HItem{1, take, s, NONE, g.first, 0, g.second, 0, TAG | (b + i), take, 0, 0, STAMP_NONE, 0});
       uint32_t np = 0;
       auto link = [&](uint32_t p) {
         if (p & TAG) ++L.items[p & ~TAG].nsucc;
         else __atomic_fetch_add(&items[p].nsucc, 1u, __ATOMIC_RELAXED);
+        // (a global predecessor through another slot: partition-inherited state)
+        if (!(p & TAG) && items[p].slot0 != s && items[p].slot1 != s) L.items[local].item_deps = 1;
         L.edges.push_back(((uint64_t)p << 32) | t);
         ++np;
       };
@@ -592,7 +608,7 @@ void Builder::lane_write(Lane &L, uint64_t chunk_elems, float *fac, unsigned lon
       d.x = g.first;
       d.y = 0;
       d.n = (uint32_t)g.second;
-      d.meta = make_meta(K_SCAL, q > 0, take, more ? 1 : 0);
+      d.meta = make_meta(K_SCAL, q > 0, take, more ? 1 : 0, false, g.second <= chunk_elems);
       if (take == 1) {
         memcpy(&d.arg, f, 4);
       } else {

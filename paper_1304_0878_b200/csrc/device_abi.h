@@ -16,14 +16,23 @@ namespace bt {
 enum : uint32_t { K_SCAL = 1, K_AXPY = 2, K_COPY = 3 };
 
 // DItem::meta: kind (bits 0-3) | K_SINGLE_PRED (bit 4) | priority level
-// (bits 5-7, device_abi Bucket) | k (bits 8-18) | successor count (bits 19-31).
+// (bits 5-7, device_abi Bucket) | k (bits 8-18) | K_ITEM_DEPS (bit 19) |
+// K_ONE_UNIT (bit 20) | successor count (bits 21-31).
 constexpr uint32_t K_MASK = 0xFu;
 // the item has exactly one predecessor, so the completion of that
 // predecessor makes it ready without touching its pending counter
 constexpr uint32_t K_SINGLE_PRED = 1u << 4;
 constexpr uint32_t K_LEVEL_SHIFT = 5, K_LEVEL_MASK = 0x7u;
 constexpr uint32_t K_K_SHIFT = 8, K_K_MASK = 0x7FFu;            // chained factors, 1..2047
-constexpr uint32_t K_NSUCC_SHIFT = 19, K_NSUCC_ESC = 0x1FFFu;   // 8191: the count is succ[succ], the list follows
+// Chunk-wise release: chunk c of an item covers elements [c*chunk, (c+1)*chunk)
+// of each operand, and a predecessor that reached the item through the same
+// (sub)handle touched the same elements at the same offsets -- so chunk c of
+// the item needs only chunk c of such a predecessor (same length), not all of
+// it (SCAL/AXPY/COPY are element-wise).  K_ITEM_DEPS: some predecessor came
+// through partition-inherited state (other offsets): wait for whole items.
+constexpr uint32_t K_ITEM_DEPS = 1u << 19;
+constexpr uint32_t K_ONE_UNIT = 1u << 20;   // the item is one work unit (n <= the epoch's chunk): no length load
+constexpr uint32_t K_NSUCC_SHIFT = 21, K_NSUCC_ESC = 0x7FFu;   // 2047: the count is succ[succ], the list follows
 
 // One work item of an epoch: a task, or a fused chain of SCAL tasks on the
 // same (sub)handle.  32 bytes (two 16-byte words), read-only during the kernel:
@@ -44,8 +53,10 @@ struct alignas(16) DItem {
   BT_HD bool single_pred() const { return (meta & K_SINGLE_PRED) != 0; }
 };
 static_assert(sizeof(DItem) == 32, "DItem layout");
-BT_HD inline uint32_t make_meta(uint32_t kind, bool single_pred, uint32_t k, uint64_t nsucc) {
-  return kind | (single_pred ? K_SINGLE_PRED : 0u) | (k << K_K_SHIFT) |
+BT_HD inline uint32_t make_meta(uint32_t kind, bool single_pred, uint32_t k, uint64_t nsucc, bool item_deps = false,
+                                bool one_unit = false) {
+  return kind | (single_pred ? K_SINGLE_PRED : 0u) | (k << K_K_SHIFT) | (item_deps ? K_ITEM_DEPS : 0u) |
+         (one_unit ? K_ONE_UNIT : 0u) |
          ((uint32_t)(nsucc < K_NSUCC_ESC ? nsucc : K_NSUCC_ESC) << K_NSUCC_SHIFT);
 }
 BT_HD inline uint32_t units_of(uint32_t n, uint64_t chunk_elems) {
@@ -98,7 +109,9 @@ constexpr unsigned long long Q_EMPTY = ~0ull;
 
 struct EpochArgs {
   const DItem *items;
-  int32_t *pending;             // unfinished predecessors per item
+  int32_t *pending;             // unfinished predecessors per item (single-unit items)
+  int32_t *cpending;            // ... per unit (unit_base[item] + chunk) of items of several units with
+                                // several predecessors (chunk-wise release); null if the epoch has none
   uint32_t *chunk_done;         // finished units per item
   const uint32_t *succ;
   const float *factors;
@@ -107,8 +120,8 @@ struct EpochArgs {
   Counters *host_ctr;           // mapped pinned host memory: the last CTA copies *ctr here
   unsigned long long *trace;    // 4 timestamps per unit, or null
   uint32_t *trace_item;         // item per unit, or null
-  const uint32_t *unit_base;    // traced epochs: first trace record of each item (its chunk c
-                                // writes record unit_base[item] + c: no shared counter)
+  const uint32_t *unit_base;    // first unit of each item (prefix of its units): index of its
+                                // units' pending counters and trace records
   Bucket *bk;                   // priority levels (scheduler_kernel_swp), else null
   uint32_t nbuckets;
   uint32_t nready;              // U0: initially ready units (queue[0, U0))

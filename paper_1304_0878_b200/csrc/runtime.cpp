@@ -835,7 +835,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
   // Pass A (per range): units, initially ready units, successors, factors
   // (a SCAL item whose factor list equals the previous item's reuses it).
   struct RangeAcc {
-    uint64_t units = 0, ready = 0, succ = 0, fac = 0, esc = 0;
+    uint64_t units = 0, ready = 0, succ = 0, fac = 0, esc = 0, needc = 0;
     uint64_t wlo = ~0ull, whi = 0, alo = ~0ull, ahi = 0;   // written / all operand byte ranges
   };
   std::vector<RangeAcc> acc(P);
@@ -847,9 +847,10 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
     const HItem *prev = nullptr;
     for (size_t i = lo; i < hi; ++i) {
       const HItem &it = B.items[i];
-      const uint64_t nc = (it.n + CE - 1) / CE;
+      const uint64_t nc = it.n <= CE ? 1 : (it.n + CE - 1) / CE;   // (no division for small items)
       a.units += nc;
       if (it.npred == 0) a.ready += nc;
+      if (nc > 1 && it.npred > 1) a.needc = 1;
       a.succ += it.nsucc + (it.nsucc >= K_NSUCC_ESC ? 1u : 0u);   // an escaped count precedes its list
       a.esc += it.nsucc >= K_NSUCC_ESC;
       const uint64_t bytes = 4 * it.n;
@@ -910,6 +911,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
     tot.ready += acc[p].ready;
     tot.succ += acc[p].succ;
     tot.esc += acc[p].esc;
+    tot.needc |= acc[p].needc;
     tot.fac += acc[p].fac;
     tot.wlo = std::min(tot.wlo, acc[p].wlo);
     tot.whi = std::max(tot.whi, acc[p].whi);
@@ -960,15 +962,19 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
                                                           : kMaxBuckets;
   const int NB = !dr && E > 0 && (kernel == 0 || kernel == 3) && !sub && !traced && (rt->cfg.flags & BT_FLAG_PRIORITY)
                      ? prio_levels : 0;
-  // device layout: ctr | items | pending | succ | factors | unit_base[N] (traced) | buckets[NB] | queue[U] |
+  // device layout: ctr | items | pending[N] | (cpending[U]) | succ | factors | unit_base[N] | buckets[NB] | queue[U] |
   // chunk_done[N] | trace
   const size_t o_ctr = 0;
   const size_t o_items = 64;
   const size_t o_pend = align_up(o_items + sizeof(DItem) * N, 16);
-  const size_t o_succ = align_up(o_pend + 4 * N, 16);
+  const size_t o_cpend = align_up(o_pend + 4 * N, 16);   // per unit, only if some item needs it (chunk-wise)
+  const size_t o_succ = align_up(o_cpend + (tot.needc ? 4 * U : 0), 16);
   const size_t o_fac = align_up(o_succ + 4 * SL, 16);
+  // unit_base: the index of an item's per-unit counters / trace records; not
+  // uploaded when nothing reads it (4 bytes per item: 4 MB in a 1M-item round)
+  const bool need_ubase = traced || tot.needc;
   const size_t o_ubase = align_up(o_fac + 4 * F, 16);
-  const size_t o_bk = align_up(o_ubase + (traced ? 4 * N : 0), 32);
+  const size_t o_bk = align_up(o_ubase + (need_ubase ? 4 * N : 0), 32);
   const size_t o_queue = align_up(o_bk + sizeof(Bucket) * NB, 16);
   const size_t upload = o_queue + 8 * U0;
   const size_t o_cdone = align_up(o_queue + 8 * U, 16);
@@ -1017,10 +1023,11 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
   ctr->tail = U0;
   DItem *di = reinterpret_cast<DItem *>(h + o_items);
   int32_t *pend = reinterpret_cast<int32_t *>(h + o_pend);
+  int32_t *cpend = tot.needc ? reinterpret_cast<int32_t *>(h + o_cpend) : nullptr;
   uint32_t *succ = reinterpret_cast<uint32_t *>(h + o_succ);
   float *fac = reinterpret_cast<float *>(h + o_fac);
   unsigned long long *q = reinterpret_cast<unsigned long long *>(h + o_queue);
-  uint32_t *ubase = traced ? reinterpret_cast<uint32_t *>(h + o_ubase) : nullptr;
+  uint32_t *ubase = need_ubase ? reinterpret_cast<uint32_t *>(h + o_ubase) : nullptr;
   rt->succ_off.resize(N);
 
   // Pass B (per range): fill items, counters, factors, initial ready queue.
@@ -1031,11 +1038,11 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
     uint32_t prev_fo = 0;
     for (size_t i = lo; i < hi; ++i) {
       const HItem &it = B.items[i];
-      DItem &d = di[i];
+      DItem d;   // built here, stored whole (two 16-byte stores into the upload blob)
       d.x = it.x;
       d.y = it.y;
       d.n = (uint32_t)it.n;
-      d.meta = make_meta(it.kind, it.npred == 1, it.k, it.nsucc);
+      d.meta = make_meta(it.kind, it.npred == 1, it.k, it.nsucc, it.item_deps, it.n <= CE);
       if (it.kind == K_SCAL && it.k == 1) {
         memcpy(&d.arg, B.factors(it), 4);
       } else if (it.kind == K_SCAL) {
@@ -1048,11 +1055,8 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
       } else {
         d.arg = it.arg;
       }
-      const uint64_t nc = (it.n + CE - 1) / CE;
-      if (ubase) {
-        ubase[i] = (uint32_t)ub;
-        ub += nc;
-      }
+      const uint64_t nc = it.n <= CE ? 1 : (it.n + CE - 1) / CE;   // (no division for small items)
+      if (ubase) ubase[i] = (uint32_t)ub;
       d.succ = (uint32_t)so;
       if (it.nsucc >= K_NSUCC_ESC) {   // the count in front of the list
         succ[so] = it.nsucc;
@@ -1061,6 +1065,10 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
       rt->succ_off[i] = (uint32_t)so;
       so += it.nsucc;
       pend[i] = (int32_t)it.npred;
+      if (cpend && nc > 1)   // every chunk waits for every predecessor (chunk-wise ones release it alone)
+        for (uint64_t c = 0; c < nc; ++c) cpend[ub + c] = (int32_t)it.npred;
+      ub += nc;
+      di[i] = d;
       if (it.npred == 0)
         for (uint64_t c = 0; c < nc; ++c) q[qi++] = ((unsigned long long)i << 32) | c;
     }
@@ -1148,7 +1156,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
         di[i].meta |= l << K_LEVEL_SHIFT;
         const uint32_t nci = units_of(di[i].n, CE);
         tot[l] += nci;
-        if (pend[i] == 0) rdy[l] += nci;
+        if (B.items[i].npred == 0) rdy[l] += nci;
       }
       uint64_t rb = 0, pb = 0, cur[kMaxBuckets];
       for (int l = 0; l < NB; ++l) {
@@ -1158,7 +1166,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
         pb += tot[l] - rdy[l];
       }
       for (size_t i = 0; i < N; ++i)   // the initially ready units, grouped by level
-        if (pend[i] == 0) {
+        if (B.items[i].npred == 0) {
           const uint32_t l = (di[i].meta >> K_LEVEL_SHIFT) & K_LEVEL_MASK;
           const uint32_t nci = units_of(di[i].n, CE);
           for (uint32_t c = 0; c < nci; ++c) q[cur[l]++] = ((unsigned long long)i << 32) | c;
@@ -1177,6 +1185,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
   EpochArgs a{};
   a.items = reinterpret_cast<const DItem *>(d + o_items);
   a.pending = reinterpret_cast<int32_t *>(d + o_pend);
+  a.cpending = tot.needc ? reinterpret_cast<int32_t *>(d + o_cpend) : nullptr;
   a.chunk_done = reinterpret_cast<uint32_t *>(d + o_cdone);
   a.succ = reinterpret_cast<const uint32_t *>(d + o_succ);
   a.factors = reinterpret_cast<const float *>(d + o_fac);
@@ -1185,7 +1194,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
   a.host_ctr = e.hctr_dev;
   a.trace = traced ? reinterpret_cast<unsigned long long *>(d + o_trace) : nullptr;
   a.trace_item = traced ? reinterpret_cast<uint32_t *>(d + o_trace + 32 * U) : nullptr;
-  a.unit_base = traced ? reinterpret_cast<const uint32_t *>(d + o_ubase) : nullptr;
+  a.unit_base = need_ubase ? reinterpret_cast<const uint32_t *>(d + o_ubase) : nullptr;
   a.bk = nb_used ? reinterpret_cast<Bucket *>(d + o_bk) : nullptr;
   a.nbuckets = (uint32_t)nb_used;
   a.nready = (uint32_t)U0;

@@ -465,8 +465,8 @@ __device__ __forceinline__ bool mailbox_put(const Mailbox &mb, unsigned long lon
 // Release metadata of a unit: read-only descriptors, so the release warp
 // loads them while the unit is still being computed (off the critical path).
 struct RelMeta {
-  uint32_t nchunks, nsucc, off;   // off: the successor list (or the single successor's id)
-  uint32_t s0, s0kind, s0nc;      // first successor (valid if nsucc > 0); s0kind = its meta
+  uint32_t n, nchunks, nsucc, off;   // off: the successor list (or the single successor's id)
+  uint32_t s0, s0kind, s0nc, s0n;    // first successor (valid if nsucc > 0); s0kind = its meta
   uint4 i0, i1;                   // its descriptor (DItem as 2 x 16 bytes)
   bool s0stage;                   // a continuation candidate that needs no factor list
 };
@@ -499,9 +499,10 @@ __device__ __forceinline__ RelMeta release_meta(const EpochArgs &a, uint32_t ite
     meta = ldro<NC>(&it.meta);
     succ = ldro<NC>(&it.succ);
   }
+  m.n = n;
   m.nchunks = units_of(n, a.chunk_elems);
   succ_list<NC>(a, meta >> K_NSUCC_SHIFT, succ, m.nsucc, m.off);
-  m.s0 = m.s0kind = m.s0nc = 0;
+  m.s0 = m.s0kind = m.s0nc = m.s0n = 0;
   m.s0stage = false;
   m.i0 = m.i1 = uint4{};
   if (m.nsucc) {
@@ -512,6 +513,7 @@ __device__ __forceinline__ RelMeta release_meta(const EpochArgs &a, uint32_t ite
     static_assert(offsetof(DItem, n) == 16 && offsetof(DItem, meta) == 20 && offsetof(DItem, arg) == 24,
                   "DItem layout");
     m.s0kind = m.i1.y;
+    m.s0n = m.i1.x;
     m.s0nc = units_of(m.i1.x, a.chunk_elems);
     m.s0stage = (m.s0kind & K_SINGLE_PRED) && m.s0nc == 1 &&
                 ((m.s0kind & K_MASK) != K_SCAL || ((m.s0kind >> K_K_SHIFT) & K_K_MASK) == 1);
@@ -519,43 +521,71 @@ __device__ __forceinline__ RelMeta release_meta(const EpochArgs &a, uint32_t ite
   return m;
 }
 
+// Publish units [c0, c1) of successor s (ready): the queue (or its priority
+// level) gets them after one release fence.
+__device__ __forceinline__ void publish_units(const EpochArgs &a, uint32_t s, uint32_t skind, uint32_t c0, uint32_t c1) {
+  const uint32_t nc = c1 - c0;
+  unsigned long long *qd;
+  if (a.bk) {   // priority level of the successor (device_abi.h Bucket)
+    Bucket *bk = a.bk + ((skind >> K_LEVEL_SHIFT) & K_LEVEL_MASK);
+    const unsigned long long pos = atomicAdd(&bk->tail, (unsigned long long)nc);
+    qd = a.queue + a.nready + __ldcg(&bk->pbase) + (pos - __ldcg(&bk->ready));
+  } else {
+    qd = a.queue + atomicAdd(&a.ctr->tail, (unsigned long long)nc);
+  }
+  fence_acq_rel_gpu();   // one release fence covers the nc relaxed publications
+#pragma unroll 1
+  for (uint32_t c = 0; c < nc; ++c) st_relaxed_u64(qd + c, ((unsigned long long)s << 32) | (c0 + c));
+}
+
+// Completion of unit (item, ch).  Per successor s:
+//  * chunk-wise (device_abi.h K_ITEM_DEPS; same length, the item has several
+//    chunks): chunk ch of s loses one predecessor now;
+//  * otherwise, once the item's last chunk is done, every chunk of s does.
+// A single-predecessor successor's chunks are ready at once (no counter); with
+// more predecessors the counter's acq_rel RMW both releases ours and acquires
+// theirs (the publication is a release either way: fence.acq_rel, then the
+// relaxed slot stores the consumer reads with ld.acquire).  One loop serves
+// every case -- small units are its one-iteration instance -- so that the
+// kernels, which inline this at several sites, stay small (a separate general
+// path grew the stream kernel by 70 % and cost the 1-wide chain 6 %).
 template <bool NC = true>
-__device__ __forceinline__ void release_unit(const EpochArgs &a, uint32_t item, const Mailbox &mb = Mailbox{},
+__device__ __forceinline__ void release_unit(const EpochArgs &a, unsigned long long unit, const Mailbox &mb = Mailbox{},
                                              const RelMeta *pre = nullptr) {
+  const uint32_t item = (uint32_t)(unit >> 32), ch = (uint32_t)unit;
   const RelMeta m = pre ? *pre : release_meta<NC>(a, item);
   const uint32_t nchunks = m.nchunks, nsucc = m.nsucc, off = m.off;
-  if (nchunks > 1) {
-    const unsigned c = atom_add_acq_rel(&a.chunk_done[item], 1u);
-    if (c + 1 != nchunks) {
-      atomicAdd(&a.ctr->done, 1ull);
-      return;
-    }
-  }
+  bool item_done = true;
+  if (nchunks > 1) item_done = atom_add_acq_rel(&a.chunk_done[item], 1u) + 1 == nchunks;
   for (uint32_t i = 0; i < nsucc; ++i) {
     const uint32_t s = i == 0 ? m.s0 : ldro<NC>(&a.succ[off + i]);
     const uint32_t skind = i == 0 ? m.s0kind : ldro<NC>(&a.items[s].meta);
-    // a single-predecessor successor is ready now (no counter); with more
-    // predecessors the acq_rel RMW both releases ours and acquires theirs
-    // (the publication below is a release either way: fence.acq_rel, then the
-    // relaxed slot stores the consumer reads with ld.acquire)
-    const bool ready = (skind & K_SINGLE_PRED)
-                           ? true
-                           : atom_add_acq_rel(reinterpret_cast<unsigned *>(&a.pending[s]), 0xFFFFFFFFu) == 1u;
-    if (ready) {
-      const uint32_t nc = i == 0 ? m.s0nc : units_of(ldro<NC>(&a.items[s].n), a.chunk_elems);
-      if (nc == 1 && mailbox_put(mb, (unsigned long long)s << 32, i == 0 && m.s0stage, m.i0, m.i1))
-        continue;   // run it here
-      unsigned long long *qd;
-      if (a.bk) {   // priority level of the successor (device_abi.h Bucket)
-        Bucket *bk = a.bk + ((skind >> K_LEVEL_SHIFT) & K_LEVEL_MASK);
-        const unsigned long long pos = atomicAdd(&bk->tail, (unsigned long long)nc);
-        qd = a.queue + a.nready + __ldcg(&bk->pbase) + (pos - __ldcg(&bk->ready));
-      } else {
-        qd = a.queue + atomicAdd(&a.ctr->tail, (unsigned long long)nc);
+    // units [c0, c1) of s lose this predecessor; cnt + c: their counters
+    uint32_t c0 = 0, c1 = 1;
+    int32_t *cnt = a.pending + s;
+    if (nchunks > 1 || !(skind & K_ONE_UNIT)) {
+      const uint32_t sn = i == 0 ? m.s0n : ldro<NC>(&a.items[s].n);
+      const bool chunkwise = nchunks > 1 && !(skind & (K_ONE_UNIT | K_ITEM_DEPS)) && sn == m.n;
+      if (chunkwise) {
+        c0 = ch;
+        c1 = ch + 1;
+      } else if (!item_done) {
+        continue;
+      } else if (!(skind & K_ONE_UNIT)) {
+        c1 = units_of(sn, a.chunk_elems);
       }
-      fence_acq_rel_gpu();   // one release fence covers the nc relaxed publications
-#pragma unroll 1
-      for (uint32_t c = 0; c < nc; ++c) st_relaxed_u64(qd + c, ((unsigned long long)s << 32) | c);
+      if (!(skind & (K_ONE_UNIT | K_SINGLE_PRED))) cnt = a.cpending + ldro<NC>(&a.unit_base[s]);
+    }
+    // a single ready unit may run on this CTA next (the mailbox: its tile is
+    // in L2); a whole single-unit successor travels with its descriptor
+    const bool one = c1 - c0 == 1;
+    for (uint32_t c = c0; c < c1; ++c) {
+      if (!(skind & K_SINGLE_PRED) && atom_add_acq_rel(reinterpret_cast<unsigned *>(cnt + c), 0xFFFFFFFFu) != 1u)
+        continue;
+      if (one && mailbox_put(mb, ((unsigned long long)s << 32) | c, i == 0 && m.s0stage, m.i0, m.i1)) continue;
+      const uint32_t e = (skind & K_SINGLE_PRED) ? c1 : c + 1;   // no counters: all at once
+      publish_units(a, s, skind, c, e);
+      c = e - 1;
     }
   }
   atomicAdd(&a.ctr->done, 1ull);
@@ -621,7 +651,7 @@ struct SlotState {
 template <bool NC = true>
 __device__ __forceinline__ void finish_slot(const EpochArgs &a, SlotState &s) {
   const long long c1 = a.trace ? clock64() : 0;
-  release_unit<NC>(a, (uint32_t)(s.unit >> 32));
+  release_unit<NC>(a, s.unit);
   s.unreleased = false;
   if (a.trace) {
     const long long c2 = clock64();
@@ -1187,7 +1217,7 @@ __global__ void __launch_bounds__(kBlock, BT_MIN_CTAS) scheduler_kernel_rw(Epoch
         const int b = (int)(v % kSlots);
         const unsigned long long unit = s_final[b];   // the popped unit, or the end of an in-slot chain
         const long long c1 = a.trace ? clock64() : 0;
-        release_unit(a, (uint32_t)(unit >> 32), Mailbox{&s_mb_unit, &s_mb_state, s_mb_item, &s_mb_staged, &s_mb_bar},
+        release_unit(a, unit, Mailbox{&s_mb_unit, &s_mb_state, s_mb_item, &s_mb_staged, &s_mb_bar},
                      lane == 0 && unit == s_unit[b] ? &pre : nullptr);
         if (a.trace) {
           // the unit's own record (item's first record + chunk): no shared
@@ -1758,38 +1788,49 @@ constexpr int kBlockWQ = 256, kWarpsWQ = kBlockWQ / 32;
 constexpr unsigned kTicketBlock = BT_TICKET_BLOCK;   // queue positions per RMW on ctr->head
 constexpr unsigned kDoneBatch = 16;                  // completions per RMW on ctr->done
 
-// Release of one finished unit by its warp's lane 0; returns a ready
-// single-unit successor for this warp to run next, or kStop.
-// s0kind / s0nc: the single successor's kind and nchunks when prefetched
-// (nsucc == 1), else ignored.  The unit's completion is counted by the caller.
-__device__ __forceinline__ unsigned long long release_wq(const EpochArgs &a, uint32_t item, const DItem &it,
-                                                         uint32_t s0kind, uint32_t s0nc, bool pre) {
+// Release of one finished unit (item, ch) by its warp's lane 0 (the cases of
+// release_unit, in one loop as there); returns a ready unit for this warp to
+// run next, or kStop.  s0kind: the single successor's meta when prefetched
+// (pre: this item and its only successor are single units), else ignored.
+// The unit's completion is counted by the caller.
+__device__ __forceinline__ unsigned long long release_wq(const EpochArgs &a, uint32_t item, uint32_t ch, const DItem &it,
+                                                         uint32_t s0kind, bool pre) {
   const uint32_t nchunks = units_of(it.n, a.chunk_elems);
-  if (nchunks > 1) {
-    const unsigned c = atom_add_acq_rel(&a.chunk_done[item], 1u);
-    if (c + 1 != nchunks) return kStop;
-  }
+  bool item_done = true;
+  if (nchunks > 1) item_done = atom_add_acq_rel(&a.chunk_done[item], 1u) + 1 == nchunks;
   unsigned long long cont = kStop;
   uint32_t nsucc, off;
   succ_list<true>(a, it.nsucc_field(), it.succ, nsucc, off);
   for (uint32_t i = 0; i < nsucc; ++i) {
     const uint32_t s = nsucc == 1 ? off : __ldg(&a.succ[off + i]);   // single successor inline
     const uint32_t skind = pre ? s0kind : __ldg(&a.items[s].meta);
-    // a single-predecessor successor is ready now; with more predecessors
-    // the acq_rel RMW both releases ours and acquires theirs
-    const bool ready = (skind & K_SINGLE_PRED)
-                           ? true
-                           : atom_add_acq_rel(reinterpret_cast<unsigned *>(&a.pending[s]), 0xFFFFFFFFu) == 1u;
-    if (!ready) continue;
-    const uint32_t nc = pre ? s0nc : units_of(__ldg(&a.items[s].n), a.chunk_elems);
-    if (cont == kStop && nc == 1) {   // run it here next
-      cont = (unsigned long long)s << 32;
-      continue;
+    uint32_t c0 = 0, c1 = 1;   // units [c0, c1) of s lose this predecessor
+    int32_t *cnt = a.pending + s;
+    if (nchunks > 1 || !(skind & K_ONE_UNIT)) {
+      const uint32_t sn = __ldg(&a.items[s].n);
+      const bool chunkwise = nchunks > 1 && !(skind & (K_ONE_UNIT | K_ITEM_DEPS)) && sn == it.n;
+      if (chunkwise) {
+        c0 = ch;
+        c1 = ch + 1;
+      } else if (!item_done) {
+        continue;
+      } else if (!(skind & K_ONE_UNIT)) {
+        c1 = units_of(sn, a.chunk_elems);
+      }
+      if (!(skind & (K_ONE_UNIT | K_SINGLE_PRED))) cnt = a.cpending + __ldg(&a.unit_base[s]);
     }
-    const unsigned long long pos = atomicAdd(&a.ctr->tail, (unsigned long long)nc);
-    fence_acq_rel_gpu();   // one release fence covers the nc relaxed publications
-#pragma unroll 1
-    for (uint32_t c = 0; c < nc; ++c) st_relaxed_u64(&a.queue[pos + c], ((unsigned long long)s << 32) | c);
+    const bool one = c1 - c0 == 1;   // a single ready unit: this warp may run it next
+    for (uint32_t c = c0; c < c1; ++c) {
+      if (!(skind & K_SINGLE_PRED) && atom_add_acq_rel(reinterpret_cast<unsigned *>(cnt + c), 0xFFFFFFFFu) != 1u)
+        continue;
+      if (one && cont == kStop) {   // run it here next
+        cont = ((unsigned long long)s << 32) | c;
+        continue;
+      }
+      const uint32_t e = (skind & K_SINGLE_PRED) ? c1 : c + 1;   // no counters: all at once
+      publish_units(a, s, skind, c, e);
+      c = e - 1;
+    }
   }
   return cont;
 }
@@ -1909,9 +1950,8 @@ __global__ void __launch_bounds__(kBlockWQ, BT_WQ_MIN_CTAS) scheduler_kernel_wq(
     __syncwarp();
     if (a.trace) c2 = clock64();
     const uint32_t s0kind = __shfl_sync(0xffffffffu, nd.y, 1);                          // word 1: n, meta, arg, succ
-    const uint32_t s0nc = units_of(__shfl_sync(0xffffffffu, nd.x, 1), a.chunk_elems);
     if (lane == 0) {
-      cont = release_wq(a, item, it, s0kind, s0nc, pre);
+      cont = release_wq(a, item, chunk, it, s0kind, pre);
       chained |= cont != kStop;
       if (++ndone == kDoneBatch) {
         atomicAdd(&a.ctr->done, (unsigned long long)ndone);

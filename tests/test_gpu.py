@@ -241,6 +241,83 @@ def test_priority_ready_queue(B, chunk_bytes):
     assert n_prio >= 15
 
 
+def _segment(bufs, nparts, rows):
+    """Oracle run of one segment (fixed partitioning) on the current contents."""
+    t = W._tasks(len(rows))
+    for i, r in enumerate(rows):
+        t[i] = r
+    return oracle.run(W.Program([b.copy() for b in bufs], list(nparts), t))
+
+
+@pytest.mark.parametrize("kernel", ["sw", "rw", "wq"])
+@pytest.mark.parametrize("fusion", [True, False])
+@pytest.mark.parametrize("chunk_bytes", [0, 256])
+def test_chunkwise_release(B, kernel, fusion, chunk_bytes):
+    """Chunk-wise release (device_abi.h K_ITEM_DEPS) in one epoch: items of
+    many chunks after a same-length predecessor on the same handle (chunk c
+    waits for chunk c only), with several predecessors (per-unit counters),
+    and after predecessors inherited through a partition / unpartition /
+    re-partition inside the epoch (other handles: whole-item release), per
+    scheduler variant, one wait at the end; against the oracle run segment by
+    segment (sequential composition)."""
+    import torch
+    rng = np.random.default_rng(W.SEED_BASE + 131)
+    n = 10_003                                   # ragged: 157 chunks of 64 floats at chunk_bytes 256
+    bufs = [W.unit_interval_floats(rng, n) for _ in range(3)]
+    X, Y, Z = 0, 1, 2
+    S, A, C = W.SCAL, W.AXPY, W.COPY
+    seg1 = [(S, 1.5, X, -1, -1, -1), (A, 0.25, X, -1, Y, -1), (C, 0, Y, -1, Z, -1), (S, -0.75, Y, -1, -1, -1),
+            (A, 0.5, Z, -1, X, -1), (S, 1.25, X, -1, -1, -1)]
+    seg2 = [(A, 0.125, X, 0, Y, 0), (S, -1.5, X, 1, -1, -1), (C, 0, Y, 2, X, 2), (A, -0.25, X, 1, Y, 1),
+            (S, 0.75, Z, 0, -1, -1), (S, 1.125, Y, 0, -1, -1)]
+    seg3 = [(A, 0.375, Y, -1, X, -1), (S, 2.0, X, -1, -1, -1), (A, -0.5, X, -1, Z, -1), (C, 0, Z, -1, Y, -1)]
+    seg4 = [(S, 0.5, X, 0, -1, -1), (S, -1.25, X, 2, -1, -1), (A, 0.25, Z, 0, Y, 0)]
+    seg5 = [(A, 1.5, X, -1, Y, -1), (S, 0.625, Y, -1, -1, -1)]
+    parts2, parts4 = [3, 3, 1], [3, 1, 1]
+    exp = _segment(bufs, [0, 0, 0], seg1)
+    exp = _segment(exp, parts2, seg2)
+    exp = _segment(exp, [0, 0, 0], seg3)
+    exp = _segment(exp, parts4, seg4)
+    exp = _segment(exp, [0, 0, 0], seg5)
+    flags = (0 if fusion else B.BT_FLAG_NO_FUSION) | KERNELS[kernel]
+    tensors = [torch.from_numpy(b.copy()).cuda() for b in bufs]
+    with B.Runtime(flags=flags, chunk_bytes=chunk_bytes) as rt:
+        hs = [rt.register_tensor(t) for t in tensors]
+
+        def submit(rows, views):
+            for c, f, b0, t0, b1, t1 in rows:
+                h0 = views[b0][t0] if t0 >= 0 else hs[b0]
+                if c == S:
+                    rt.scal(h0, f)
+                    continue
+                h1 = views[b1][t1] if t1 >= 0 else hs[b1]
+                if c == A:
+                    rt.axpy(f, h0, h1)
+                else:
+                    rt.copy(h0, h1)
+
+        def partition(nparts):
+            return [rt.partition(h, k) for h, k in zip(hs, nparts)]
+
+        submit(seg1, None)
+        submit(seg2, partition(parts2))
+        for h in hs:
+            rt.unpartition(h)
+        submit(seg3, None)
+        submit(seg4, partition(parts4))
+        for h in hs:
+            rt.unpartition(h)
+        submit(seg5, None)
+        rt.wait()
+        st = rt.stats()
+        for h in hs:
+            rt.unregister(h)
+    torch.cuda.synchronize()
+    assert st["tasks_submitted"] == len(seg1 + seg2 + seg3 + seg4 + seg5) and st["epochs"] == 1, st
+    for b in range(3):
+        assert_bits_equal(tensors[b].cpu().numpy(), exp[b], f"buffer {b}")
+
+
 def test_c3_reduced(B):
     p = W.c3_random_dag(nbuf=64, nx=1 << 12, ntasks=10000)
     stats = compare_program(p, chunk_bytes=4096)
