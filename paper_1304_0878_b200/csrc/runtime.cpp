@@ -835,7 +835,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
   // Pass A (per range): units, initially ready units, successors, factors
   // (a SCAL item whose factor list equals the previous item's reuses it).
   struct RangeAcc {
-    uint64_t units = 0, ready = 0, succ = 0, fac = 0, esc = 0, needc = 0;
+    uint64_t units = 0, ready = 0, succ = 0, fac = 0, esc = 0, needc = 0, single = 0;
     uint64_t wlo = ~0ull, whi = 0, alo = ~0ull, ahi = 0;   // written / all operand byte ranges
   };
   std::vector<RangeAcc> acc(P);
@@ -851,6 +851,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
       a.units += nc;
       if (it.npred == 0) a.ready += nc;
       if (nc > 1 && it.npred > 1) a.needc = 1;
+      a.single += it.npred == 1;
       a.succ += it.nsucc + (it.nsucc >= K_NSUCC_ESC ? 1u : 0u);   // an escaped count precedes its list
       a.esc += it.nsucc >= K_NSUCC_ESC;
       const uint64_t bytes = 4 * it.n;
@@ -912,6 +913,7 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
     tot.succ += acc[p].succ;
     tot.esc += acc[p].esc;
     tot.needc |= acc[p].needc;
+    tot.single += acc[p].single;
     tot.fac += acc[p].fac;
     tot.wlo = std::min(tot.wlo, acc[p].wlo);
     tot.whi = std::max(tot.whi, acc[p].whi);
@@ -939,6 +941,22 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
   // use the instance whose bodies prefetch the next step's data
   const bool prefetch = avg_work < kPrefetchBelowK * avg_elems;
   int kernel = avg_elems <= kWarpUnitMax ? (wide && rt->grid_wq > 0 ? 2 : 1) : prefetch ? 3 : 0;
+  if (E > 0 && !dr) {
+    // DAG epochs (tools/kernel_matrix.py, profiles/r02_kernel_matrix.jsonl).
+    // Mostly chains (most items have a single predecessor): "rw" for small
+    // units, which it runs in its slots (3-5x faster than "sw" at 1 to 256
+    // chains of 4 KiB), else "sw" (256 KiB chains: equal; C2 unfused, 1,024
+    // initially ready units: 0.25 vs 0.28 ms).  Other DAGs: "rw" when every
+    // slot of every CTA has a unit from the start (C3 with 4 MiB buffers,
+    // 1,792 initially ready units: 12.6 vs 13.5 ms; a 100k-task DAG of 4 KiB
+    // buffers: 1.20 vs 1.36 ms, "wq" 2.1), else "sw" (C3 with 4 KiB - 1 MiB
+    // buffers, ~30 initially ready, 15 % single-predecessor items: 3.25 vs
+    // 4.3 ms at 16 KiB -- "rw" holds up to four ready units per CTA while
+    // other CTAs idle)
+    const bool chains = tot.single * 2 >= N;
+    const bool rw = chains ? avg_elems <= kWarpUnitMax : U0 >= 2ull * (uint64_t)rt->grid_max;
+    kernel = rw ? 1 : prefetch ? 3 : 0;
+  }
   if (kv) kernel = kv[0] == 'w' ? 2 : kv[0] == 'r' ? 1 : prefetch ? 3 : 0;
   if (rt->cfg.flags & BT_FLAG_KERNEL_SW) kernel = prefetch ? 3 : 0;
   if (rt->cfg.flags & BT_FLAG_KERNEL_RW) kernel = 1;
