@@ -2,7 +2,9 @@
 how many CTAs run a unit body over time, i.e. whether C3 is starved of ready
 work (DAG-bound) or runs every CTA and is bound by the bodies.
 
-    python tools/c3_timeline.py [--levels-off]
+    python tools/c3_timeline.py [sw|rw|auto]
+
+(tracing turns the local continuations off: an approximation of the untraced run)
 """
 import json
 import os
@@ -20,7 +22,9 @@ from paper_1304_0878_b200 import btask as B  # noqa: E402
 import bench_configs as bc  # noqa: E402
 
 p = W.c3_random_dag()
-r, tr = bc._run(torch, B, p, 1, flags=B.BT_FLAG_TIMESTAMPS | B.BT_FLAG_KERNEL_SW)
+kern = sys.argv[1] if len(sys.argv) > 1 else "auto"
+kf = {"sw": B.BT_FLAG_KERNEL_SW, "rw": B.BT_FLAG_KERNEL_RW, "auto": 0}[kern]
+r, tr = bc._run(torch, B, p, 1, flags=B.BT_FLAG_TIMESTAMPS | kf)
 t, item = tr
 mhz = 1965.0
 start = t[:, 0] + t[:, 1] * 1e3 / mhz            # body start (ns)
@@ -35,7 +39,13 @@ hist = {}
 for lo, hi in [(0, 100), (100, 200), (200, 300), (300, 400), (400, 445)]:
     sel = (conc >= lo) & (conc < hi)
     hist[f"{lo}-{hi}"] = float(dt[sel].sum() / total)
-out = {"device_ms": r["device_span_ms"], "units": int(t.shape[0]), "span_ms": total / 1e6,
+# concurrency over the run in 20 slices (is the start, the middle or the tail starved?)
+edges = np.linspace(0, total, 21)
+sl = []
+for a0, a1 in zip(edges[:-1], edges[1:]):
+    seg = (ev[:, 0] >= a0) & (ev[:, 0] < a1)
+    sl.append(round(float((conc[seg] * dt[seg]).sum() / max(1.0, dt[seg].sum())), 1))
+out = {"kernel": kern, "concurrency_by_twentieth": sl, "device_ms": r["device_span_ms"], "units": int(t.shape[0]), "span_ms": total / 1e6,
        "mean_concurrent_bodies": float((conc * dt).sum() / total), "time_fraction_by_concurrency": hist,
        "body_us_median": float(np.median(t[:, 2]) / mhz), "pop_us_median": float(np.median(t[:, 1]) / mhz),
        "release_us_median": float(np.median(t[:, 3]) / mhz)}
