@@ -91,9 +91,11 @@ struct HItem {
   uint32_t npred;
   uint32_t nsucc;      // updated atomically by lanes for shared predecessors
   uint32_t stamp : 31; // dedupe marker (sequential path; item ids < 2^31)
-  // 1: some predecessor reached this item through ANOTHER (sub)handle (a
-  // partition's parent / parts): its element ranges may not line up with this
-  // item's, so every predecessor counts as a whole (no chunk-wise release)
+  // 1: some predecessor's operand on the (sub)handle it was found through has
+  // another base address than this item's operand there (partition-inherited
+  // state: a parent, parts, or a reused slot): its chunks need not line up
+  // with this item's, so every predecessor counts as a whole (no chunk-wise
+  // release)
   uint32_t item_deps : 1;
 };
 
@@ -320,13 +322,18 @@ class Builder {
   }
 
   // The predecessors in the state of (sub)handle `slot`, which item t accesses.
-  // A predecessor that accessed the same slot touched the same elements at
-  // the same offsets (chunk c of both covers the same elements); one found
-  // through partition-inherited state did not (item_deps).
+  // A predecessor with an operand at the same base address as t's operand on
+  // `slot` touched, in its chunk c, exactly the elements t's chunk c touches
+  // there (equal lengths are checked on the device); any other -- found
+  // through partition-inherited state, or on a slot id reused within the
+  // epoch by another part -- makes t wait for whole predecessors (item_deps).
+  // Base addresses, not slot ids: a freed slot range is reused by the next
+  // partition with as many parts, possibly of another parent.
   void collect(DepState &st, uint32_t t, uint32_t mode, uint32_t slot) {
+    const uint64_t base = slot == items[t].slot0 ? items[t].x : items[t].y;
     auto add = [&](uint32_t p) {
       const HItem &pi = items[p];
-      if (pi.slot0 != slot && pi.slot1 != slot) items[t].item_deps = 1;
+      if (pi.x != base && pi.y != base) items[t].item_deps = 1;
       edge(p, t);
     };
     if (st.writer != NONE) add(st.writer);
@@ -495,8 +502,8 @@ void Builder::lane_runs(Lane &L, const LaneEntry *const *chunks, const uint32_t 
       auto link = [&](uint32_t p) {
         if (p & TAG) ++L.items[p & ~TAG].nsucc;
         else __atomic_fetch_add(&items[p].nsucc, 1u, __ATOMIC_RELAXED);
-        // (a global predecessor through another slot: partition-inherited state)
-        if (!(p & TAG) && items[p].slot0 != s && items[p].slot1 != s) L.items[local].item_deps = 1;
+        // (a global predecessor whose operand has another base: as collect())
+        if (!(p & TAG) && items[p].x != g.first && items[p].y != g.first) L.items[local].item_deps = 1;
         L.edges.push_back(((uint64_t)p << 32) | t);
         ++np;
       };
