@@ -106,6 +106,73 @@ __global__ void __launch_bounds__(kThreads) run_jobs_pf(const Job *jobs, uint32_
   }
 }
 
+// The same with the operands staged through shared memory by cp.async
+// (LDGSTS: no registers hold the bytes in flight): NS stages of SB float4 per
+// operand, NS-1 stages in flight while one is consumed.
+__device__ __forceinline__ void cp16(void *smem, const void *g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int NS, int SB>   // SB float4 per stage and operand (multiple of kThreads)
+__global__ void __launch_bounds__(kThreads) run_jobs_cp(const Job *jobs, uint32_t njobs, float *const *bufs,
+                                                        unsigned *next) {
+  extern __shared__ float4 sm[];   // [NS][2][SB]
+  __shared__ uint32_t s_j;
+  constexpr int n4 = kChunk / 4, nst = n4 / SB, per = SB / kThreads;
+  for (;;) {
+    if (threadIdx.x == 0) s_j = atomicAdd(next, 1u);
+    __syncthreads();
+    const uint32_t j = s_j;
+    __syncthreads();
+    if (j >= njobs) return;
+    const Job jb = jobs[j];
+    const float4 *x = reinterpret_cast<const float4 *>(bufs[jb.x] + (size_t)jb.chunk * kChunk);
+    float4 *y = reinterpret_cast<float4 *>(bufs[jb.y] + (size_t)jb.chunk * kChunk);
+    const bool two = jb.kind == 2;
+    auto issue = [&](int st) {
+      float4 *bx = sm + (size_t)(st % NS) * 2 * SB, *by = bx + SB;
+#pragma unroll
+      for (int q = 0; q < per; ++q) {
+        const int i = st * SB + q * kThreads + threadIdx.x;
+        cp16(bx + q * kThreads + threadIdx.x, x + i);
+        if (two) cp16(by + q * kThreads + threadIdx.x, y + i);
+      }
+    };
+#pragma unroll
+    for (int st = 0; st < NS - 1; ++st) {
+      if (st < nst) issue(st);
+      cp_commit();
+    }
+    for (int st = 0; st < nst; ++st) {
+      if (st + NS - 1 < nst) issue(st + NS - 1);
+      cp_commit();
+      cp_wait<NS - 1>();   // stage st has landed (each thread reads only what it copied)
+      const float4 *bx = sm + (size_t)(st % NS) * 2 * SB, *by = bx + SB;
+#pragma unroll
+      for (int q = 0; q < per; ++q) {
+        const int k = q * kThreads + threadIdx.x, i = st * SB + k;
+        float4 v = bx[k];
+        if (jb.kind == 1) {
+          v.x = __fmul_rn(v.x, jb.a); v.y = __fmul_rn(v.y, jb.a); v.z = __fmul_rn(v.z, jb.a); v.w = __fmul_rn(v.w, jb.a);
+          __stcg(y + i, v);
+        } else if (two) {
+          float4 w = by[k];
+          w.x = __fadd_rn(__fmul_rn(jb.a, v.x), w.x); w.y = __fadd_rn(__fmul_rn(jb.a, v.y), w.y);
+          w.z = __fadd_rn(__fmul_rn(jb.a, v.z), w.z); w.w = __fadd_rn(__fmul_rn(jb.a, v.w), w.w);
+          __stcg(y + i, w);
+        } else {
+          __stcg(y + i, v);
+        }
+      }
+    }
+    cp_wait<0>();
+  }
+}
+
 // read-only L2 eviction (a written scratch would leave dirty lines behind)
 __global__ void touch(const float4 *p, size_t n4, float *out) {
   float s = 0.f;
@@ -175,6 +242,35 @@ int main(int argc, char **argv) {
            "\"algorithmic_GBps\":%.1f}\n",
            argv[1], njobs, grid_mul, grid, med, bytes / med / 1e6);
   }
+  auto run_cp = [&](auto kern, int ns, int sb, int grid_mul) -> int {
+    const size_t smem = (size_t)ns * 2 * sb * 16;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ2 = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, kern, kThreads, smem));
+    const int gm = std::min(grid_mul, occ2);
+    std::vector<float> ms;
+    for (int r = 0; r < reps + 1; ++r) {
+      touch<<<sms * 4, 256>>>(reinterpret_cast<const float4 *>(flush), ((size_t)512 << 20) / 16, flush);
+      CK(cudaMemset(next, 0, 4));
+      CK(cudaEventRecord(e0));
+      kern<<<sms * gm, kThreads, smem>>>(dj, njobs, db, next);
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float t;
+      CK(cudaEventElapsedTime(&t, e0, e1));
+      if (r) ms.push_back(t);
+    }
+    std::sort(ms.begin(), ms.end());
+    const float med = ms[ms.size() / 2];
+    printf("{\"probe\":\"c3_jobs_no_deps_cp_async\",\"file\":\"%s\",\"stages\":%d,\"stage_bytes_per_operand\":%d,"
+           "\"ctas_per_sm\":%d,\"ms\":%.3f,\"algorithmic_GBps\":%.1f}\n",
+           argv[1], ns, sb * 16, gm, med, bytes / med / 1e6);
+    return 0;
+  };
+  run_cp(run_jobs_cp<4, 512>, 4, 512, 3);     // 4 x 8 KiB per operand: 64 KiB per CTA
+  run_cp(run_jobs_cp<3, 1024>, 3, 1024, 3);   // 3 x 16 KiB: 96 KiB (2 CTAs/SM fit)
+  run_cp(run_jobs_cp<8, 256>, 8, 256, 3);     // 8 x 4 KiB: 64 KiB
+  run_cp(run_jobs_cp<4, 256>, 4, 256, 3);     // 4 x 4 KiB: 32 KiB
   for (int grid_mul : {3, 2}) {
     for (int pf : {16384, 65536}) {
       const int grid = sms * grid_mul;
