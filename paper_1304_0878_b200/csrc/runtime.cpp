@@ -935,28 +935,25 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
   // a 1-wide dependency chain) is latency-bound, and the CTA-wide "rw" kernel
   // runs chains in its slots with the shortest dependency latency
   const bool wide = U0 * 4 >= (uint64_t)rt->grid_wq * 8;
-  // units above 16 KiB: CTA-wide bodies with one scheduler warp ("sw"; C3
-  // with 64 KiB units: 14.1 ms vs 14.7 ms on "rw", tools/c3_chunks.py); epochs
-  // of short chains (average k below the FP32/HBM ridge) are HBM-bound and
-  // use the instance whose bodies prefetch the next step's data
+  // units above 16 KiB: CTA-wide bodies with one scheduler warp ("sw"; DAG
+  // epochs: the rule below); epochs of short chains (average k below the
+  // FP32/HBM ridge) are HBM-bound and use the instance whose bodies prefetch
+  // the next step's data
   const bool prefetch = avg_work < kPrefetchBelowK * avg_elems;
   int kernel = avg_elems <= kWarpUnitMax ? (wide && rt->grid_wq > 0 ? 2 : 1) : prefetch ? 3 : 0;
-  if (E > 0 && !dr) {
-    // DAG epochs (tools/kernel_matrix.py, profiles/r02_kernel_matrix.jsonl).
-    // Mostly chains (most items have a single predecessor): "rw" for small
-    // units, which it runs in its slots (3-5x faster than "sw" at 1 to 256
-    // chains of 4 KiB), else "sw" (256 KiB chains: equal; C2 unfused, 1,024
-    // initially ready units: 0.25 vs 0.28 ms).  Other DAGs: "rw" when every
-    // slot of every CTA has a unit from the start (C3 with 4 MiB buffers,
-    // 1,792 initially ready units: 12.6 vs 13.5 ms; a 100k-task DAG of 4 KiB
-    // buffers: 1.20 vs 1.36 ms, "wq" 2.1), else "sw" (C3 with 4 KiB - 1 MiB
-    // buffers, ~30 initially ready, 15 % single-predecessor items: 3.25 vs
-    // 4.3 ms at 16 KiB -- "rw" holds up to four ready units per CTA while
-    // other CTAs idle)
-    const bool chains = tot.single * 2 >= N;
-    const bool rw = chains ? avg_elems <= kWarpUnitMax : U0 >= 2ull * (uint64_t)rt->grid_max;
-    kernel = rw ? 1 : prefetch ? 3 : 0;
-  }
+  // DAG epochs other than chains (fewer than half the items have a single
+  // predecessor; tools/kernel_matrix.py, profiles/r02_kernel_matrix.jsonl):
+  // "rw" when every slot of every CTA has a unit from the start (C3 with 4 MiB
+  // buffers, 1,792 initially ready units: 12.6 vs 13.5 ms on "sw"; a 100k-task
+  // DAG of 4 KiB buffers: 1.20 vs 1.36 ms, "wq" 2.1), else "sw" at any unit
+  // size (C3 with 4 KiB - 1 MiB buffers, ~30 initially ready, 15 %
+  // single-predecessor items: 3.25 vs 4.3 ms at 16 KiB -- "rw" holds up to
+  // four ready units per CTA while other CTAs idle).  Chains keep the rule
+  // above: "rw" runs narrow ones in its slots (3-5x faster than "sw" at 1 to
+  // 256 chains of 4 KiB), "wq" wide ones (C4: 1.4 vs 2.5 ms on "rw"), "sw"
+  // large units (C2 unfused: 0.25 vs 0.28 ms on "rw").
+  if (E > 0 && !dr && tot.single * 2 < N)
+    kernel = U0 >= 2ull * (uint64_t)rt->grid_max ? 1 : prefetch ? 3 : 0;
   if (kv) kernel = kv[0] == 'w' ? 2 : kv[0] == 'r' ? 1 : prefetch ? 3 : 0;
   if (rt->cfg.flags & BT_FLAG_KERNEL_SW) kernel = prefetch ? 3 : 0;
   if (rt->cfg.flags & BT_FLAG_KERNEL_RW) kernel = 1;

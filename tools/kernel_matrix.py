@@ -56,6 +56,7 @@ def cases():
     for k in (1, 2, 4, 8, 16, 32, 64, 256):
         for n in (1024, 65536):
             yield f"{k} chains n={n}", k_chains(k, n, 8192 // k if k < 256 else 64), 0
+    yield "4096 chains n=1024 (wide)", k_chains(4096, 1024, 16), 0
     if os.environ.get("KM_RUNS"):   # pipelined SCAL runs (the first round's choice holds for the run)
         p = W.c4_fine()
         yield "C4 unfused", p, B.BT_FLAG_NO_FUSION
