@@ -82,8 +82,10 @@ _SIGS = {
     "bt_comm_init": (_c.c_int, [_c.c_void_p, _c.c_char_p]),
     "bt_insert_task": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_void_p, _c.c_size_t, _P(bt_handle), _P(_c.c_int),
                                    _c.c_uint]),
-    "bt_insert_task_batch": (_c.c_int, [_c.c_void_p, _c.c_size_t, _P(_c.c_int32), _P(_c.c_float), _P(bt_handle),
-                                         _P(bt_handle), _P(_c.c_size_t)]),
+    # (const int32_t *codelets, const float *scalars, const bt_handle *h0, const bt_handle *h1):
+    # raw addresses, so a call marshals four integers (ndarray.ctypes.data_as costs ~3 us each)
+    "bt_insert_task_batch": (_c.c_int, [_c.c_void_p, _c.c_size_t, _c.c_void_p, _c.c_void_p, _c.c_void_p,
+                                         _c.c_void_p, _P(_c.c_size_t)]),
     "bt_flush": (_c.c_int, [_c.c_void_p]),
     "bt_task_wait_for_all": (_c.c_int, [_c.c_void_p]),
     "bt_data_acquire": (_c.c_int, [_c.c_void_p, bt_handle, _c.c_int]),
@@ -234,10 +236,11 @@ class Runtime:
         s = np.ascontiguousarray(scalars, np.float32)
         a0 = np.ascontiguousarray(h0, np.uint64)
         a1 = None if h1 is None else np.ascontiguousarray(h1, np.uint64)
+        if not (c.shape[0] == s.shape[0] == a0.shape[0] and (a1 is None or a1.shape[0] == c.shape[0])):
+            raise ValueError("insert_batch: arrays of different lengths")
         n = ctypes.c_size_t()
-        rc = bt_insert_task_batch(self.rt, c.shape[0], c.ctypes.data_as(_P(ctypes.c_int32)),
-                                  s.ctypes.data_as(_P(ctypes.c_float)), _u64p(a0),
-                                  None if a1 is None else _u64p(a1), ctypes.byref(n))
+        rc = bt_insert_task_batch(self.rt, c.shape[0], c.ctypes.data, s.ctypes.data, a0.ctypes.data,
+                                  None if a1 is None else a1.ctypes.data, ctypes.byref(n))
         self._check(rc, f"bt_insert_task_batch (accepted {n.value})")
         return n.value
 
