@@ -53,9 +53,9 @@
 extern "C" {
 #endif
 
-#define BT_ABI_VERSION 4   /* 2: bt_stats.kernel_launches, BT_FLAG_KERNEL_*; 3: bt_stats.sched_launches,
+#define BT_ABI_VERSION 5   /* 2: bt_stats.kernel_launches, BT_FLAG_KERNEL_*; 3: bt_stats.sched_launches,
                                BT_FLAG_NO_STREAM; 4: bt_stats.stream_resumes, bt_stats.prio_epochs,
-                               BT_FLAG_PRIORITY, bt_debug_gate */
+                               BT_FLAG_PRIORITY, bt_debug_gate; 5: bt_dag_view.item_flags */
 
 typedef struct bt_runtime bt_runtime;
 typedef uint64_t bt_handle;
@@ -308,10 +308,18 @@ typedef struct bt_dag_view {
   const uint32_t *item_npred; /* [nitems] */
   const uint32_t *succ_off;   /* [nitems+1] CSR offsets */
   const uint32_t *succ;       /* [nedges] successor items */
+  const uint8_t *item_flags;  /* [nitems] BT_DAG_WHOLE_PREDS: some predecessor's operand on the handle it
+                                 was found through has another base address than the item's (partition-
+                                 inherited state), so the item's work units wait for whole predecessors;
+                                 otherwise unit c of an item of several units waits only for unit c of
+                                 each same-length predecessor (chunk-wise release) */
 } bt_dag_view;
+enum { BT_DAG_WHOLE_PREDS = 1 };
 
 /* Close the pending epoch WITHOUT executing it and expose its DAG (valid until
- * the next call on rt).  Only for BT_FLAG_HOST_ONLY runtimes (-EPERM else). */
+ * the next call on rt).  Only for BT_FLAG_HOST_ONLY runtimes (-EPERM else),
+ * where a registered vector's host address stands in for its device replica
+ * (operand base addresses; nothing is dereferenced). */
 int bt_dag_snapshot(bt_runtime *rt, bt_dag_view *out);
 
 /* Per-unit device timestamps of the last completed epoch (BT_FLAG_TIMESTAMPS):

@@ -18,11 +18,12 @@ import numpy as np
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BT_LIB_PATH") or os.path.join(_PKG, "libbtask.so")   # override: experiments only
 
-BT_ABI_VERSION = 4
+BT_ABI_VERSION = 5
 BT_R, BT_W, BT_RW = 1, 2, 3
 BT_CL_SCAL, BT_CL_AXPY, BT_CL_COPY = 1, 2, 3
 BT_FLAG_NO_FUSION, BT_FLAG_HOST_ONLY, BT_FLAG_TIMESTAMPS, BT_FLAG_SYNC_EPOCH, BT_FLAG_NO_STREAM = 1, 2, 4, 8, 16
 BT_FLAG_PRIORITY = 32
+BT_DAG_WHOLE_PREDS = 1   # bt_dag_view.item_flags
 BT_FLAG_KERNEL_SW, BT_FLAG_KERNEL_RW, BT_FLAG_KERNEL_WQ = 1 << 8, 1 << 9, 1 << 10
 
 bt_handle = ctypes.c_uint64
@@ -56,7 +57,7 @@ class bt_dag_view(ctypes.Structure):
                 ("task_item", ctypes.POINTER(ctypes.c_uint32)), ("task_pos", ctypes.POINTER(ctypes.c_uint32)),
                 ("item_kind", ctypes.POINTER(ctypes.c_uint8)), ("item_k", ctypes.POINTER(ctypes.c_uint32)),
                 ("item_npred", ctypes.POINTER(ctypes.c_uint32)), ("succ_off", ctypes.POINTER(ctypes.c_uint32)),
-                ("succ", ctypes.POINTER(ctypes.c_uint32))]
+                ("succ", ctypes.POINTER(ctypes.c_uint32)), ("item_flags", ctypes.POINTER(ctypes.c_uint8))]
 
 
 if not os.path.exists(LIB_PATH):
@@ -270,7 +271,7 @@ class Runtime:
                 "task_item": arr(v.task_item, n, np.uint32), "task_pos": arr(v.task_pos, n, np.uint32),
                 "item_kind": arr(v.item_kind, m, np.uint8), "item_k": arr(v.item_k, m, np.uint32),
                 "item_npred": arr(v.item_npred, m, np.uint32), "succ_off": arr(v.succ_off, m + 1, np.uint32),
-                "succ": arr(v.succ, e, np.uint32)}
+                "succ": arr(v.succ, e, np.uint32), "item_flags": arr(v.item_flags, m, np.uint8)}
 
     def trace(self):
         t = ctypes.POINTER(ctypes.c_uint64)()

@@ -316,6 +316,7 @@ struct bt_runtime {
   // host-only snapshot storage
   std::vector<uint8_t> snap_kind;
   std::vector<uint32_t> snap_k, snap_npred, snap_off, snap_succ;
+  std::vector<uint8_t> snap_flags;
   std::vector<uint32_t> snap_task_item, snap_task_pos;
 
   // last trace
@@ -1684,6 +1685,10 @@ int bt_vector_data_register(bt_runtime *rt, bt_handle *out, int home_node, void 
   }
   float *dptr = nullptr;
   bool owns = false;
+  // host-only (analysis) runtimes: the host address stands in for the replica,
+  // so operand base addresses in the DAG are distinct per range (never
+  // dereferenced: nothing executes)
+  if (rt->host_only && ptr) dptr = static_cast<float *>(ptr);
   if (!rt->host_only && ptr) {
     cudaSetDevice(rt->device);
     if (home_node == 1) {
@@ -2760,6 +2765,7 @@ int bt_dag_snapshot(bt_runtime *rt, bt_dag_view *out) {
   rt->snap_kind.resize(N);
   rt->snap_k.resize(N);
   rt->snap_npred.resize(N);
+  rt->snap_flags.resize(N);
   rt->snap_off.resize(N + 1);
   rt->snap_succ.resize(B.edges.size());
   uint32_t acc = 0;
@@ -2769,6 +2775,7 @@ int bt_dag_snapshot(bt_runtime *rt, bt_dag_view *out) {
     rt->snap_kind[i] = (uint8_t)B.items[i].kind;
     rt->snap_k[i] = B.items[i].k;
     rt->snap_npred[i] = B.items[i].npred;
+    rt->snap_flags[i] = B.items[i].item_deps ? (uint8_t)BT_DAG_WHOLE_PREDS : (uint8_t)0;
   }
   rt->snap_off[N] = acc;
   rt->cursor.assign(rt->snap_off.begin(), rt->snap_off.end() - 1);
@@ -2785,6 +2792,7 @@ int bt_dag_snapshot(bt_runtime *rt, bt_dag_view *out) {
   out->item_npred = rt->snap_npred.data();
   out->succ_off = rt->snap_off.data();
   out->succ = rt->snap_succ.data();
+  out->item_flags = rt->snap_flags.data();
   rt->stats.items += N;
   rt->stats.edges += B.edges.size();
   rt->stats.fused_tasks += B.fused;

@@ -245,6 +245,46 @@ def test_partition_unpartition_dependencies(B):
     assert int(ti[2]) not in R[ti[1]] and int(ti[1]) not in R[ti[2]]
 
 
+def test_whole_predecessor_flags(B):
+    """Chunk-wise release (device_abi.h K_ITEM_DEPS; bt_dag_view.item_flags):
+    an item waits for whole predecessors exactly when some predecessor's
+    operand on the handle it was found through starts at another address --
+    partition-inherited state (a part other than the first, or the parent of a
+    part after unpartition) -- and chunk by chunk otherwise, including across
+    operands of AXPY/COPY on the same handles and through a re-partition that
+    reuses another parent's freed slots."""
+    WHOLE = B.BT_DAG_WHOLE_PREDS
+    n = 12
+    a, b, c = (np.ones(n, np.float32) for _ in range(3))
+    rt = host_rt(B, flags=B.BT_FLAG_NO_FUSION)
+    ha, hb, hc = rt.register_array(a), rt.register_array(b), rt.register_array(c)
+    rt.scal(ha, 2.0)                 # T0
+    rt.axpy(0.5, ha, hb)             # T1: after T0 (a, same base)
+    rt.copy(hb, hc)                  # T2: after T1 (b as T1's y, same base)
+    rt.scal(ha, 3.0)                 # T3: after T0 (WAW) and T1 (WAR), both through a
+    pa = rt.partition(ha, 3)         # parts of 4: part 0 starts at a, parts 1-2 do not
+    rt.scal(pa[0], 5.0)              # T4: after T3 through part 0's inherited state, same base
+    rt.scal(pa[1], 5.0)              # T5: after T3 through part 1's inherited state, another base
+    rt.unpartition(ha)
+    rt.scal(ha, 7.0)                 # T6: after T4 (base a) and T5 (base a + 16 bytes)
+    pc = rt.partition(hc, 3)         # c's parts
+    rt.scal(pc[2], 1.5)              # T7: after T2 (base c) through part 2: another base
+    rt.unpartition(hc)
+    pb = rt.partition(hb, 3)         # reuses c's freed 3-part slots: b's part 2 has c's part 2's slot id
+    rt.scal(pb[2], 1.5)              # T8: after T1/T2 on b (bases b) through part 2 of b: another base
+    rt.scal(pb[2], 2.5)              # T9: after T8, same part: same base
+    snap = rt.dag_snapshot()
+    rt.unpartition(hb)
+    for h in (ha, hb, hc):
+        rt.unregister(h)
+    rt.close()
+    ti, fl, npred = snap["task_item"], snap["item_flags"], snap["item_npred"]
+    assert snap["nitems"] == 10 and fl.shape == (10,)
+    whole = [bool(fl[ti[t]] & WHOLE) for t in range(10)]
+    assert whole == [False, False, False, False, False, True, True, True, True, False], whole
+    assert [int(npred[ti[t]]) for t in (0, 1, 2, 3, 4, 5, 9)] == [0, 1, 1, 2, 1, 1, 1]
+
+
 def test_error_conventions(B):
     rt = host_rt(B)
     x = np.ones(16, np.float32)
