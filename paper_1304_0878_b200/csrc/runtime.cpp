@@ -955,6 +955,9 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
   // large units (C2 unfused: 0.25 vs 0.28 ms on "rw").
   if (E > 0 && !dr && tot.single * 2 < N)
     kernel = U0 >= 2ull * (uint64_t)rt->grid_max ? 1 : prefetch ? 3 : 0;
+  // BT_FLAG_PRIORITY: the priority levels live in the "sw" bodies ("swp"), so
+  // a runtime that asks for them keeps its DAG epochs there
+  if (E > 0 && !dr && (rt->cfg.flags & BT_FLAG_PRIORITY) && kernel == 1) kernel = prefetch ? 3 : 0;
   if (kv) kernel = kv[0] == 'w' ? 2 : kv[0] == 'r' ? 1 : prefetch ? 3 : 0;
   if (rt->cfg.flags & BT_FLAG_KERNEL_SW) kernel = prefetch ? 3 : 0;
   if (rt->cfg.flags & BT_FLAG_KERNEL_RW) kernel = 1;
