@@ -366,6 +366,31 @@ def test_batch_equals_single_inserts(B):
             assert np.array_equal(a[k], b[k]), k
 
 
+def test_batch_marshalling(B):
+    """insert_batch passes the arrays' addresses as they are (strided or
+    mistyped inputs are converted first) and rejects arrays of different
+    lengths before the call (the C ABI takes one count for all of them)."""
+    x = np.ones(64, np.float32)
+    rt = host_rt(B)
+    h = rt.register_array(x)
+    subs = rt.partition(h, 4)
+    t = W._tasks(8)
+    t["codelet"] = W.SCAL
+    t["scalar"] = np.float32(2.0)
+    hs = np.asarray(subs, np.uint64)[np.arange(8) % 4]
+    assert rt.insert_batch(t["codelet"], t["scalar"], hs) == 8      # strided fields of a structured array
+    assert rt.insert_batch(np.ones(8, np.int64), np.ones(8), hs.astype(np.int64)) == 8   # converted
+    with pytest.raises(ValueError):
+        rt.insert_batch(np.ones(8, np.int32), np.ones(7, np.float32), hs)
+    with pytest.raises(ValueError):
+        rt.insert_batch(np.ones(8, np.int32), np.ones(8, np.float32), hs, hs[:5])
+    snap = rt.dag_snapshot()
+    assert snap["ntasks"] == 16
+    rt.unpartition(h)
+    rt.unregister(h)
+    rt.close()
+
+
 def test_rank_filter_and_cross_rank_error(B):
     x = np.ones(64, np.float32)
     y = np.ones(64, np.float32)
