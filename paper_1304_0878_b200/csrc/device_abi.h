@@ -142,16 +142,21 @@ struct EpochArgs {
 constexpr int kDirectItemsSmall = 16, kDirectFactorsSmall = 256;
 constexpr int kDirectItems = 512;       // items per direct launch (at most)
 constexpr int kDirectFactors = 1024;    // distinct chained factors per direct launch (at most)
+// A group of items with the same kind, length, factors / scalar whose operands
+// advance by one stride (C2's 256 tiles x 16 sweeps: ONE group): items
+// first .. (the next group's first) - 1, item first + j at x + j * stride
+// (y + j * stride).  Groups keep the launch's parameter block small.
 struct DirectItem {
-  uint64_t x, y, n;   // as DItem
+  uint64_t x, y, n;   // as DItem (the group's first item)
   uint32_t kind;      // K_SCAL / K_AXPY / K_COPY
   uint32_t k;         // SCAL: chained factors
   uint32_t arg;       // SCAL: offset of its factors in DirectArgs::factors; AXPY: float bits of a
-  uint32_t pad;
+  uint32_t first;     // index of the group's first item (groups in item order)
+  uint64_t stride;    // bytes from one item's operands to the next one's
 };
 template <int NI, int NF>
 struct DirectArgsT {
-  uint32_t nitems;
+  uint32_t nitems;    // groups
   uint32_t chunk;     // elements per CTA (grid.x covers the largest item; grid.y = items)
   DirectItem items[NI];
   float factors[NF];

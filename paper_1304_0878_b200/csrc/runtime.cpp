@@ -36,7 +36,7 @@ namespace bt {
 cudaError_t launch_epoch(const EpochArgs &args, int grid, cudaStream_t stream, int kernel);
 cudaError_t launch_stream(StreamCtl *ctl, uint64_t watchdog_ns, uint64_t quiesce_ns, int grid, cudaStream_t stream,
                           bool prefetch, bool resume);
-cudaError_t launch_direct(const DirectArgs &args, unsigned grid_x, cudaStream_t stream);
+cudaError_t launch_direct(const DirectArgs &args, unsigned grid_x, unsigned nall, cudaStream_t stream);
 cudaError_t scheduler_occupancy(int *blocks_per_sm, int *block);
 cudaError_t scheduler_occupancy_wq(int *blocks_per_sm, int *block);
 cudaError_t launch_stage(void *dst, const void *src_mapped, size_t bytes, unsigned long long *q_empty, size_t nq,
@@ -1347,33 +1347,54 @@ int flush_epoch(bt_runtime *rt, cudaStream_t stream = nullptr, const DirectRound
          (unsigned long long)rt->ep_seq + 1, (unsigned long long)U, kernel, kgrid, (void *)stream, (int)direct);
   if (direct) {
     DirectArgs da{};
-    da.nitems = (uint32_t)N;
     da.chunk = 16384;
-    uint32_t fo = 0, prev_fo = 0;
+    uint32_t fo = 0, prev_fo = 0, ng = 0;
     for (size_t i = 0; i < N; ++i) {
       const HItem &it = B.items[i];
-      DirectItem &di2 = da.items[i];
+      DirectItem di2{};
       di2.x = it.x;
       di2.y = it.y;
       di2.n = it.n;
       di2.kind = it.kind;
       di2.k = it.k;
+      di2.first = (uint32_t)i;
       if (it.kind == K_SCAL) {
         if (it.k == 1 || !rt->cursor[i]) {   // rt->cursor[i] == 1: same list as the previous k > 1 item
-          memcpy(&da.factors[fo], B.factors(it), 4ull * it.k);
-          if (it.k > 1) prev_fo = fo;
-          di2.arg = fo;
-          fo += it.k;
+          if (it.k == 1 && ng && da.items[ng - 1].kind == K_SCAL && da.items[ng - 1].k == 1 &&
+              memcmp(&da.factors[da.items[ng - 1].arg], B.factors(it), 4) == 0) {
+            di2.arg = da.items[ng - 1].arg;   // the same single factor: joinable with the previous group
+          } else {
+            memcpy(&da.factors[fo], B.factors(it), 4ull * it.k);
+            if (it.k > 1) prev_fo = fo;
+            di2.arg = fo;
+            fo += it.k;
+          }
         } else {
           di2.arg = prev_fo;
         }
       } else {
         di2.arg = it.arg;
       }
+      // join the previous group: same kind, length, factors / scalar, operands
+      // one constant stride on (the first join fixes the stride)
+      if (ng) {
+        DirectItem &g = da.items[ng - 1];
+        const uint64_t cnt = i - g.first;   // items in g so far
+        const uint64_t dx = it.x - g.x, dy = it.y - g.y;
+        const bool same = g.kind == di2.kind && g.k == di2.k && g.arg == di2.arg && g.n == di2.n;
+        const bool stride_ok = dx % cnt == 0 && (cnt == 1 || dx / cnt == g.stride) &&
+                               (it.kind == K_SCAL || dy == dx) && it.x > g.x;
+        if (same && stride_ok) {
+          g.stride = dx / cnt;
+          continue;
+        }
+      }
+      da.items[ng++] = di2;
     }
+    da.nitems = ng;
     rt->stats.grid = (uint32_t)((max_n + da.chunk - 1) / da.chunk);
     rt->stats.block = 256;
-    CUDA_TRY(rt, launch_direct(da, (unsigned)((max_n + da.chunk - 1) / da.chunk), stream));
+    CUDA_TRY(rt, launch_direct(da, (unsigned)((max_n + da.chunk - 1) / da.chunk), (unsigned)N, stream));
   } else {
     CUDA_TRY(rt, launch_epoch(a, kgrid, stream, kernel));
   }

@@ -1992,7 +1992,17 @@ cudaError_t launch_stream(StreamCtl *ctl, uint64_t watchdog_ns, uint64_t quiesce
 template <class Args>
 __global__ void __launch_bounds__(256) direct_kernel(const __grid_constant__ Args p) {
   __shared__ __align__(16) float sf[sizeof(p.factors) / sizeof(float)];
-  const DirectItem &it = p.items[blockIdx.y];
+  // item blockIdx.y's group: the last one whose first item is <= it
+  uint32_t g0 = 0, g1 = p.nitems - 1;
+  while (g0 < g1) {
+    const uint32_t mid = (g0 + g1 + 1) >> 1;
+    if (p.items[mid].first <= blockIdx.y) g0 = mid;
+    else g1 = mid - 1;
+  }
+  DirectItem it = p.items[g0];
+  const uint64_t step = (uint64_t)(blockIdx.y - it.first) * it.stride;
+  it.x += step;
+  if (it.kind != K_SCAL) it.y += step;
   const uint64_t lo = (uint64_t)blockIdx.x * p.chunk;
   if (lo >= it.n) return;
   const uint64_t n = min(it.n - lo, (uint64_t)p.chunk);
@@ -2020,7 +2030,7 @@ __global__ void __launch_bounds__(256) direct_kernel(const __grid_constant__ Arg
 // The smallest parameter block that holds the epoch (the launch copies the
 // whole block: C2's 256 items in the 24.6 KB block cost ~20 us of launch).
 template <class Small>
-bool launch_direct_as(const DirectArgs &args, uint32_t nf, unsigned grid_x, cudaStream_t stream) {
+bool launch_direct_as(const DirectArgs &args, uint32_t nf, unsigned grid_x, unsigned nall, cudaStream_t stream) {
   constexpr uint32_t kI = sizeof(Small::items) / sizeof(DirectItem), kF = sizeof(Small::factors) / sizeof(float);
   if (args.nitems > kI || nf > kF) return false;
   Small sm;
@@ -2028,18 +2038,19 @@ bool launch_direct_as(const DirectArgs &args, uint32_t nf, unsigned grid_x, cuda
   sm.chunk = args.chunk;
   memcpy(sm.items, args.items, sizeof(DirectItem) * args.nitems);
   memcpy(sm.factors, args.factors, 4 * nf);
-  direct_kernel<Small><<<dim3(grid_x, args.nitems), 256, 0, stream>>>(sm);
+  direct_kernel<Small><<<dim3(grid_x, nall), 256, 0, stream>>>(sm);
   return true;
 }
 
-cudaError_t launch_direct(const DirectArgs &args, unsigned grid_x, cudaStream_t stream) {
+// nall: items (grid.y); args.nitems: their groups
+cudaError_t launch_direct(const DirectArgs &args, unsigned grid_x, unsigned nall, cudaStream_t stream) {
   uint32_t nf = 0;   // factors used
   for (uint32_t i = 0; i < args.nitems; ++i)
     if (args.items[i].kind == K_SCAL) nf = max(nf, args.items[i].arg + args.items[i].k);
-  if (!launch_direct_as<DirectArgsSmall>(args, nf, grid_x, stream) &&
-      !launch_direct_as<DirectArgsT<64, 256>>(args, nf, grid_x, stream) &&
-      !launch_direct_as<DirectArgsT<256, 256>>(args, nf, grid_x, stream))
-    direct_kernel<DirectArgs><<<dim3(grid_x, args.nitems), 256, 0, stream>>>(args);
+  if (!launch_direct_as<DirectArgsSmall>(args, nf, grid_x, nall, stream) &&
+      !launch_direct_as<DirectArgsT<64, 256>>(args, nf, grid_x, nall, stream) &&
+      !launch_direct_as<DirectArgsT<256, 256>>(args, nf, grid_x, nall, stream))
+    direct_kernel<DirectArgs><<<dim3(grid_x, nall), 256, 0, stream>>>(args);
   return cudaGetLastError();
 }
 

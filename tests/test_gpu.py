@@ -64,6 +64,29 @@ def test_direct_launch(B, seed):
     assert st["kernel_launches"] == 1 and st["block"] == 256, st
 
 
+def test_direct_launch_groups(B):
+    """A direct launch groups items of the same kind, length and factors whose
+    operands advance by one stride (device_abi.h DirectItem): ragged tiles
+    (two lengths: two groups), AXPY with x and y advancing together, COPY in
+    reverse tile order (negative stride: no group), single factors that
+    alternate (no group) and repeat (a group) -- one epoch, one launch,
+    bit-exact."""
+    rng = np.random.default_rng(W.SEED_BASE + 141)
+    n, T = 1000, 7                                   # tiles of 143 (x6) and 142
+    bufs = [W.unit_interval_floats(rng, n) for _ in range(6)]
+    rows = [(W.SCAL, 1.5, 0, t, -1, -1) for t in range(T)]
+    rows += [(W.AXPY, 0.25, 1, t, 2, t) for t in range(T)]
+    rows += [(W.COPY, 0, 3, t, 4, t) for t in reversed(range(T))]
+    rows += [(W.SCAL, (0.75, -2.0)[t % 2], 5, t, -1, -1) for t in range(4)]
+    rows += [(W.SCAL, 3.0, 5, t, -1, -1) for t in range(4, T)]
+    t = W._tasks(len(rows))
+    for i, r in enumerate(rows):
+        t[i] = r
+    p = W.Program(bufs, [T] * 6, t, name="direct launch groups")
+    st = compare_program(p)
+    assert st["kernel_launches"] == 1 and st["block"] == 256 and st["items"] == len(rows), st
+
+
 def test_c1_paper_example(B):
     from tests.golden import load
     pins = load("scal_pins.txt")
