@@ -1999,28 +1999,26 @@ __global__ void __launch_bounds__(256) direct_kernel(const __grid_constant__ Arg
     if (p.items[mid].first <= blockIdx.y) g0 = mid;
     else g1 = mid - 1;
   }
-  DirectItem it = p.items[g0];
+  const DirectItem &it = p.items[g0];   // read in place (parameter space): registers for the bodies
   const uint64_t step = (uint64_t)(blockIdx.y - it.first) * it.stride;
-  it.x += step;
-  if (it.kind != K_SCAL) it.y += step;
   const uint64_t lo = (uint64_t)blockIdx.x * p.chunk;
   if (lo >= it.n) return;
   const uint64_t n = min(it.n - lo, (uint64_t)p.chunk);
+  float *const x = reinterpret_cast<float *>(it.x + step) + lo;
   const int tid = threadIdx.x;
   switch (it.kind) {
     case K_SCAL:
       for (uint32_t j = tid; j < it.k; j += blockDim.x) sf[j] = p.factors[it.arg + j];
       __syncthreads();
       // short chains are HBM-bound: keep the next step's loads in flight (as "sws")
-      if (it.k < 32) scal_range_pf<2, 256>(reinterpret_cast<float *>(it.x) + lo, n, sf, it.k, tid);
-      else scal_range<4, 256>(reinterpret_cast<float *>(it.x) + lo, n, sf, it.k, tid);
+      if (it.k < 32) scal_range_pf<2, 256>(x, n, sf, it.k, tid);
+      else scal_range<4, 256>(x, n, sf, it.k, tid);
       break;
     case K_AXPY:
-      axpy_range<256>(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, n,
-                      __uint_as_float(it.arg), tid);
+      axpy_range<256>(x, reinterpret_cast<float *>(it.y + step) + lo, n, __uint_as_float(it.arg), tid);
       break;
     case K_COPY:
-      copy_range<256>(reinterpret_cast<const float *>(it.x) + lo, reinterpret_cast<float *>(it.y) + lo, n, tid);
+      copy_range<256>(x, reinterpret_cast<float *>(it.y + step) + lo, n, tid);
       break;
     default:
       break;
