@@ -87,6 +87,35 @@ def test_direct_launch_groups(B):
     assert st["kernel_launches"] == 1 and st["block"] == 256 and st["items"] == len(rows), st
 
 
+@pytest.mark.parametrize("seed", range(8))
+def test_direct_launch_groups_random(B, seed):
+    """Random epochs of independent tasks (each tile written once, sources
+    never written): tiles in random order and random subsets, factors from a
+    small set, AXPY/COPY between equally partitioned buffers, ragged tile
+    lengths -- item groups form and break at random; one direct launch each,
+    bit-exact."""
+    rng = np.random.default_rng(W.SEED_BASE + 150 + seed)
+    for rep in range(6):
+        n = int(rng.integers(40, 3000))
+        T = int(rng.integers(2, 40))
+        bufs = [W.unit_interval_floats(rng, n) for _ in range(6)]
+        rows = []
+        for b in (0, 1):                                        # SCAL targets
+            for t in rng.permutation(T)[: int(rng.integers(1, T + 1))]:
+                rows.append((W.SCAL, float(rng.choice([0.5, 1.25, -3.0])), b, int(t), -1, -1))
+        for t in rng.permutation(T)[: int(rng.integers(1, T + 1))]:
+            rows.append((W.AXPY, float(rng.choice([0.25, -0.75])), 2, int(t), 3, int(t)))
+        for t in np.sort(rng.permutation(T)[: int(rng.integers(1, T + 1))]):
+            rows.append((W.COPY, 0.0, 4, int(t), 5, int(t)))
+        order = rng.permutation(len(rows)) if rng.random() < 0.3 else np.arange(len(rows))
+        t = W._tasks(len(rows))
+        for i, j in enumerate(order):
+            t[i] = rows[j]
+        p = W.Program(bufs, [T] * 6, t, name=f"direct groups seed {seed} rep {rep}")
+        st = compare_program(p)
+        assert st["kernel_launches"] == 1 and st["block"] == 256, st
+
+
 def test_c1_paper_example(B):
     from tests.golden import load
     pins = load("scal_pins.txt")
